@@ -1,0 +1,188 @@
+/*
+ * pfc.h — C-ABI of the B200-native Partial FC layer (arXiv 2010.05222, /root/reference/PAPER.md).
+ *
+ * One context per process / rank / GPU. The layer owns one contiguous shard of the class-centre matrix W
+ * ("partition W into k sub-matrices w of size d x C/k and place the i-th on the i-th GPU", PAPER.md:102;
+ * "evenly divided ... according to the order") together with its momentum buffer V
+ * ("each parameter will occupy 12 bytes, as we use momentum SGD").
+ *
+ * Conventions for every entry point
+ *   - Pointers named *_dev are device pointers on cfg.device; *_host are host pointers. All are owned by
+ *     the caller and must stay valid until the work enqueued on `stream` has completed.
+ *   - `stream` is a cudaStream_t passed as void*. NULL means the legacy default stream.
+ *     Work is enqueued asynchronously; no entry point of the hot path synchronises the host.
+ *   - Layouts are row-major, dense: x is [B][d] float32, grad_x is [B][d] float32, labels is [B] int64,
+ *     W and V are [C_local][d] float32 (row j = class centre a_i + j).
+ *   - Collective contract (world_size > 1): every rank calls the hot-path entry points in the same order
+ *     with the same B (Alg.1 is a collective program).
+ *   - Host-detectable errors are returned synchronously and leave the context unchanged. Errors found on
+ *     the device (label outside [0, C), zero-norm row, non-finite loss) set a sticky device word that is
+ *     reported by the next synchronising call (pfc_step, pfc_get_*, pfc_check) — or at once when the
+ *     environment variable PFC_SYNC_CHECK=1 is set.
+ *   - Not re-entrant: one host thread per context.
+ */
+#ifndef PFC_H_
+#define PFC_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  PFC_OK = 0,
+  PFC_ERR_CONFIG = 1,      /* invalid pfc_config (C < world_size, r outside (0,1], bad margin, d % 128 != 0 ...) */
+  PFC_ERR_CONTRACT = 2,    /* NULL / misaligned pointer, wrong call order (pfc_step without forward_backward) */
+  PFC_ERR_DATA = 3,        /* a label outside [0, C) (device-detected) */
+  PFC_ERR_DEGENERATE = 4,  /* a zero-norm feature or class-centre row (norm clamped to 1e-12, reported) */
+  PFC_ERR_NUMERIC = 5,     /* non-finite loss */
+  PFC_ERR_CUDA = 6,        /* CUDA runtime error (message in pfc_last_error) */
+  PFC_ERR_NCCL = 7,        /* NCCL error */
+  PFC_ERR_OOM = 8          /* device allocation failed */
+} pfc_status;
+
+typedef enum { PFC_MARGIN_NONE = 0, PFC_MARGIN_ARCFACE = 1, PFC_MARGIN_COSFACE = 2 } pfc_margin;
+
+/* Arithmetic of the three contractions. PFC_BF16: bf16 operands on the tcgen05 tensor cores with fp32
+ * accumulation, cosines stored as fp16, target cosine refined in fp32. PFC_FP32: fp32 FFMA throughout. */
+typedef enum { PFC_FP32 = 0, PFC_BF16 = 1 } pfc_precision;
+
+/* How the world_size ranks exchange data.
+ * PFC_COMM_NCCL: one process per GPU, NCCL all-gather / all-reduce / reduce-scatter over NVLink.
+ * PFC_COMM_LOOPBACK: all world_size contexts live in ONE process (any devices, typically one GPU) and are
+ *   driven together by pfc_group_forward_backward; the collectives are rank-ordered device copies and
+ *   rank-ascending sums (the single-matrix form of Alg.1). Used for multi-rank parity on one GPU and for the
+ *   per-rank solo timing of the scaling study. pfc_forward_backward rejects such a context when world_size > 1. */
+typedef enum { PFC_COMM_NCCL = 0, PFC_COMM_LOOPBACK = 1 } pfc_comm_mode;
+
+typedef struct {
+  int64_t num_classes;   /* C >= world_size      */
+  int32_t dim;           /* d, multiple of 128 in [128, 1024] (512 in the paper)      */
+  int32_t batch;         /* N = B, features per rank, equal on all ranks, >= 1      */
+  double sample_rate;    /* r in (0, 1]      */
+  float scale;           /* s > 0 (64 in the paper)      */
+  int32_t margin_type;   /* pfc_margin      */
+  float margin;          /* ArcFace 0 <= m < pi/2 (0.5); CosFace 0 <= m < 1 (0.4)      */
+  float momentum;        /* mu in [0, 1)      */
+  float weight_decay;    /* lambda >= 0 (the paper is silent; explicit)                                 */
+  int32_t precision;     /* pfc_precision                                                               */
+  uint64_t seed;         /* keys the Philox negative sampler (R2)                             */
+  int32_t rank;          /* i in [0, world_size)                                                        */
+  int32_t world_size;    /* k >= 1                                                                      */
+  int32_t device;        /* CUDA device ordinal for this rank                                            */
+  const void* nccl_unique_id; /* 128-byte ncclUniqueId from pfc_get_unique_id on rank 0, broadcast by the
+                                 caller (e.g. over torch.distributed); required iff world_size > 1 and
+                                 comm_mode == PFC_COMM_NCCL                                               */
+  int32_t comm_mode;     /* pfc_comm_mode                                                                */
+} pfc_config;
+
+typedef struct pfc_ctx pfc_ctx;
+
+/* ------------------------------------------------------------------------------------------------------
+ * Lifecycle
+ * ---------------------------------------------------------------------------------------------------- */
+
+/* Writes a fresh 128-byte NCCL unique id into id_out (host buffer of >= 128 bytes). Call on rank 0 only. */
+pfc_status pfc_get_unique_id(void* id_out_host);
+
+/* Validates cfg, selects cfg->device, computes the shard [a_i, a_i + C_local) (balanced, first C mod k
+ * ranks get one more row; R6), allocates W and V (zero-filled) and the step workspace, and
+ * creates the NCCL communicator when world_size > 1. *out receives the context (NULL on error). */
+pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out);
+
+/* Frees all device memory and the communicator. NULL is a no-op. */
+pfc_status pfc_destroy(pfc_ctx* ctx);
+
+/* Text of the last error of ctx (or of the last failed pfc_init when ctx is NULL). Never NULL. */
+const char* pfc_last_error(const pfc_ctx* ctx);
+
+/* ------------------------------------------------------------------------------------------------------
+ * Hot path
+ * ---------------------------------------------------------------------------------------------------- */
+
+/* One forward + backward pass of the sampled model-parallel margin-softmax layer on this rank
+ * (Alg.1, with the PPRN sampler of PAPER.md:292-316 and Eq.9):
+ *   X = allgather(x / ||x||) and labels; P_i = labels in this shard; k_i = max(ceil(r C_local), |P_i|);
+ *   the k_i - |P_i| negatives with the smallest Philox keys (R1-R4); W_s = normalised sampled
+ *   rows; logits = s * X W_s^T with the margin at each row's own class; global softmax over
+ *   the union of all ranks' samples via all-reduce (Alg.1 L6-7); loss = mean over the global batch
+ *   M = k B of the cross-entropy (Eq.5); grad_x = d loss / d x for this rank's B rows (Alg.1 L12-13);
+ *   the gradient of the sampled W rows is kept for pfc_step.
+ * x_dev      [B][d] float32 features of this rank (any norm > 0).
+ * labels_dev [B] int64 global class ids in [0, C).
+ * grad_x_dev [B][d] float32 output; may alias nothing else.
+ * loss_dev   float32 scalar output (same value on every rank) or NULL.
+ * Increments the context's step counter, which keys the sampler of the next call. */
+pfc_status pfc_forward_backward(pfc_ctx* ctx, const float* x_dev, const int64_t* labels_dev,
+                                float* grad_x_dev, float* loss_dev, void* stream);
+
+/* One forward + backward of ALL ranks of a loopback group (comm_mode == PFC_COMM_LOOPBACK): ctxs[i] is rank
+ * i (n == world_size, same config otherwise); x_dev[i], labels_dev[i], grad_x_dev[i] as in
+ * pfc_forward_backward for rank i. loss_dev (or NULL) receives the loss. All work goes to `stream`. */
+pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* const* x_dev,
+                                      const int64_t* const* labels_dev, float* const* grad_x_dev, float* loss_dev,
+                                      void* stream);
+
+/* The same pass with HOST buffers: copies x and labels host->device and grad_x, loss device->host on
+ * `stream` (pinned host memory gives asynchronous copies), then synchronises `stream`. loss_host may be
+ * NULL. Used for the end-to-end measurement. */
+pfc_status pfc_forward_backward_host(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host,
+                                     float* grad_x_host, float* loss_host, void* stream);
+
+/* Lazy momentum-SGD update of the rows sampled by the last pfc_forward_backward (DESIGN.md
+ * R15): g = (dw_hat - w_hat (w_hat . dw_hat)) / ||w||; v <- mu v + g + lambda w; w <- w - lr v.
+ * Rows not sampled are untouched. Returns PFC_ERR_CONTRACT if no forward_backward preceded it or it was
+ * already applied. Reports sticky device errors (synchronises `stream`). */
+pfc_status pfc_step(pfc_ctx* ctx, float lr, void* stream);
+
+/* ------------------------------------------------------------------------------------------------------
+ * Introspection, state and parity (synchronising; not on the hot path)
+ * ---------------------------------------------------------------------------------------------------- */
+
+/* Global start a_i and row count C_local of this rank's shard. */
+pfc_status pfc_shard_range(const pfc_ctx* ctx, int64_t* start, int64_t* count);
+
+/* Sizes: M = world_size * B, k_max = max(ceil(r C_local), min(M, C_local)) (the workspace bound). */
+pfc_status pfc_sizes(const pfc_ctx* ctx, int64_t* M, int64_t* k_max);
+
+/* Device pointers to the library-owned W and V shards ([C_local][d] float32). The caller may read or
+ * write them between calls (stream-ordered on the stream it uses). */
+pfc_status pfc_param_ptrs(pfc_ctx* ctx, float** W_dev, float** V_dev);
+
+/* Sampled global class ids of the last forward_backward, ascending (R4), and k_i.
+ * idx_host has room for `capacity` entries (>= k_i, else PFC_ERR_CONTRACT with *k_out set). */
+pfc_status pfc_get_sampled(pfc_ctx* ctx, int64_t* idx_host, int64_t capacity, int64_t* k_out);
+
+/* Gradient of the loss w.r.t. the raw W rows of the sampled set of the last forward_backward,
+ * [k_i][d] float32 in the order of pfc_get_sampled. Must be called before pfc_step. */
+pfc_status pfc_get_sampled_grad(pfc_ctx* ctx, float* dW_host, int64_t capacity_rows);
+
+/* Per-row log-sum-exp over the global sampled set (M floats) of the last forward_backward. */
+pfc_status pfc_get_lse(pfc_ctx* ctx, float* lse_host, int64_t capacity);
+
+/* Step counter (number of forward_backward calls since init / set). */
+pfc_status pfc_get_step(const pfc_ctx* ctx, uint64_t* step);
+pfc_status pfc_set_step(pfc_ctx* ctx, uint64_t step);
+
+/* Synchronises the context's last stream and returns the sticky device error (PFC_OK if none). */
+pfc_status pfc_check(pfc_ctx* ctx);
+
+/* Standalone PPRN sampler (K2-K4) of shard `rank` of `world_size` (no context): labels_dev [M] int64 global
+ * labels of the global batch (device), idx_dev receives the k_i sampled global ids ascending (device, room for
+ * max(ceil(r C_local), min(M, C_local)) entries), *k_out = k_i (host; synchronises `stream`).
+ * Same arithmetic as inside pfc_forward_backward with the given `step`. */
+pfc_status pfc_sample_shard(int64_t num_classes, int32_t world_size, int32_t rank, double sample_rate, uint64_t seed,
+                            uint64_t step, const int64_t* labels_dev, int32_t M, int64_t* idx_dev, int64_t* k_out,
+                            void* stream);
+
+/* Number of kernels this library launched since init (each launch counted once). */
+int64_t pfc_launch_count(const pfc_ctx* ctx);
+
+/* Library version string. */
+const char* pfc_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFC_H_ */

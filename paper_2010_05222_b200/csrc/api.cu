@@ -1,0 +1,641 @@
+// C-ABI (include/pfc.h) and the stream-ordered step orchestrator.
+//
+// Per pfc_forward_backward on rank i (all on the caller's stream, no host sync):
+//   K1 normalize_x -> [NCCL all-gather X_hat, Y] -> K1b X_hat->bf16 -> K2..K4 sampler -> K5 gather W_s
+//   -> K5b target cos -> K6 logits GEMM (+margin, scale, per-tile max/sum-exp) -> K7 row combine
+//   -> [NCCL all-reduce MAX] -> prep -> [NCCL all-reduce SUM] -> finalize (LSE, loss)
+//   -> K8 softmax grad -> K9 dX GEMM -> [NCCL reduce-scatter] -> K10 x-norm backward -> K11 dW GEMM
+// pfc_step: K12 lazy momentum SGD on the sampled rows.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "pfc_internal.cuh"
+
+using namespace pfc;
+
+static thread_local std::string g_init_error;
+
+struct pfc_ctx {
+  pfc_config cfg{};
+  Sizes sz{};
+  MarginParams mp{};
+  bool bf16 = false;
+  bool use_tc = false;
+  bool sync_check = false;
+  std::string err;
+  ncclComm_t comm = nullptr;
+  uint64_t step = 0;
+  bool fb_done = false;      // a forward_backward happened and its gradient was not yet applied
+  cudaStream_t last_stream = nullptr;
+  int64_t launches = 0;
+  std::vector<void*> allocs;
+
+  // parameters
+  float* W = nullptr;
+  float* V = nullptr;
+  // features / labels
+  float* xh_local = nullptr;   // B x d
+  float* xnorm = nullptr;      // B
+  float* X32 = nullptr;        // M_pad x d (all-gathered x_hat)
+  int64_t* Y = nullptr;        // M
+  __nv_bfloat16* Xb = nullptr; // M_pad x d
+  // sampler
+  uint32_t* bits = nullptr;
+  uint32_t* keys = nullptr;
+  int* hist = nullptr;
+  int* tile_cnt = nullptr;
+  SamplerState* st = nullptr;
+  int32_t* idx = nullptr;      // k_pad
+  int32_t* tcol = nullptr;     // M
+  // sampled centres
+  void* Ws = nullptr;          // k_pad x d (bf16 or fp32)
+  float* inv_norm = nullptr;   // k_pad
+  float* ct = nullptr;         // M
+  // logits and softmax
+  void* cosv = nullptr;        // M x k_pad (fp16 or fp32)
+  float2* partials = nullptr;  // M x n_ltiles
+  float* rowmax = nullptr;     // M
+  float* gmax = nullptr;       // M
+  float* rowsum = nullptr;     // M
+  float* zt = nullptr;         // M
+  float* red = nullptr;        // M + 1
+  float* lse = nullptr;        // M
+  float* loss_dev = nullptr;   // 1 (scratch when the caller passes NULL)
+  void* G = nullptr;           // M x k_pad (bf16 or fp32)
+  // gradients
+  float* dXh = nullptr;        // M x d
+  float* dxh_local = nullptr;  // B x d (reduce-scatter output)
+  float* split_ws = nullptr;   // split-K partials of the dx GEMM
+  float* dWh = nullptr;        // k_pad x d
+  int* err_dev = nullptr;
+  // host-buffer entry point
+  float* x_in = nullptr;
+  int64_t* y_in = nullptr;
+  float* gx_out = nullptr;
+};
+
+namespace {
+
+pfc_status set_err(pfc_ctx* c, pfc_status s, const std::string& msg) {
+  if (c) c->err = msg; else g_init_error = msg;
+  return s;
+}
+
+#define CUDA_TRY(ctx, expr)                                                                          \
+  do {                                                                                               \
+    cudaError_t e_ = (expr);                                                                         \
+    if (e_ != cudaSuccess)                                                                           \
+      return set_err(ctx, e_ == cudaErrorMemoryAllocation ? PFC_ERR_OOM : PFC_ERR_CUDA,              \
+                     std::string(#expr) + ": " + cudaGetErrorString(e_));                            \
+  } while (0)
+
+#define NCCL_TRY(ctx, expr)                                                                          \
+  do {                                                                                               \
+    ncclResult_t r_ = (expr);                                                                        \
+    if (r_ != ncclSuccess) return set_err(ctx, PFC_ERR_NCCL, std::string(#expr) + ": " + ncclGetErrorString(r_)); \
+  } while (0)
+
+template <typename T>
+pfc_status dalloc(pfc_ctx* c, T** p, size_t bytes) {
+  void* q = nullptr;
+  cudaError_t e = cudaMalloc(&q, std::max<size_t>(bytes, 16));
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return set_err(c, PFC_ERR_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+  }
+  c->allocs.push_back(q);
+  *p = reinterpret_cast<T*>(q);
+  return PFC_OK;
+}
+
+pfc_status device_error(pfc_ctx* c) {
+  int h = 0;
+  CUDA_TRY(c, cudaMemcpy(&h, c->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  if (!h) return PFC_OK;
+  CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(int)));
+  if (h & ERR_DATA) return set_err(c, PFC_ERR_DATA, "a label is outside [0, num_classes)");
+  if (h & ERR_DEGENERATE) return set_err(c, PFC_ERR_DEGENERATE, "a feature or class-centre row has zero norm");
+  if (h & ERR_NUMERIC) return set_err(c, PFC_ERR_NUMERIC, "non-finite loss");
+  return set_err(c, PFC_ERR_CUDA, "internal sampler consistency check failed (selected count != k_i)");
+}
+
+pfc_status validate(const pfc_config* c) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "cfg is NULL");
+  if (c->world_size < 1 || c->rank < 0 || c->rank >= c->world_size)
+    return set_err(nullptr, PFC_ERR_CONFIG, "need 0 <= rank < world_size");
+  if (c->num_classes < c->world_size) return set_err(nullptr, PFC_ERR_CONFIG, "need num_classes >= world_size");
+  if (c->num_classes >= (int64_t(1) << 31) * c->world_size)
+    return set_err(nullptr, PFC_ERR_CONFIG, "shard larger than 2^31 rows");
+  if (c->dim < 128 || c->dim % 128 != 0 || c->dim > 1024)
+    return set_err(nullptr, PFC_ERR_CONFIG, "dim must be a multiple of 128 in [128, 1024]");
+  if (c->batch < 1) return set_err(nullptr, PFC_ERR_CONFIG, "batch must be >= 1");
+  if (!(c->sample_rate > 0.0 && c->sample_rate <= 1.0)) return set_err(nullptr, PFC_ERR_CONFIG, "sample_rate must be in (0, 1]");
+  if (!(c->scale > 0.f)) return set_err(nullptr, PFC_ERR_CONFIG, "scale must be > 0");
+  if (c->margin_type == PFC_MARGIN_ARCFACE && !(c->margin >= 0.f && c->margin < 1.5707963f))
+    return set_err(nullptr, PFC_ERR_CONFIG, "ArcFace margin must be in [0, pi/2)");
+  if (c->margin_type == PFC_MARGIN_COSFACE && !(c->margin >= 0.f && c->margin < 1.f))
+    return set_err(nullptr, PFC_ERR_CONFIG, "CosFace margin must be in [0, 1)");
+  if (c->margin_type < 0 || c->margin_type > 2) return set_err(nullptr, PFC_ERR_CONFIG, "unknown margin_type");
+  if (c->precision != PFC_FP32 && c->precision != PFC_BF16) return set_err(nullptr, PFC_ERR_CONFIG, "unknown precision");
+  if (!(c->momentum >= 0.f && c->momentum < 1.f)) return set_err(nullptr, PFC_ERR_CONFIG, "momentum must be in [0, 1)");
+  if (!(c->weight_decay >= 0.f)) return set_err(nullptr, PFC_ERR_CONFIG, "weight_decay must be >= 0");
+  if (c->comm_mode != PFC_COMM_NCCL && c->comm_mode != PFC_COMM_LOOPBACK)
+    return set_err(nullptr, PFC_ERR_CONFIG, "unknown comm_mode");
+  if (c->comm_mode == PFC_COMM_LOOPBACK && c->world_size > kMaxLoopback)
+    return set_err(nullptr, PFC_ERR_CONFIG, "loopback groups support at most 16 ranks");
+  if (c->world_size > 1 && c->comm_mode == PFC_COMM_NCCL && !c->nccl_unique_id)
+    return set_err(nullptr, PFC_ERR_CONFIG, "world_size > 1 needs nccl_unique_id");
+  if ((int64_t)c->world_size * c->batch > (1 << 24)) return set_err(nullptr, PFC_ERR_CONFIG, "global batch too large");
+  return PFC_OK;
+}
+
+int64_t round_up(int64_t v, int64_t m) { return (v + m - 1) / m * m; }
+
+}  // namespace
+
+extern "C" {
+
+const char* pfc_version(void) { return "pfc-b200 0.1 (sm_100a)"; }
+
+const char* pfc_last_error(const pfc_ctx* ctx) {
+  if (!ctx) return g_init_error.c_str();
+  return ctx->err.c_str();
+}
+
+pfc_status pfc_get_unique_id(void* id_out) {
+  if (!id_out) return set_err(nullptr, PFC_ERR_CONTRACT, "id_out is NULL");
+  ncclUniqueId id;
+  ncclResult_t r = ncclGetUniqueId(&id);
+  if (r != ncclSuccess) return set_err(nullptr, PFC_ERR_NCCL, ncclGetErrorString(r));
+  std::memcpy(id_out, &id, sizeof(id));
+  return PFC_OK;
+}
+
+pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
+  if (!out) return set_err(nullptr, PFC_ERR_CONTRACT, "out is NULL");
+  *out = nullptr;
+  pfc_status v = validate(cfg);
+  if (v != PFC_OK) return v;
+  pfc_ctx* c = new pfc_ctx();
+  c->cfg = *cfg;
+  c->cfg.nccl_unique_id = nullptr;
+  c->bf16 = cfg->precision == PFC_BF16;
+  const char* sc = std::getenv("PFC_SYNC_CHECK");
+  c->sync_check = sc && sc[0] == '1';
+  const char* gb = std::getenv("PFC_GEMM");
+  c->use_tc = c->bf16 && tc_available() && !(gb && std::string(gb) == "simt");
+
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) {
+    delete c;
+    return set_err(nullptr, PFC_ERR_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  }
+
+  Sizes& sz = c->sz;
+  const int64_t C = cfg->num_classes;
+  const int k = cfg->world_size, i = cfg->rank;
+  sz.C = C;
+  sz.world = k;
+  sz.rank = i;
+  sz.C_local = C / k + (i < C % k ? 1 : 0);                 // R6
+  sz.a = (int64_t)i * (C / k) + std::min<int64_t>(i, C % k);
+  sz.d = cfg->dim;
+  sz.B = cfg->batch;
+  sz.M = k * cfg->batch;
+  sz.M_pad = (int)round_up(sz.M, 128);
+  sz.budget = (int64_t)std::ceil((double)cfg->sample_rate * (double)sz.C_local);  // R1 (IEEE double)
+  sz.k_max = std::max<int64_t>(sz.budget, std::min<int64_t>(sz.M, sz.C_local));
+  sz.k_pad = round_up(sz.k_max, kKPad);
+  sz.ltile = c->use_tc ? 128 : 64;
+  sz.n_ltiles = (int)(sz.k_pad / sz.ltile);
+  sz.ntiles_sel = (int)((sz.C_local + kSelTile - 1) / kSelTile);
+
+  MarginParams& mp = c->mp;
+  mp.type = cfg->margin_type;
+  mp.s = cfg->scale;
+  mp.m = cfg->margin;
+  mp.cos_m = (float)std::cos((double)cfg->margin);
+  mp.sin_m = (float)std::sin((double)cfg->margin);
+  mp.th = (float)std::cos(M_PI - (double)cfg->margin);
+  mp.mm = (float)(std::sin((double)cfg->margin) * (double)cfg->margin);
+
+  const size_t d = sz.d, M = sz.M, Mp = sz.M_pad, B = sz.B, kp = sz.k_pad;
+  const size_t esz = c->bf16 ? 2 : 4;
+  pfc_status s = PFC_OK;
+#define ALLOC(p, bytes) \
+  if ((s = dalloc(c, &(p), (bytes))) != PFC_OK) { g_init_error = c->err; pfc_destroy(c); return s; }
+  ALLOC(c->W, (size_t)sz.C_local * d * 4);
+  ALLOC(c->V, (size_t)sz.C_local * d * 4);
+  ALLOC(c->xh_local, B * d * 4);
+  ALLOC(c->xnorm, B * 4);
+  ALLOC(c->X32, Mp * d * 4);
+  ALLOC(c->Y, M * 8);
+  ALLOC(c->Xb, Mp * d * 2);
+  ALLOC(c->bits, ((sz.C_local + 31) / 32) * 4);
+  ALLOC(c->keys, (size_t)sz.C_local * 4);
+  ALLOC(c->hist, 5120 * 4);
+  ALLOC(c->tile_cnt, (size_t)sz.ntiles_sel * 4 * 4);
+  ALLOC(c->st, sizeof(SamplerState));
+  ALLOC(c->idx, kp * 4);
+  ALLOC(c->tcol, M * 4);
+  ALLOC(c->Ws, kp * d * esz);
+  ALLOC(c->inv_norm, kp * 4);
+  ALLOC(c->ct, M * 4);
+  ALLOC(c->cosv, M * kp * esz);
+  ALLOC(c->partials, M * (size_t)sz.n_ltiles * sizeof(float2));
+  ALLOC(c->rowmax, M * 4);
+  ALLOC(c->gmax, M * 4);
+  ALLOC(c->rowsum, M * 4);
+  ALLOC(c->zt, M * 4);
+  ALLOC(c->red, (M + 1) * 4);
+  ALLOC(c->lse, M * 4);
+  ALLOC(c->loss_dev, 16);
+  ALLOC(c->G, M * kp * esz);
+  ALLOC(c->dXh, Mp * d * 4);
+  ALLOC(c->dxh_local, B * d * 4);
+  ALLOC(c->split_ws, (size_t)64 * Mp * d * 4);
+  ALLOC(c->dWh, kp * d * 4);
+  ALLOC(c->err_dev, 16);
+  ALLOC(c->x_in, B * d * 4);
+  ALLOC(c->y_in, B * 8);
+  ALLOC(c->gx_out, B * d * 4);
+#undef ALLOC
+  cudaMemset(c->W, 0, (size_t)sz.C_local * d * 4);
+  cudaMemset(c->V, 0, (size_t)sz.C_local * d * 4);
+  cudaMemset(c->X32, 0, Mp * d * 4);
+  cudaMemset(c->Xb, 0, Mp * d * 2);
+  cudaMemset(c->dXh, 0, Mp * d * 4);
+  cudaMemset(c->err_dev, 0, 16);
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) {
+    std::string m = std::string("init memset: ") + cudaGetErrorString(e);
+    pfc_destroy(c);
+    return set_err(nullptr, PFC_ERR_CUDA, m);
+  }
+  if (k > 1 && cfg->comm_mode == PFC_COMM_NCCL) {
+    ncclUniqueId id;
+    std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+    ncclResult_t r = ncclCommInitRank(&c->comm, k, id, i);
+    if (r != ncclSuccess) {
+      std::string m = std::string("ncclCommInitRank: ") + ncclGetErrorString(r);
+      pfc_destroy(c);
+      return set_err(nullptr, PFC_ERR_NCCL, m);
+    }
+  }
+  *out = c;
+  return PFC_OK;
+}
+
+pfc_status pfc_destroy(pfc_ctx* c) {
+  if (!c) return PFC_OK;
+  cudaSetDevice(c->cfg.device);
+  cudaDeviceSynchronize();
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (void* p : c->allocs) cudaFree(p);
+  delete c;
+  return PFC_OK;
+}
+
+// ------------------------------------------------------------------------------------------------
+// Step phases. Between them sit the three collectives of Alg.1 (all-gather L2, all-reduce L7,
+// all-reduce + get_submatrix L12-13 = reduce-scatter), either NCCL or the loopback group.
+// ------------------------------------------------------------------------------------------------
+namespace {
+
+pfc_status check_fb_args(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x) {
+  if (!x || !labels || !grad_x) return set_err(c, PFC_ERR_CONTRACT, "x, labels and grad_x must be non-NULL");
+  if ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(grad_x)) & 15)
+    return set_err(c, PFC_ERR_CONTRACT, "x and grad_x must be 16-byte aligned");
+  return PFC_OK;
+}
+
+// K1: normalise this rank's features into its all-gather slot; copy labels into theirs.
+void phase_a(pfc_ctx* c, const float* x, const int64_t* labels, cudaStream_t s) {
+  c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, s);
+}
+
+// K1b, sampler K2-K4, K5, K5b, K6 logits + partial den_i, K7 local row (max, sum).
+void phase_b(pfc_ctx* c, cudaStream_t s) {
+  const Sizes& sz = c->sz;
+  const bool bf = c->bf16;
+  int n = 0;
+  if (bf) n += launch_x_to_bf16(sz, c->X32, c->Xb, s);
+  n += launch_sampler(sz, c->Y, c->cfg.seed, (uint32_t)c->step, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
+                      c->tcol, c->err_dev, s);
+  n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
+  n += launch_target_cos(sz, c->X32, c->W, c->idx, c->tcol, c->inv_norm, c->ct, s);
+  if (c->use_tc)
+    n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
+                          c->partials, s);
+  else
+    n += launch_logits_simt(sz, bf, bf ? (const void*)c->Xb : (const void*)c->X32, c->Ws, c->tcol, c->ct, c->st, c->mp,
+                            c->cosv, c->partials, s);
+  n += launch_row_combine(sz, c->partials, c->tcol, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, s);
+  c->launches += n;
+}
+
+// after all-reduce MAX: red[n] = l_n e^{m_n - gm_n}, red[M] = local sum of target logits
+void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
+  c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->red, s);
+}
+
+// after all-reduce SUM: LSE, loss, K8 (prob - onehot), K9 dX_hat partial
+void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, cudaStream_t s) {
+  const Sizes& sz = c->sz;
+  int n = 0;
+  n += launch_finalize(sz, gmax, c->red, c->lse, loss_out, c->err_dev, s);
+  n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->tcol, c->ct, c->st, c->mp, c->G, s);
+  if (c->use_tc)
+    n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
+  else
+    n += launch_dx_simt(sz, c->bf16, c->G, c->Ws, c->st, c->dXh, s);
+  c->launches += n;
+}
+
+// after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat
+void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, cudaStream_t s) {
+  const Sizes& sz = c->sz;
+  int n = 0;
+  n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
+  if (c->use_tc)
+    n += launch_dw_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, c->dWh, s);
+  else
+    n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
+  c->launches += n;
+}
+
+pfc_status finish_fb(pfc_ctx* c, cudaStream_t s) {
+  CUDA_TRY(c, cudaGetLastError());
+  c->step += 1;
+  c->fb_done = true;
+  c->last_stream = s;
+  if (c->sync_check) {
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return device_error(c);
+  }
+  return PFC_OK;
+}
+
+}  // namespace
+
+pfc_status pfc_forward_backward(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss,
+                                void* stream) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  pfc_status a = check_fb_args(c, x, labels, grad_x);
+  if (a != PFC_OK) return a;
+  if (c->sz.world > 1 && c->cfg.comm_mode == PFC_COMM_LOOPBACK)
+    return set_err(c, PFC_ERR_CONTRACT, "loopback contexts are driven by pfc_group_forward_backward");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const Sizes& sz = c->sz;
+  const bool multi = sz.world > 1;
+  float* loss_out = loss ? loss : c->loss_dev;
+
+  phase_a(c, x, labels, s);
+  if (multi) {  // Alg.1 L2: X = allgather(x_i) (+ labels)
+    NCCL_TRY(c, ncclGroupStart());
+    NCCL_TRY(c, ncclAllGather(c->X32 + (size_t)sz.rank * sz.B * sz.d, c->X32, (size_t)sz.B * sz.d, ncclFloat, c->comm, s));
+    NCCL_TRY(c, ncclAllGather(c->Y + (size_t)sz.rank * sz.B, c->Y, (size_t)sz.B, ncclInt64, c->comm, s));
+    NCCL_TRY(c, ncclGroupEnd());
+  }
+  phase_b(c, s);
+  const float* gmax = c->rowmax;
+  if (multi) {  // Alg.1 L7 (stabilised, R12): global row max, then global sum
+    NCCL_TRY(c, ncclAllReduce(c->rowmax, c->gmax, sz.M, ncclFloat, ncclMax, c->comm, s));
+    gmax = c->gmax;
+  }
+  phase_c(c, gmax, s);
+  if (multi) NCCL_TRY(c, ncclAllReduce(c->red, c->red, sz.M + 1, ncclFloat, ncclSum, c->comm, s));
+  phase_d(c, gmax, loss_out, s);
+  const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
+  if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
+    NCCL_TRY(c, ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
+    dxh = c->dxh_local;
+  }
+  phase_e(c, dxh, grad_x, s);
+  return finish_fb(c, s);
+}
+
+pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* const* x, const int64_t* const* labels,
+                                      float* const* grad_x, float* loss, void* stream) {
+  if (!ctxs || n < 1 || n > kMaxLoopback || !x || !labels || !grad_x)
+    return set_err(nullptr, PFC_ERR_CONTRACT, "bad group arguments (1 <= n <= 16, non-NULL arrays)");
+  for (int r = 0; r < n; ++r) {
+    pfc_ctx* c = ctxs[r];
+    if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "NULL context in group");
+    if (c->sz.world != n || c->sz.rank != r || (n > 1 && c->cfg.comm_mode != PFC_COMM_LOOPBACK))
+      return set_err(c, PFC_ERR_CONTRACT, "group contexts must be loopback ranks 0..n-1 of a world of size n");
+    if (c->sz.B != ctxs[0]->sz.B || c->sz.d != ctxs[0]->sz.d || c->sz.C != ctxs[0]->sz.C || c->step != ctxs[0]->step)
+      return set_err(c, PFC_ERR_CONTRACT, "group contexts disagree on B, d, C or step");
+    pfc_status a = check_fb_args(c, x[r], labels[r], grad_x[r]);
+    if (a != PFC_OK) return a;
+  }
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const Sizes& sz = ctxs[0]->sz;
+  const size_t rowbytes = (size_t)sz.B * sz.d * 4;
+  pfc_ctx* c0 = ctxs[0];
+  PtrPack src{}, dst{};
+  for (int r = 0; r < n; ++r) phase_a(ctxs[r], x[r], labels[r], s);
+  for (int r = 0; r < n; ++r)      // all-gather: copy rank r's slot into every other rank
+    for (int q = 0; q < n; ++q) {
+      if (q == r) continue;
+      CUDA_TRY(c0, cudaMemcpyAsync(ctxs[q]->X32 + (size_t)r * sz.B * sz.d, ctxs[r]->X32 + (size_t)r * sz.B * sz.d,
+                                   rowbytes, cudaMemcpyDefault, s));
+      CUDA_TRY(c0, cudaMemcpyAsync(ctxs[q]->Y + (size_t)r * sz.B, ctxs[r]->Y + (size_t)r * sz.B, (size_t)sz.B * 8,
+                                   cudaMemcpyDefault, s));
+    }
+  for (int r = 0; r < n; ++r) phase_b(ctxs[r], s);
+  for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->rowmax; dst.p[r] = ctxs[r]->gmax; }
+  c0->launches += launch_group_reduce(sz.M, src, 0, dst, n, n, 1, s);
+  for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
+  for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->red; dst.p[r] = ctxs[r]->red; }
+  c0->launches += launch_group_reduce(sz.M + 1, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
+  for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, s);
+  for (int r = 0; r < n; ++r) src.p[r] = ctxs[r]->dXh;
+  for (int r = 0; r < n; ++r) {  // reduce-scatter: owner r sums rows [rB, (r+1)B) over ranks
+    PtrPack one{};
+    one.p[0] = ctxs[r]->dxh_local;
+    c0->launches += launch_group_reduce((int64_t)sz.B * sz.d, src, (int64_t)r * sz.B * sz.d, one, n, 1, 0, s);
+  }
+  for (int r = 0; r < n; ++r) phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], s);
+  for (int r = 0; r < n; ++r) {
+    pfc_status f = finish_fb(ctxs[r], s);
+    if (f != PFC_OK) return f;
+  }
+  return PFC_OK;
+}
+
+pfc_status pfc_forward_backward_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                                     float* loss_host, void* stream) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (!x_host || !labels_host || !grad_x_host) return set_err(c, PFC_ERR_CONTRACT, "NULL host buffer");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  const size_t xb = (size_t)c->sz.B * c->sz.d * 4;
+  CUDA_TRY(c, cudaMemcpyAsync(c->x_in, x_host, xb, cudaMemcpyHostToDevice, s));
+  CUDA_TRY(c, cudaMemcpyAsync(c->y_in, labels_host, (size_t)c->sz.B * 8, cudaMemcpyHostToDevice, s));
+  pfc_status r = pfc_forward_backward(c, c->x_in, c->y_in, c->gx_out, c->loss_dev, stream);
+  if (r != PFC_OK) return r;
+  CUDA_TRY(c, cudaMemcpyAsync(grad_x_host, c->gx_out, xb, cudaMemcpyDeviceToHost, s));
+  if (loss_host) CUDA_TRY(c, cudaMemcpyAsync(loss_host, c->loss_dev, 4, cudaMemcpyDeviceToHost, s));
+  CUDA_TRY(c, cudaStreamSynchronize(s));
+  return PFC_OK;
+}
+
+pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (!c->fb_done) return set_err(c, PFC_ERR_CONTRACT, "pfc_step without a preceding pfc_forward_backward");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  c->last_stream = s;
+  c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, lr, c->cfg.momentum,
+                            c->cfg.weight_decay, s);
+  CUDA_TRY(c, cudaGetLastError());
+  c->fb_done = false;
+  if (c->sync_check) {
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return device_error(c);
+  }
+  return PFC_OK;
+}
+
+pfc_status pfc_shard_range(const pfc_ctx* c, int64_t* start, int64_t* count) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (start) *start = c->sz.a;
+  if (count) *count = c->sz.C_local;
+  return PFC_OK;
+}
+
+pfc_status pfc_sizes(const pfc_ctx* c, int64_t* M, int64_t* k_max) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (M) *M = c->sz.M;
+  if (k_max) *k_max = c->sz.k_max;
+  return PFC_OK;
+}
+
+pfc_status pfc_param_ptrs(pfc_ctx* c, float** W, float** V) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (W) *W = c->W;
+  if (V) *V = c->V;
+  return PFC_OK;
+}
+
+static pfc_status sync_and_check(pfc_ctx* c) {
+  CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  return device_error(c);
+}
+
+pfc_status pfc_check(pfc_ctx* c) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  return sync_and_check(c);
+}
+
+pfc_status pfc_get_sampled(pfc_ctx* c, int64_t* idx_host, int64_t capacity, int64_t* k_out) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  pfc_status r = sync_and_check(c);
+  if (r != PFC_OK) return r;
+  SamplerState h;
+  CUDA_TRY(c, cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  if (k_out) *k_out = h.k;
+  if (!idx_host) return PFC_OK;
+  if (capacity < h.k) return set_err(c, PFC_ERR_CONTRACT, "idx capacity < k_i");
+  std::vector<int32_t> tmp(h.k);
+  CUDA_TRY(c, cudaMemcpy(tmp.data(), c->idx, (size_t)h.k * 4, cudaMemcpyDeviceToHost));
+  for (int i = 0; i < h.k; ++i) idx_host[i] = c->sz.a + tmp[i];
+  return PFC_OK;
+}
+
+pfc_status pfc_get_sampled_grad(pfc_ctx* c, float* dW_host, int64_t capacity_rows) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (!c->fb_done) return set_err(c, PFC_ERR_CONTRACT, "no pending gradient (call before pfc_step)");
+  pfc_status r = sync_and_check(c);
+  if (r != PFC_OK) return r;
+  SamplerState h;
+  CUDA_TRY(c, cudaMemcpy(&h, c->st, sizeof(h), cudaMemcpyDeviceToHost));
+  if (capacity_rows < h.k) return set_err(c, PFC_ERR_CONTRACT, "capacity_rows < k_i");
+  float* tmp = nullptr;
+  const size_t bytes = (size_t)h.k * c->sz.d * 4;
+  CUDA_TRY(c, cudaMalloc(&tmp, std::max<size_t>(bytes, 16)));
+  c->launches += launch_raw_grad(c->sz, c->W, c->dWh, c->idx, c->inv_norm, c->st, tmp, 0);
+  cudaError_t e = cudaMemcpy(dW_host, tmp, bytes, cudaMemcpyDeviceToHost);
+  cudaFree(tmp);
+  CUDA_TRY(c, e);
+  return PFC_OK;
+}
+
+pfc_status pfc_get_lse(pfc_ctx* c, float* lse_host, int64_t capacity) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  if (capacity < c->sz.M) return set_err(c, PFC_ERR_CONTRACT, "capacity < M");
+  pfc_status r = sync_and_check(c);
+  if (r != PFC_OK) return r;
+  CUDA_TRY(c, cudaMemcpy(lse_host, c->lse, (size_t)c->sz.M * 4, cudaMemcpyDeviceToHost));
+  return PFC_OK;
+}
+
+pfc_status pfc_get_step(const pfc_ctx* c, uint64_t* step) {
+  if (!c || !step) return set_err(nullptr, PFC_ERR_CONTRACT, "NULL argument");
+  *step = c->step;
+  return PFC_OK;
+}
+
+pfc_status pfc_set_step(pfc_ctx* c, uint64_t step) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  c->step = step;
+  c->fb_done = false;
+  return PFC_OK;
+}
+
+int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
+
+pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, uint64_t seed, uint64_t step,
+                            const int64_t* labels, int32_t M, int64_t* idx_out, int64_t* k_out, void* stream) {
+  if (!labels || !idx_out || !k_out || M < 1) return set_err(nullptr, PFC_ERR_CONTRACT, "bad arguments");
+  if (world < 1 || rank < 0 || rank >= world || C < world || !(r > 0.0 && r <= 1.0))
+    return set_err(nullptr, PFC_ERR_CONFIG, "bad shard configuration");
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  Sizes sz{};
+  sz.C = C; sz.world = world; sz.rank = rank; sz.M = M;
+  sz.C_local = C / world + (rank < C % world ? 1 : 0);
+  sz.a = (int64_t)rank * (C / world) + std::min<int64_t>(rank, C % world);
+  sz.budget = (int64_t)std::ceil(r * (double)sz.C_local);
+  sz.k_max = std::max<int64_t>(sz.budget, std::min<int64_t>(M, sz.C_local));
+  sz.ntiles_sel = (int)((sz.C_local + kSelTile - 1) / kSelTile);
+  uint32_t *bits = nullptr, *keys = nullptr;
+  int *hist = nullptr, *tile = nullptr, *err = nullptr;
+  SamplerState* st = nullptr;
+  int32_t *idx = nullptr, *tcol = nullptr;
+  cudaError_t e = cudaSuccess;
+  auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 16)); };
+  A((void**)&bits, ((sz.C_local + 31) / 32) * 4);
+  A((void**)&keys, sz.C_local * 4);
+  A((void**)&hist, 5120 * 4);
+  A((void**)&tile, (size_t)sz.ntiles_sel * 16);
+  A((void**)&err, 16);
+  A((void**)&st, sizeof(SamplerState));
+  A((void**)&idx, sz.k_max * 4);
+  A((void**)&tcol, (size_t)M * 4);
+  pfc_status res = PFC_OK;
+  if (e != cudaSuccess) {
+    res = set_err(nullptr, PFC_ERR_OOM, cudaGetErrorString(e));
+  } else {
+    cudaMemsetAsync(err, 0, 16, s);
+    launch_sampler(sz, labels, seed, (uint32_t)step, bits, keys, hist, tile, st, idx, tcol, err, s);
+    launch_idx_to_global(sz.k_max, idx, st, sz.a, idx_out, s);
+    SamplerState h{};
+    int herr = 0;
+    cudaMemcpyAsync(&h, st, sizeof(h), cudaMemcpyDeviceToHost, s);
+    cudaMemcpyAsync(&herr, err, 4, cudaMemcpyDeviceToHost, s);
+    e = cudaStreamSynchronize(s);
+    if (e != cudaSuccess) res = set_err(nullptr, PFC_ERR_CUDA, cudaGetErrorString(e));
+    else if (herr & ERR_INTERNAL) res = set_err(nullptr, PFC_ERR_CUDA, "sampler consistency check failed");
+    *k_out = h.k;
+  }
+  cudaFree(bits); cudaFree(keys); cudaFree(hist); cudaFree(tile); cudaFree(err); cudaFree(st); cudaFree(idx);
+  cudaFree(tcol);
+  return res;
+}
+
+}  // extern "C"

@@ -1,0 +1,166 @@
+// Internal declarations of the B200 Partial FC library (not part of the C-ABI).
+// Kernel numbering K1..K12 follows SURVEY.md §2.2 / DESIGN.md §Kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <nccl.h>
+#include <stdint.h>
+#include <string>
+
+#include "../../include/pfc.h"
+
+namespace pfc {
+
+// Sticky device error bits (reported as pfc_status by the next synchronising call).
+enum : int { ERR_DATA = 1, ERR_DEGENERATE = 2, ERR_NUMERIC = 4, ERR_INTERNAL = 8 };
+
+constexpr float kNormEps = 1e-12f;   // DESIGN.md R8
+constexpr float kArcDerivEps = 1e-6f;  // DESIGN.md R10
+
+// Device-resident state of the sampler for one step.
+struct SamplerState {
+  int npos;        // |P_i|
+  int k;           // k_i = max(ceil(r C_local), |P_i|)
+  int n_neg;       // n_i = k_i - |P_i|
+  int none;        // n_i == 0: no negative selected
+  uint32_t prefix; // radix-select prefix after each pass
+  int remaining;   // rank of the threshold inside the current prefix bucket (1-based)
+  uint32_t T;      // threshold key
+  int t;           // number of tied (key == T) negatives to take, smallest ids first
+  int total;       // number of selected rows written by the compaction (== k)
+  int pad[7];
+};
+
+// Margin parameters used by the epilogues (R9-R11).
+struct MarginParams {
+  int type;          // pfc_margin
+  float s;           // scale
+  float m;           // margin
+  float cos_m, sin_m, th, mm;  // ArcFace: cos m, sin m, cos(pi - m), m sin m
+};
+
+__device__ __forceinline__ float margin_phi(const MarginParams& mp, float c) {
+  if (mp.type == PFC_MARGIN_COSFACE) return c - mp.m;
+  if (mp.type == PFC_MARGIN_ARCFACE) {
+    float cc = fminf(1.f, fmaxf(-1.f, c));
+    if (cc > mp.th) {
+      float sn = sqrtf(fmaxf(0.f, 1.f - cc * cc));
+      return cc * mp.cos_m - sn * mp.sin_m;        // cos(theta + m)
+    }
+    return c - mp.mm;                               // theta + m >= pi (R9)
+  }
+  return c;
+}
+
+__device__ __forceinline__ float margin_dphi(const MarginParams& mp, float c) {
+  if (mp.type == PFC_MARGIN_ARCFACE) {
+    float cc = fminf(1.f, fmaxf(-1.f, c));
+    if (cc > mp.th) {
+      float sn = fmaxf(sqrtf(fmaxf(0.f, 1.f - cc * cc)), kArcDerivEps);
+      return mp.cos_m + cc * mp.sin_m / sn;        // d/dc cos(acos c + m)
+    }
+  }
+  return 1.f;
+}
+
+// Philox4x32-10 (Random123 constants), first output word: the sampler key of global class j
+// (R2): ctr = {j lo, j hi, step, 0}, key = {seed lo, seed hi}.
+__device__ __forceinline__ uint32_t philox_class_key(uint64_t j, uint32_t step, uint64_t seed) {
+  uint32_t c0 = (uint32_t)j, c1 = (uint32_t)(j >> 32), c2 = step, c3 = 0u;
+  uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    if (r) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const uint32_t lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const uint32_t lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  return c0;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// ---------------------------------------------------------------------------------------------
+// Launchers (host side). Each returns the number of kernels it launched.
+// ---------------------------------------------------------------------------------------------
+struct Sizes {
+  int64_t C, C_local, a;   // classes, shard rows, shard start
+  int d, B, M, M_pad;      // dim, per-rank batch, global batch, M rounded up to 128
+  int rank, world;
+  int64_t budget;          // ceil(r C_local)
+  int64_t k_max, k_pad;    // workspace bound and its padding to the tile width
+  int ltile;               // columns per logits partial tile (64 SIMT, 128 tcgen05)
+  int n_ltiles;            // number of logits column tiles (k_pad / ltile)
+  int ntiles_sel;          // sampler compaction tiles
+};
+
+constexpr int kSelTile = 8192;   // sampler compaction tile (256 threads x 32)
+constexpr int kKPad = 256;       // k_pad granularity (multiple of every GEMM tile width)
+
+// sampler.cu
+int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, uint32_t step, uint32_t* bits,
+                   uint32_t* keys, int* hist, int* tile_cnt, SamplerState* st, int32_t* idx, int32_t* tcol,
+                   int* err, cudaStream_t s);
+
+// rows.cu
+int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
+                       float* X32, int64_t* Y, int* err, cudaStream_t s);
+int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s);
+int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st,
+                    void* Ws, float* inv_norm, int* err, cudaStream_t s);
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int32_t* idx, const int32_t* tcol,
+                      const float* inv_norm, float* ct, cudaStream_t s);
+int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* tcol, const float* ct,
+                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
+int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
+                    float* red, cudaStream_t s);
+int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* loss_out, int* err,
+                    cudaStream_t s);
+int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const int32_t* tcol,
+                        const float* ct, const SamplerState* st, MarginParams mp, void* G, cudaStream_t s);
+int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
+                          float* grad_x, cudaStream_t s);
+int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
+               const SamplerState* st, float lr, float mu, float lambda, cudaStream_t s);
+int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
+                    const SamplerState* st, float* out, cudaStream_t s);
+
+// loopback collectives: dst[r][i] = op_{q ascending} src[q][src_off + i] for r < ndst (op 0 = sum, 1 = max)
+constexpr int kMaxLoopback = 16;
+struct PtrPack { float* p[kMaxLoopback]; };
+int launch_group_reduce(int64_t n, const PtrPack& src, int64_t src_off, const PtrPack& dst, int nranks, int ndst,
+                        int op, cudaStream_t s);
+int launch_idx_to_global(int64_t k_max, const int32_t* idx, const SamplerState* st, int64_t a, int64_t* out,
+                         cudaStream_t s);
+
+// gemm_simt.cu — fp32 (and bf16-operand) FFMA contractions
+int launch_logits_simt(const Sizes& sz, bool bf16, const void* X, const void* Ws, const int32_t* tcol,
+                       const float* ct, const SamplerState* st, MarginParams mp, void* cosv, float2* partials,
+                       cudaStream_t s);
+int launch_dx_simt(const Sizes& sz, bool bf16, const void* G, const void* Ws, const SamplerState* st, float* dXh,
+                   cudaStream_t s);
+int launch_dw_simt(const Sizes& sz, bool bf16, const void* G, const void* X, const SamplerState* st, float* dWh,
+                   cudaStream_t s);
+
+// gemm_tc.cu — tcgen05 / TMEM / TMA bf16 contractions (sm_100a)
+bool tc_available();
+int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+                     const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
+                     cudaStream_t s);
+int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,
+                 float* dXh, float* split_ws, cudaStream_t s);
+int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                 float* dWh, cudaStream_t s);
+
+}  // namespace pfc

@@ -1,0 +1,412 @@
+// Row-wise and streaming kernels of the Partial FC step (everything that is not a contraction).
+//   K1  normalize_x      x_hat = x / max(||x||, eps) (Eq.6) into the all-gather slot
+//   K5  gather_w         W_s[p] = W[idx_p] / ||W[idx_p]|| (bf16 or fp32), inv_norm[p]
+//   K5b target_cos       c_t[n] = x_hat_n . w_hat_{y_n} in fp32
+//   K7  row_combine      per-row (max, sum-exp) over the logits tiles (Alg.1 L5 den_i)
+//       prep_sum/finalize global LSE after the all-reduces (Alg.1 L6-7), loss (Eq.5)
+//   K8  softmax_grad     Gc = (s/M)(p - onehot) phi'(c_t) (Alg.1 L8-9)
+//   K10 xnorm_backward   dx = (dx_hat - x_hat (x_hat . dx_hat)) / ||x||
+//   K12 sgd              lazy momentum SGD of the sampled rows
+#include "pfc_internal.cuh"
+
+namespace pfc {
+namespace {
+
+// ---------------------------------------------------------------- K1
+__global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __restrict__ x,
+                              const int64_t* __restrict__ labels, float* __restrict__ xh_local,
+                              float* __restrict__ xnorm, float* __restrict__ X32, int64_t* __restrict__ Y, int* err) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= B) return;
+  const float* xr = x + (int64_t)warp * d;
+  float ss = 0.f;
+  for (int c = lane; c < d; c += 32) { float v = xr[c]; ss += v * v; }
+  ss = warp_sum(ss);
+  const float nrm = sqrtf(ss);
+  const float inv = 1.f / fmaxf(nrm, kNormEps);
+  float* out_l = xh_local + (int64_t)warp * d;
+  float* out_g = X32 + ((int64_t)rank * B + warp) * d;
+  for (int c = lane; c < d; c += 32) { float v = xr[c] * inv; out_l[c] = v; out_g[c] = v; }
+  if (lane == 0) {
+    xnorm[warp] = nrm;
+    int64_t y = labels[warp];
+    Y[(int64_t)rank * B + warp] = y;
+    if (y < 0 || y >= C) atomicOr(err, ERR_DATA);
+    if (!(nrm > 0.f)) atomicOr(err, ERR_DEGENERATE);
+  }
+}
+
+__global__ void k_x_to_bf16(int64_t n, const float* __restrict__ X32, __nv_bfloat16* __restrict__ Xb) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) Xb[i] = __float2bfloat16_rn(X32[i]);
+}
+
+// ---------------------------------------------------------------- K5: one warp per sampled row
+template <bool BF16>
+__global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, const int32_t* __restrict__ idx,
+                           const SamplerState* st, void* __restrict__ Ws, float* __restrict__ inv_norm, int* err) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= k_pad) return;
+  const int k = st->k;
+  if (p >= k) {  // padding rows: zero so that the K = k contraction sees exact zeros
+    for (int c = lane * 4; c < d; c += 128) {
+      if (BF16) {
+        __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
+        __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)Ws + p * d + c);
+        o[0] = z; o[1] = z;
+      } else {
+        *reinterpret_cast<float4*>((float*)Ws + p * d + c) = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+    if (lane == 0) inv_norm[p] = 0.f;
+    return;
+  }
+  const float* wr = W + (int64_t)idx[p] * d;
+  float4 v[4];
+  const int nv = d / 128;  // d % 128 == 0 checked at init for the vector path
+  float ss = 0.f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < nv) {
+      v[i] = __ldg(reinterpret_cast<const float4*>(wr + i * 128 + lane * 4));
+      ss += v[i].x * v[i].x + v[i].y * v[i].y + v[i].z * v[i].z + v[i].w * v[i].w;
+    }
+  }
+  for (int c = 512 + lane * 4; c < d; c += 128) {  // d > 512
+    float4 u = __ldg(reinterpret_cast<const float4*>(wr + c));
+    ss += u.x * u.x + u.y * u.y + u.z * u.z + u.w * u.w;
+  }
+  ss = warp_sum(ss);
+  const float nrm = sqrtf(ss);
+  const float inv = 1.f / fmaxf(nrm, kNormEps);
+  if (lane == 0) {
+    inv_norm[p] = inv;
+    if (!(nrm > 0.f)) atomicOr(err, ERR_DEGENERATE);
+  }
+  auto store = [&](int c, float4 u) {
+    if (BF16) {
+      __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)Ws + p * d + c);
+      o[0] = __floats2bfloat162_rn(u.x * inv, u.y * inv);
+      o[1] = __floats2bfloat162_rn(u.z * inv, u.w * inv);
+    } else {
+      *reinterpret_cast<float4*>((float*)Ws + p * d + c) = make_float4(u.x * inv, u.y * inv, u.z * inv, u.w * inv);
+    }
+  };
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nv) store(i * 128 + lane * 4, v[i]);
+  for (int c = 512 + lane * 4; c < d; c += 128) store(c, __ldg(reinterpret_cast<const float4*>(wr + c)));
+}
+
+// ---------------------------------------------------------------- K5b: one warp per batch row
+__global__ void k_target_cos(int M, int d, const float* __restrict__ X32, const float* __restrict__ W,
+                             const int32_t* __restrict__ idx, const int32_t* __restrict__ tcol,
+                             const float* __restrict__ inv_norm, float* __restrict__ ct) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (n >= M) return;
+  const int p = tcol[n];
+  if (p < 0) { if (lane == 0) ct[n] = 0.f; return; }
+  const float* xr = X32 + (int64_t)n * d;
+  const float* wr = W + (int64_t)idx[p] * d;
+  float acc = 0.f;
+  for (int c = lane; c < d; c += 32) acc += xr[c] * wr[c];
+  acc = warp_sum(acc);
+  if (lane == 0) ct[n] = acc * inv_norm[p];
+}
+
+// ---------------------------------------------------------------- K7: one warp per batch row
+__global__ void k_row_combine(int M, int ntiles, int ltile, const float2* __restrict__ partials,
+                              const int32_t* __restrict__ tcol, const float* __restrict__ ct, const SamplerState* st,
+                              MarginParams mp, float* __restrict__ rowmax, float* __restrict__ rowsum,
+                              float* __restrict__ zt) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (n >= M) return;
+  const float2* pr = partials + (int64_t)n * ntiles;
+  const int nvalid = (st->k + ltile - 1) / ltile;  // tiles past k_i are never written
+  ntiles = min(ntiles, nvalid);
+  float m = -INFINITY;
+  for (int t = lane; t < ntiles; t += 32) m = fmaxf(m, pr[t].x);
+  m = warp_max(m);
+  float l = 0.f;
+  if (m > -INFINITY)
+    for (int t = lane; t < ntiles; t += 32) { float2 v = pr[t]; l += v.y * __expf(v.x - m); }
+  l = warp_sum(l);
+  if (lane == 0) {
+    rowmax[n] = m;
+    rowsum[n] = l;
+    zt[n] = tcol[n] >= 0 ? mp.s * margin_phi(mp, ct[n]) : 0.f;
+  }
+}
+
+// red[n] = rowsum[n] e^{rowmax[n] - gmax[n]} (n < M); red[M] = sum of the local target logits.
+__global__ void __launch_bounds__(1024) k_prep_sum(int M, const float* __restrict__ rowmax,
+                                                   const float* __restrict__ gmax, const float* __restrict__ rowsum,
+                                                   const float* __restrict__ zt, float* __restrict__ red) {
+  __shared__ float sh[32];
+  float acc = 0.f;
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    float rm = rowmax[n];
+    red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
+    acc += zt[n];
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[M] = v;
+  }
+}
+
+// LSE_n = gmax_n + log(gsum_n); loss = (sum_n LSE_n - sum_n z_t) / M   (Eq.5 over the global batch, R13)
+__global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restrict__ gmax, const float* __restrict__ red,
+                                                   float* __restrict__ lse, float* __restrict__ loss_out, int* err) {
+  __shared__ float sh[32];
+  float acc = 0.f;
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    float v = gmax[n] + __logf(red[n]);
+    lse[n] = v;
+    acc += v;
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) {
+      float L = (v - red[M]) / (float)M;
+      if (loss_out) *loss_out = L;
+      if (!isfinite(L)) atomicOr(err, ERR_NUMERIC);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K8: softmax gradient, 8 columns per thread
+template <bool BF16>
+__global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, const void* __restrict__ cosv,
+                                                      const float* __restrict__ lse, const int32_t* __restrict__ tcol,
+                                                      const float* __restrict__ ct, const SamplerState* st,
+                                                      MarginParams mp, void* __restrict__ G) {
+  const int n = blockIdx.y;
+  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+  if (c0 >= k_pad) return;
+  const int k = st->k;
+  const float L2E = 1.4426950408889634f;
+  const float sl = mp.s * L2E;
+  const float off = lse[n] * L2E;
+  const int tc = tcol[n];
+  const float gs = mp.s / (float)M;
+  float c[8];
+  const int64_t base = (int64_t)n * k_pad + c0;
+  if (BF16) {
+    uint4 raw = *reinterpret_cast<const uint4*>((const __half*)cosv + base);
+    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); c[2 * i] = f.x; c[2 * i + 1] = f.y; }
+  } else {
+    float4 a = *reinterpret_cast<const float4*>((const float*)cosv + base);
+    float4 b = *reinterpret_cast<const float4*>((const float*)cosv + base + 4);
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  }
+  float g[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t col = c0 + i;
+    if (col < k) {
+      if (col == tc) {
+        float ctv = ct[n];
+        float p = exp2f(mp.s * margin_phi(mp, ctv) * L2E - off);
+        g[i] = gs * (p - 1.f) * margin_dphi(mp, ctv);
+      } else {
+        g[i] = gs * exp2f(c[i] * sl - off);
+      }
+    } else {
+      g[i] = 0.f;
+    }
+  }
+  if (BF16) {
+    uint4 o;
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+    *reinterpret_cast<uint4*>((__nv_bfloat16*)G + base) = o;
+  } else {
+    *reinterpret_cast<float4*>((float*)G + base) = make_float4(g[0], g[1], g[2], g[3]);
+    *reinterpret_cast<float4*>((float*)G + base + 4) = make_float4(g[4], g[5], g[6], g[7]);
+  }
+}
+
+// ---------------------------------------------------------------- K10
+__global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, const float* __restrict__ xh,
+                                 const float* __restrict__ xnorm, float* __restrict__ gx) {
+  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (n >= B) return;
+  const float* g = dxh + (int64_t)n * d;
+  const float* xr = xh + (int64_t)n * d;
+  float dot = 0.f;
+  for (int c = lane; c < d; c += 32) dot += xr[c] * g[c];
+  dot = warp_sum(dot);
+  const float inv = 1.f / fmaxf(xnorm[n], kNormEps);
+  for (int c = lane; c < d; c += 32) gx[(int64_t)n * d + c] = (g[c] - xr[c] * dot) * inv;
+}
+
+// ---------------------------------------------------------------- K12 (+ raw-gradient introspection)
+template <bool UPDATE>
+__global__ void k_sgd(int64_t k_pad, int d, float* __restrict__ W, float* __restrict__ V, const float* __restrict__ dWh,
+                      const int32_t* __restrict__ idx, const float* __restrict__ inv_norm, const SamplerState* st,
+                      float lr, float mu, float lambda, float* __restrict__ out) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= st->k) return;
+  const int64_t j = idx[p];
+  float* wr = W + j * d;
+  const float* gr = dWh + p * d;
+  const float inv = inv_norm[p];
+  float dot = 0.f;
+  for (int c = lane * 4; c < d; c += 128) {
+    float4 w = *reinterpret_cast<const float4*>(wr + c);
+    float4 g = *reinterpret_cast<const float4*>(gr + c);
+    dot += (w.x * g.x + w.y * g.y + w.z * g.z + w.w * g.w);
+  }
+  dot = warp_sum(dot) * inv;  // w_hat . dw_hat
+  for (int c = lane * 4; c < d; c += 128) {
+    float4 w = *reinterpret_cast<const float4*>(wr + c);
+    float4 g = *reinterpret_cast<const float4*>(gr + c);
+    float4 gg;
+    gg.x = (g.x - w.x * inv * dot) * inv;
+    gg.y = (g.y - w.y * inv * dot) * inv;
+    gg.z = (g.z - w.z * inv * dot) * inv;
+    gg.w = (g.w - w.w * inv * dot) * inv;
+    if (UPDATE) {
+      float* vr = V + j * d;
+      float4 v = *reinterpret_cast<const float4*>(vr + c);
+      v.x = mu * v.x + gg.x + lambda * w.x;
+      v.y = mu * v.y + gg.y + lambda * w.y;
+      v.z = mu * v.z + gg.z + lambda * w.z;
+      v.w = mu * v.w + gg.w + lambda * w.w;
+      w.x -= lr * v.x; w.y -= lr * v.y; w.z -= lr * v.z; w.w -= lr * v.w;
+      *reinterpret_cast<float4*>(vr + c) = v;
+      *reinterpret_cast<float4*>(wr + c) = w;
+    } else {
+      *reinterpret_cast<float4*>(out + p * d + c) = gg;
+    }
+  }
+}
+
+}  // namespace
+
+int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
+                       float* X32, int64_t* Y, int* err, cudaStream_t s) {
+  k_normalize_x<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, sz.rank, sz.C, x, labels, xh_local, xnorm, X32, Y,
+                                                        err);
+  return 1;
+}
+
+int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s) {
+  int64_t n = (int64_t)sz.M * sz.d;
+  k_x_to_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, X32, Xb);
+  return 1;
+}
+
+int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st, void* Ws,
+                    float* inv_norm, int* err, cudaStream_t s) {
+  unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
+  if (bf16) k_gather_w<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, inv_norm, err);
+  else k_gather_w<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, inv_norm, err);
+  return 1;
+}
+
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int32_t* idx, const int32_t* tcol,
+                      const float* inv_norm, float* ct, cudaStream_t s) {
+  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, X32, W, idx, tcol, inv_norm, ct);
+  return 1;
+}
+
+int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* tcol, const float* ct,
+                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s) {
+  k_row_combine<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, partials, tcol, ct, st, mp, rowmax,
+                                                        rowsum, zt);
+  return 1;
+}
+
+int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
+                    float* red, cudaStream_t s) {
+  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, rowmax, gmax, rowsum, zt, red);
+  return 1;
+}
+
+int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* loss_out, int* err,
+                    cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, loss_out, err);
+  return 1;
+}
+
+int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const int32_t* tcol,
+                        const float* ct, const SamplerState* st, MarginParams mp, void* G, cudaStream_t s) {
+  dim3 grid((unsigned)((sz.k_pad / 8 + 255) / 256), sz.M);
+  if (bf16) k_softmax_grad<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, tcol, ct, st, mp, G);
+  else k_softmax_grad<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, tcol, ct, st, mp, G);
+  return 1;
+}
+
+int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm, float* grad_x,
+                          cudaStream_t s) {
+  k_xnorm_backward<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, dxh, xh_local, xnorm, grad_x);
+  return 1;
+}
+
+int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
+               const SamplerState* st, float lr, float mu, float lambda, cudaStream_t s) {
+  unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
+  k_sgd<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, dWh, idx, inv_norm, st, lr, mu, lambda, nullptr);
+  return 1;
+}
+
+int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
+                    const SamplerState* st, float* out, cudaStream_t s) {
+  unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
+  k_sgd<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, const_cast<float*>(W), nullptr, dWh, idx, inv_norm, st, 0.f, 0.f,
+                                    0.f, out);
+  return 1;
+}
+
+}  // namespace pfc
+
+// ---------------------------------------------------------------- loopback collectives (one process, k ranks)
+namespace pfc {
+namespace {
+__global__ void k_group_reduce(int64_t n, PtrPack src, int64_t src_off, PtrPack dst, int nranks, int nd, int op) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float acc = src.p[0][src_off + i];
+  for (int r = 1; r < nranks; ++r) {  // rank-ascending
+    float v = src.p[r][src_off + i];
+    acc = op == 0 ? acc + v : fmaxf(acc, v);
+  }
+  for (int r = 0; r < nd; ++r) dst.p[r][i] = acc;
+}
+}  // namespace
+
+int launch_group_reduce(int64_t n, const PtrPack& src, int64_t src_off, const PtrPack& dst, int nranks, int ndst,
+                        int op, cudaStream_t s) {
+  k_group_reduce<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, src, src_off, dst, nranks, ndst, op);
+  return 1;
+}
+
+namespace {
+__global__ void k_idx_to_global(const int32_t* __restrict__ idx, const SamplerState* st, int64_t a,
+                                int64_t* __restrict__ out) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p < st->k) out[p] = a + idx[p];
+}
+}  // namespace
+
+int launch_idx_to_global(int64_t k_max, const int32_t* idx, const SamplerState* st, int64_t a, int64_t* out,
+                         cudaStream_t s) {
+  k_idx_to_global<<<(unsigned)((k_max + 255) / 256), 256, 0, s>>>(idx, st, a, out);
+  return 1;
+}
+}  // namespace pfc

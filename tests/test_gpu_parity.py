@@ -1,0 +1,225 @@
+"""Parity of the CUDA path (through the C-ABI) with the float64 oracle, element by element.
+
+Bars (BASELINE.json north_star; R19 metrics): sampled indices bit-exact; fp32 mode 1e-4 relative
+on loss and max-relative (max|a-b| / max|b|) on grad_x and dW; bf16 mode 1e-3 on loss and 2e-2 on
+grad_x / dW. Inputs come from synth/ (W rows are bit-identical on both sides)."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+from oracle import OracleConfig
+
+pytestmark = pytest.mark.gpu
+
+pfc = pytest.importorskip("paper_2010_05222_b200")
+MT = {"none": 0, "arcface": 1, "cosface": 2}
+TOL = {"fp32": (1e-4, 1e-4), "bf16": (1e-3, 2e-2)}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    torch.cuda.set_device(0)
+
+
+def maxrel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b)) / max(np.max(np.abs(b)), 1e-300))
+
+
+def make_layer(C, d, B, r, margin_type, m, precision, seed=0, wseed=1, world=1, rank=0, comm="nccl", mu=0.9,
+               lam=5e-4, scale=64.0):
+    layer = pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, scale=scale, margin_type=margin_type,
+                          margin=m, momentum=mu, weight_decay=lam, precision=precision, seed=seed, rank=rank,
+                          world_size=world, comm_mode=comm)
+    W, V = layer.params()
+    synth.fill_w_shard(W, wseed, layer.shard_start)
+    V.zero_()
+    torch.cuda.synchronize()
+    return layer
+
+
+def ocfg(C, d, B, r, margin_type, m, seed=0, world=1, mu=0.9, lam=5e-4, scale=64.0):
+    return OracleConfig(num_classes=C, dim=d, batch=B, world_size=world, sample_rate=r, scale=scale,
+                        margin_type=MT[margin_type], margin=m, momentum=mu, weight_decay=lam, seed=seed)
+
+
+# ------------------------------------------------------------------------------------------------ sampler
+SAMPLER_CASES = [
+    # (C, world, M, r, ranks, label mode)           BASELINE.json configs' shard shapes
+    (1000, 1, 64, 0.1, [0], "uniform"),              # C1
+    (85742, 8, 1024, 0.1, list(range(8)), "uniform"),  # C2 MS1MV2-shaped, all 8 shards
+    (360232, 8, 1024, 0.1, [0, 7], "uniform"),       # C3 r = 0.1
+    (360232, 1, 128, 1.0, [0], "uniform"),           # C3 r = 1.0 (identity)
+    (360232, 4, 512, 0.1, [1, 3], "uniform"),
+    (10_000_000, 8, 2048, 0.1, [0, 5], "uniform"),   # C4 shard (1.25M)
+    (10_000_000, 1, 256, 0.1, [0], "uniform"),       # C4 on one GPU (10M)
+    (2000, 2, 256, 0.01, [0, 1], "stress"),          # all labels in shard 0: k_0 = |P_0|
+    (777, 3, 5, 0.37, [0, 1, 2], "uniform"),         # ragged: odd sizes everywhere
+]
+
+
+@pytest.mark.parametrize("C,world,M,r,ranks,mode", SAMPLER_CASES)
+def test_sampler_bit_exact(C, world, M, r, ranks, mode):
+    y = np.concatenate(synth.make_labels(5, 0, 1, M, C, mode=mode, stress_range=C // world // 2))
+    yd = torch.from_numpy(y).cuda()
+    for step in [0, 3]:
+        for rank in ranks:
+            got = pfc.sample_shard(C, world, rank, r, seed=42, step=step, labels=yd).cpu().numpy()
+            a, Cl = oracle.shard_range(C, world, rank)
+            exp, npos = oracle.sample_shard(y, a, Cl, r, seed=42, step=step)
+            assert got.shape == exp.shape, (rank, step, got.shape, exp.shape)
+            assert np.array_equal(got, exp), (rank, step)
+
+
+def test_sampler_100m_shard_bit_exact():
+    # C5: 100M ids over 8 ranks -> 12.5M-class shard, spot one rank
+    C, world, M, r = 100_000_000, 8, 2048, 0.1
+    y = np.concatenate(synth.make_labels(9, 0, 1, M, C))
+    got = pfc.sample_shard(C, world, 3, r, seed=7, step=11, labels=torch.from_numpy(y).cuda()).cpu().numpy()
+    a, Cl = oracle.shard_range(C, world, 3)
+    exp, _ = oracle.sample_shard(y, a, Cl, r, seed=7, step=11)
+    assert len(got) == 1_250_000 and np.array_equal(got, exp)
+
+
+# ------------------------------------------------------------------------------------------------ fwd/bwd/step
+FB_CASES = [
+    # C, d, B, r, margin, m, dist
+    (1000, 128, 64, 0.1, "arcface", 0.5, "init"),       # C1 (BASELINE.json configs[0])
+    (1000, 128, 64, 0.1, "arcface", 0.5, "trained"),
+    (5000, 256, 32, 0.3, "cosface", 0.4, "trained"),
+    (3001, 128, 40, 1.0, "none", 0.0, "init"),          # r = 1: full softmax, ragged k
+    (20000, 512, 96, 0.05, "arcface", 0.5, "trained"),  # d = 512, several logits tiles, ragged M
+]
+
+
+def _run_single(case, precision, steps=2):
+    C, d, B, r, mt, m, dist = case
+    lr = 0.1
+    layer = make_layer(C, d, B, r, mt, m, precision, seed=3, wseed=1)
+    cfg = ocfg(C, d, B, r, mt, m, seed=3)
+    Vh = {}
+    Wcur = {}
+
+    def w_rows(ids):
+        ids = np.asarray(ids)
+        base = synth.w_rows_np(1, ids, d)
+        for t, j in enumerate(ids):
+            if int(j) in Wcur:
+                base[t] = Wcur[int(j)]
+        return base
+
+    results = []
+    for step in range(steps):
+        ys = synth.make_labels(10 + step, step, 1, B, C)
+        xs = synth.make_features(10 + step, step, 1, B, d, labels=ys, dist=dist, sigma=0.045, w_seed=1)
+        x = torch.from_numpy(xs[0]).cuda()
+        y = torch.from_numpy(ys[0]).cuda()
+        gx = torch.empty_like(x)
+        loss = torch.zeros(1, device="cuda")
+        layer.forward_backward(x, y, gx, loss)
+        idx = layer.sampled()
+        dW = layer.sampled_grad()
+        ref = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
+        assert np.array_equal(idx, ref["idx"][0]), "sampled indices differ"
+        results.append((float(loss.item()), ref["loss"], gx.cpu().numpy(), ref["grad_x"][0], dW, ref["dW"][0]))
+        # momentum SGD on the sampled rows (lazy)
+        Wd, Vd = layer.params()
+        W_before = Wd.clone()
+        layer.step(lr)
+        layer.check()
+        Wrows_ref, Vrows_ref = oracle.sgd_momentum_rows(w_rows(idx), np.stack([Vh.get(int(j), np.zeros(d)) for j in idx]),
+                                                        ref["dW"][0], lr, cfg.momentum, cfg.weight_decay)
+        ti = torch.from_numpy(idx).cuda()
+        results[-1] += (Wd[ti].cpu().numpy(), Wrows_ref, Vd[ti].cpu().numpy(), Vrows_ref)
+        mask = torch.ones(C, dtype=torch.bool, device="cuda")
+        mask[ti] = False
+        assert torch.equal(Wd[mask], W_before[mask]), "unsampled rows changed"
+        for t, j in enumerate(idx):
+            Wcur[int(j)] = Wrows_ref[t]
+            Vh[int(j)] = Vrows_ref[t]
+    layer.close()
+    return results
+
+
+@pytest.mark.parametrize("case", FB_CASES, ids=lambda c: f"C{c[0]}-d{c[1]}-B{c[2]}-r{c[3]}-{c[4]}-{c[6]}")
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_forward_backward_step_parity(case, precision):
+    tl, tg = TOL[precision]
+    for (L, Lr, gx, gxr, dW, dWr, Wn, Wnr, Vn, Vnr) in _run_single(case, precision):
+        assert abs(L - Lr) / abs(Lr) <= tl, (L, Lr)
+        assert maxrel(gx, gxr) <= tg
+        assert maxrel(dW, dWr) <= tg
+        # updated rows (lr = 0.1): V within the gradient tolerance; W = W - lr V, so its error is lr times
+        # V's error on top of fp32 rounding of W
+        assert maxrel(Vn, Vnr) <= tg
+        bound = 1e-6 + 0.1 * tg * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+        assert maxrel(Wn, Wnr) <= bound
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_loopback_group_parity(world, precision):
+    C, d, B, r, mt, m = 6007, 128, 24, 0.1, "arcface", 0.5
+    layers = [make_layer(C, d, B, r, mt, m, precision, seed=5, wseed=2, world=world, rank=i, comm="loopback")
+              for i in range(world)]
+    cfg = ocfg(C, d, B, r, mt, m, seed=5, world=world)
+    ys = synth.make_labels(1, 0, world, B, C)
+    xs = synth.make_features(1, 0, world, B, d, labels=ys, dist="trained", w_seed=2)
+    xt = [torch.from_numpy(x).cuda() for x in xs]
+    yt = [torch.from_numpy(y).cuda() for y in ys]
+    gt = [torch.empty_like(x) for x in xt]
+    loss = torch.zeros(1, device="cuda")
+    pfc.group_forward_backward(layers, xt, yt, gt, loss)
+    ref = oracle.forward_backward(cfg, xs, ys, lambda i: synth.w_rows_np(2, i, d), step=0)
+    tl, tg = TOL[precision]
+    assert abs(loss.item() - ref["loss"]) / ref["loss"] <= tl
+    for i, layer in enumerate(layers):
+        assert np.array_equal(layer.sampled(), ref["idx"][i])
+        assert maxrel(gt[i].cpu().numpy(), ref["grad_x"][i]) <= tg
+        assert maxrel(layer.sampled_grad(), ref["dW"][i]) <= tg
+    for layer in layers:
+        layer.close()
+
+
+def test_host_buffer_entry_matches_device_entry():
+    C, d, B = 2000, 128, 32
+    a = make_layer(C, d, B, 0.2, "arcface", 0.5, "bf16", seed=1)
+    b = make_layer(C, d, B, 0.2, "arcface", 0.5, "bf16", seed=1)
+    ys = synth.make_labels(2, 0, 1, B, C)
+    xs = synth.make_features(2, 0, 1, B, d)
+    x = torch.from_numpy(xs[0]).pin_memory()
+    y = torch.from_numpy(ys[0]).pin_memory()
+    gh = torch.empty_like(x).pin_memory()
+    lh = torch.zeros(1).pin_memory()
+    a.forward_backward_host(x, y, gh, lh)
+    gd = torch.empty_like(x, device="cuda")
+    ld = torch.zeros(1, device="cuda")
+    b.forward_backward(x.cuda(), y.cuda(), gd, ld)
+    torch.cuda.synchronize()
+    assert torch.equal(gh, gd.cpu()) and lh.item() == ld.item()
+
+
+def test_device_errors_are_reported():
+    C, d, B = 1000, 128, 8
+    layer = make_layer(C, d, B, 0.1, "arcface", 0.5, "fp32")
+    x = torch.randn(B, d, device="cuda")
+    y = torch.full((B,), C, dtype=torch.int64, device="cuda")  # out of range
+    gx = torch.empty_like(x)
+    layer.forward_backward(x, y, gx)
+    with pytest.raises(pfc.PfcError) as e:
+        layer.check()
+    assert e.value.status == 3
+    y.fill_(1)
+    layer.forward_backward(x, y, gx)
+    layer.step(0.1)
+    with pytest.raises(pfc.PfcError) as e:
+        layer.step(0.1)
+    assert e.value.status == 2
+    layer.close()
