@@ -1,0 +1,354 @@
+#!/usr/bin/env python
+"""Partial FC hot-path benchmark (BASELINE.json metric: samples/s of pfc_forward_backward + pfc_step).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config c4|c2|c3|c3r1|c5]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 --master-port P bench.py --gpus N ...
+
+One step = one forward+backward of the sampled margin-softmax layer (every SURVEY.md §8(a) row: normalise +
+all-gather, PPRN sampling, gather/normalise, logits GEMM + fused margin/LSE partials, global softmax,
+softmax gradient, dX and dW GEMMs, reduce-scatter, x-norm backward) plus the lazy momentum-SGD update, on
+one synthetic batch already resident in HBM. Default workload (N = 1): BASELINE.json configs[3], 10M
+identities, d = 512, B = 256 per GPU, r = 0.1, ArcFace m = 0.5, s = 64, bf16 tensor-core mode; with N GPUs
+the 10M classes are sharded over the N ranks (per-GPU batch fixed: "weak").
+
+Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
+"""
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "PFC fwd+bwd samples/s, 10M ids r=0.1, 1/8×B200; tensor-pipe % of peak"
+CONFIGS = {
+    # name: (C, d, B per GPU, r, margin, m, description)
+    "c4": (10_000_000, 512, 256, 0.1, "arcface", 0.5, "10M identities, d=512, B=256/GPU, r=0.1, ArcFace m=0.5 (BASELINE configs[3])"),
+    "c2": (85_742, 512, 128, 0.1, "arcface", 0.5, "MS1MV2-shaped: C=85,742, d=512, B=128/GPU, r=0.1, ArcFace (BASELINE configs[1])"),
+    "c3": (360_232, 512, 128, 0.1, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=0.1, CosFace m=0.4 (BASELINE configs[2])"),
+    "c3r1": (360_232, 512, 128, 1.0, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=1.0, CosFace m=0.4 (BASELINE configs[2])"),
+    "c5": (100_000_000, 512, 256, 0.1, "arcface", 0.5, "100M identities, d=512, B=256/GPU, r=0.1, ArcFace (BASELINE configs[4])"),
+}
+SCALE = 64.0
+MOMENTUM, WEIGHT_DECAY, LR = 0.9, 5e-4, 0.1
+
+
+def load_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained", d["bf16_tflops"]), "src": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0, "src": "fallback"}
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons with NVML during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x10: "sync_boost", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception as e:  # pragma: no cover - only without NVML
+            self.nv = None
+            self.err = str(e)
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(0.005)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        if not self.nv or not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": float(np.median(self.samples)), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------------ roofline
+def kernel_work(section, M, k, d):
+    """Algorithmic work per launch: (amount, unit, bound)."""
+    if section in ("logits_gemm", "dx_gemm", "dw_gemm"):
+        return 2.0 * M * k * d, "flop", "tensor"
+    if section == "gather_w":
+        return 4.0 * k * d, "byte", "hbm"          # read the sampled fp32 rows once
+    if section == "sgd":
+        return 16.0 * k * d, "byte", "hbm"         # W, V read-modify-write of the sampled rows
+    if section == "softmax_grad":
+        return 4.0 * M * k, "byte", "hbm"          # fp16 cosine in, bf16 gradient out (design minimum)
+    return None
+
+
+def roofline_entry(section, ms, launches, M, k, d, peaks, traffic):
+    w = kernel_work(section, M, k, d)
+    if w is None or launches == 0:
+        return None
+    amount, unit, bound = w
+    t = ms / launches / 1e3
+    if bound == "tensor":
+        achieved = amount / t / 1e12
+        peak = peaks["bf16_tflops_sustained"]
+        u = "TFLOP/s"
+    else:
+        achieved = amount / t / 1e9
+        peak = peaks["hbm_gbs"]
+        u = "GB/s"
+    return {"kernel": section, "bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": u,
+            "frac": round(achieved / peak, 4), "traffic": traffic.get(section),
+            "avg_ms": round(ms / launches, 4), "per_launch": amount,
+            "peak_src": f"{peaks['src']} ({'sustained bf16' if bound == 'tensor' else 'copy'})"}
+
+
+# ------------------------------------------------------------------------------------------------ CPU baseline
+def cpu_baseline(cfgname, budget_s=25.0, steps=1, warm=0):
+    """The oracle (oracle/, float64 numpy, as it stands) on the host cores, on a bounded sample of the
+    workload: B_ref = 8 samples against a contiguous C_ref-class slice of the shard (r, margin, d as the
+    workload), one full step (sampler, forward, backward, momentum SGD) per bench step. Every part of the
+    oracle step scales with the class count, so samples/s of the full workload ~ B_ref (C_ref / C) / t."""
+    import torch
+    import oracle
+    import synth
+    from oracle import OracleConfig
+    C, d, B, r, mt, m, _ = CONFIGS[cfgname]
+    B_ref = 8
+    MT = {"none": 0, "arcface": 1, "cosface": 2}
+
+    def one(C_ref, step):
+        cfg = OracleConfig(num_classes=C_ref, dim=d, batch=B_ref, sample_rate=r, scale=SCALE, margin_type=MT[mt],
+                           margin=m, momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, seed=0)
+        ys = synth.make_labels(0, step, 1, B_ref, C_ref)
+        xs = synth.make_features(0, step, 1, B_ref, d)
+        idx, _ = oracle.sample_shard(ys[0], 0, C_ref, r, 0, step)   # untimed: only to pre-generate input rows
+        rows = synth.w_rows_np(1, idx, d)
+        cache = {"ids": idx, "rows": rows}
+
+        def w_rows(ids):
+            ids = np.asarray(ids)
+            if ids.shape == cache["ids"].shape and np.array_equal(ids, cache["ids"]):
+                return cache["rows"]
+            return synth.w_rows_np(1, ids, d)
+        t0 = time.perf_counter()
+        out = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
+        oracle.sgd_momentum_rows(rows, np.zeros_like(rows), out["dW"][0], LR, MOMENTUM, WEIGHT_DECAY)
+        return time.perf_counter() - t0
+
+    probe_c = min(C, 100_000)
+    tp = one(probe_c, 0)
+    per_class = tp / probe_c
+    C_ref = int(min(C, max(20_000, budget_s / max(steps, 1) / per_class)))
+    times = []
+    for i in range(warm + steps):
+        t = one(C_ref, i + 1)
+        if i >= warm:
+            times.append(t)
+    t = float(np.mean(times))
+    value = B_ref * (C_ref / C) / t
+    return {"value": value, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "oracle",
+            "sample": f"{B_ref} samples x {C_ref}-class slice of the {C}-class shard per step (r={r}, d={d}), "
+                      f"full oracle step (sampler, fwd, bwd, SGD) in float64 numpy; value = {B_ref}*({C_ref}/{C})/"
+                      f"{t:.3f}s, i.e. scaled to the full workload by class count; {len(times)} step(s)",
+            "seconds_per_step": t}
+
+
+# ------------------------------------------------------------------------------------------------ main
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget", type=float, default=20.0)
+    args = ap.parse_args()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    C, d, B, r, mt, m, desc = CONFIGS[args.config]
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        budget = max(30.0, 150.0 / max(1, args.steps + args.warmup)) * (args.steps + args.warmup)
+        cb = cpu_baseline(args.config, budget_s=min(budget, 150.0), steps=args.steps, warm=args.warmup)
+        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": {"workload": desc, "oracle": "oracle/pfc.py (float64 numpy, CPU)"},
+                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
+                "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import torch.distributed as dist
+    import synth
+    import paper_2010_05222_b200 as pfc
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    layer = pfc.PartialFC.from_process_group(**dict(
+        num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m, momentum=MOMENTUM,
+        weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local)) if world > 1 else \
+        pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m,
+                      momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local)
+    W, V = layer.params()
+    synth.fill_w_shard(W, 1, layer.shard_start)
+    V.zero_()
+    M, k = layer.global_batch, layer.k_max
+    # synthetic init-like batches, resident in HBM before the timed region
+    NB = 4
+    xs, ys = [], []
+    for i in range(NB):
+        yl = synth.make_labels(77, i, world, B, C)[rank]
+        xl = synth.make_features(77, i, world, B, d)[rank]
+        xs.append(torch.from_numpy(xl).cuda())
+        ys.append(torch.from_numpy(yl).cuda())
+    gx = torch.empty(B, d, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def step(i):
+        layer.forward_backward(xs[i % NB], ys[i % NB], gx, loss, stream)
+        layer.step(LR, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    layer.check()
+
+    # ---------------- timed region (device-resident inputs)
+    layer.profile(True)
+    l0 = layer.launch_count()
+    barrier()
+    torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    barrier()
+    ms_total = ev0.elapsed_time(ev1)
+    launches = layer.launch_count() - l0
+    prof = layer.profile_read()
+    layer.profile(False)
+    loss_val = float(loss.item())
+    layer.check()
+    t = torch.tensor([ms_total], device="cuda")
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = M * args.steps / (ms_max / 1e3)
+
+    # ---------------- end-to-end through the C-ABI with host buffers (pinned), copies inside the timed region
+    xh = [x.cpu().pin_memory() for x in xs]
+    yh = [y.cpu().pin_memory() for y in ys]
+    gh = torch.empty(B, d).pin_memory()
+    lh = torch.zeros(1).pin_memory()
+    for i in range(2):
+        layer.forward_backward_host(xh[i % NB], yh[i % NB], gh, lh, stream)
+        layer.step(LR, stream)
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.steps):
+        layer.forward_backward_host(xh[i % NB], yh[i % NB], gh, lh, stream)
+        layer.step(LR, stream)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    te = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e2e_value = M * args.steps / (float(te.item()) / 1e3)
+
+    if rank == 0:
+        peaks = load_peaks()
+        traffic = {}
+        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tp):
+            tj = json.load(open(tp))
+            if tj.get("workload") == args.config and tj.get("n_gpus", 1) == world:
+                traffic = tj.get("bytes_per_launch", {})
+        entries = [e for e in (roofline_entry(s, ms, n, M, k, d, peaks, traffic) for s, (ms, n) in prof.items()) if e]
+        dominant = max(prof.items(), key=lambda kv: kv[1][0])[0]
+        dom = next((e for e in entries if e["kernel"] == dominant), None)
+        if dom is None and entries:
+            dom = max(entries, key=lambda e: e["avg_ms"])
+        step_ms = ms_total / args.steps
+        sections = {s: {"ms_per_step": round(ms / args.steps, 4), "share": round(ms / ms_total, 4)}
+                    for s, (ms, n) in prof.items() if n}
+        line = {
+            "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
+            "config": {"workload": desc, "num_classes": C, "dim": d, "batch_per_gpu": B, "global_batch": M,
+                       "sample_rate": r, "k_per_gpu": k, "shard_rows": layer.shard_size, "margin": f"{mt} {m}",
+                       "scale": SCALE, "parallelism": f"class-parallel x{world}",
+                       "l2": "inputs larger than L2 (W+V shard %.1f GB, %.1f GB of sampled rows per step)"
+                             % (2 * layer.shard_size * d * 4 / 1e9, k * d * 4 / 1e9)},
+            "clocks": clk.summary(),
+            "e2e": {"value": round(e2e_value, 1), "unit": "samples/s", "h2d_bytes_per_step": B * d * 4 + B * 8,
+                    "d2h_bytes_per_step": B * d * 4 + 4},
+            "gpu_launches": launches,
+            "roofline": {kk: dom[kk] for kk in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | {
+                "kernel": dom["kernel"], "peak_src": dom["peak_src"]} if dom else None,
+            "kernels": entries, "sections": sections, "loss": loss_val,
+            "step_ms_rank0": round(step_ms, 4),
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            cb = cpu_baseline(args.config, budget_s=args.cpu_budget)
+            line["cpu_baseline"] = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -176,6 +176,20 @@ pfc_status pfc_sample_shard(int64_t num_classes, int32_t world_size, int32_t ran
                             uint64_t step, const int64_t* labels_dev, int32_t M, int64_t* idx_dev, int64_t* k_out,
                             void* stream);
 
+/* ------------------------------------------------------------------------------------------------------
+ * Per-kernel timing (CUDA events recorded on the launching stream between the kernels of the step)
+ * ---------------------------------------------------------------------------------------------------- */
+#define PFC_PROF_SECTIONS 10
+/* Sections: 0 normalize_x (+all-gather), 1 sampler, 2 gather_w (+target cos), 3 logits GEMM, 4 row combine +
+ * all-reduces + finalize, 5 softmax_grad, 6 dx GEMM, 7 reduce-scatter + x-norm backward, 8 dw GEMM, 9 sgd. */
+/* Enables (1) or disables (0) event recording; clears the accumulators. Not for loopback groups. */
+pfc_status pfc_profile_enable(pfc_ctx* ctx, int32_t enable);
+/* Synchronises, adds the elapsed time of every recorded step to ms[PFC_PROF_SECTIONS] (milliseconds) and the
+ * number of recorded launches to count[PFC_PROF_SECTIONS], then clears the record. */
+pfc_status pfc_profile_read(pfc_ctx* ctx, double* ms, int64_t* count);
+/* Name of section i, or NULL. */
+const char* pfc_profile_section(int32_t i);
+
 /* Number of kernels this library launched since init (each launch counted once). */
 int64_t pfc_launch_count(const pfc_ctx* ctx);
 

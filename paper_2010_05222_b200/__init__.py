@@ -29,7 +29,9 @@ STATUS = {0: "PFC_OK", 1: "PFC_ERR_CONFIG", 2: "PFC_ERR_CONTRACT", 3: "PFC_ERR_D
 EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pfc_forward_backward",
            "pfc_forward_backward_host", "pfc_step", "pfc_shard_range", "pfc_sizes", "pfc_param_ptrs",
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
-           "pfc_launch_count", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard"]
+           "pfc_launch_count", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
+           "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section"]
+PROF_SECTIONS = 10
 
 
 class PfcError(RuntimeError):
@@ -80,6 +82,9 @@ def load_library(path=LIB_PATH):
         "pfc_check": (st, [VP]),
         "pfc_launch_count": (I64, [VP]),
         "pfc_version": (ctypes.c_char_p, []),
+        "pfc_profile_enable": (st, [VP, ctypes.c_int32]),
+        "pfc_profile_read": (st, [VP, P(ctypes.c_double), P(I64)]),
+        "pfc_profile_section": (ctypes.c_char_p, [ctypes.c_int32]),
         "pfc_group_forward_backward": (st, [P(VP), ctypes.c_int32, P(VP), P(VP), P(VP), VP, VP]),
         "pfc_sample_shard": (st, [I64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, U64, U64, VP, ctypes.c_int32,
                                   VP, P(I64), VP]),
@@ -236,6 +241,17 @@ class PartialFC:
 
     def check(self):
         self._check(self._lib.pfc_check(self._h))
+
+    def profile(self, enable=True):
+        """Record CUDA events between the kernels of every following step (pfc_profile_enable)."""
+        self._check(self._lib.pfc_profile_enable(self._h, 1 if enable else 0))
+
+    def profile_read(self):
+        """{section: (total_ms, launches)} accumulated since the last read (synchronises)."""
+        ms = (ctypes.c_double * PROF_SECTIONS)()
+        cnt = (ctypes.c_int64 * PROF_SECTIONS)()
+        self._check(self._lib.pfc_profile_read(self._h, ms, cnt))
+        return {self._lib.pfc_profile_section(i).decode(): (ms[i], cnt[i]) for i in range(PROF_SECTIONS)}
 
     def launch_count(self):
         return int(self._lib.pfc_launch_count(self._h))

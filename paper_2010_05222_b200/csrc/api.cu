@@ -12,6 +12,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <array>
 #include <vector>
 
 #include "pfc_internal.cuh"
@@ -65,6 +66,7 @@ struct pfc_ctx {
   float* zt = nullptr;         // M
   float* red = nullptr;        // M + 1
   float* lse = nullptr;        // M
+  float* gt = nullptr;         // M, p_t - 1 per row
   float* loss_dev = nullptr;   // 1 (scratch when the caller passes NULL)
   void* G = nullptr;           // M x k_pad (bf16 or fp32)
   // gradients
@@ -77,6 +79,13 @@ struct pfc_ctx {
   float* x_in = nullptr;
   int64_t* y_in = nullptr;
   float* gx_out = nullptr;
+  // per-kernel event timing (pfc_profile_*)
+  bool prof = false;
+  std::vector<std::array<cudaEvent_t, PFC_PROF_SECTIONS + 1>> prof_ev;
+  std::vector<std::array<bool, PFC_PROF_SECTIONS + 1>> prof_set;
+  size_t prof_used = 0;
+  std::array<cudaEvent_t, PFC_PROF_SECTIONS + 1>* prof_cur = nullptr;
+  std::array<bool, PFC_PROF_SECTIONS + 1>* prof_cur_set = nullptr;
 };
 
 namespace {
@@ -252,7 +261,8 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->gmax, M * 4);
   ALLOC(c->rowsum, M * 4);
   ALLOC(c->zt, M * 4);
-  ALLOC(c->red, (M + 1) * 4);
+  ALLOC(c->red, 2 * M * 4);
+  ALLOC(c->gt, M * 4);
   ALLOC(c->lse, M * 4);
   ALLOC(c->loss_dev, 16);
   ALLOC(c->G, M * kp * esz);
@@ -296,6 +306,8 @@ pfc_status pfc_destroy(pfc_ctx* c) {
   cudaSetDevice(c->cfg.device);
   cudaDeviceSynchronize();
   if (c->comm) ncclCommDestroy(c->comm);
+  for (auto& ev : c->prof_ev)
+    for (auto& e : ev) cudaEventDestroy(e);
   for (void* p : c->allocs) cudaFree(p);
   delete c;
   return PFC_OK;
@@ -314,6 +326,27 @@ pfc_status check_fb_args(pfc_ctx* c, const float* x, const int64_t* labels, floa
   return PFC_OK;
 }
 
+// Event boundary b of the current step (b = section index; b + 1 closes it).
+void mark(pfc_ctx* c, int b, cudaStream_t s) {
+  if (!c->prof || !c->prof_cur) return;
+  cudaEventRecord((*c->prof_cur)[b], s);
+  (*c->prof_cur_set)[b] = true;
+}
+
+void prof_begin_step(pfc_ctx* c) {
+  if (!c->prof) return;
+  if (c->prof_used == c->prof_ev.size()) {
+    std::array<cudaEvent_t, PFC_PROF_SECTIONS + 1> ev;
+    for (auto& e : ev) cudaEventCreate(&e);
+    c->prof_ev.push_back(ev);
+    c->prof_set.emplace_back();
+  }
+  c->prof_cur = &c->prof_ev[c->prof_used];
+  c->prof_cur_set = &c->prof_set[c->prof_used];
+  c->prof_cur_set->fill(false);
+  c->prof_used++;
+}
+
 // K1: normalise this rank's features into its all-gather slot; copy labels into theirs.
 void phase_a(pfc_ctx* c, const float* x, const int64_t* labels, cudaStream_t s) {
   c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, s);
@@ -324,22 +357,26 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
   const Sizes& sz = c->sz;
   const bool bf = c->bf16;
   int n = 0;
+  mark(c, 1, s);
   if (bf) n += launch_x_to_bf16(sz, c->X32, c->Xb, s);
   n += launch_sampler(sz, c->Y, c->cfg.seed, (uint32_t)c->step, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
                       c->tcol, c->err_dev, s);
+  mark(c, 2, s);
   n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
   n += launch_target_cos(sz, c->X32, c->W, c->idx, c->tcol, c->inv_norm, c->ct, s);
+  mark(c, 3, s);
   if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);
   else
     n += launch_logits_simt(sz, bf, bf ? (const void*)c->Xb : (const void*)c->X32, c->Ws, c->tcol, c->ct, c->st, c->mp,
                             c->cosv, c->partials, s);
+  mark(c, 4, s);
   n += launch_row_combine(sz, c->partials, c->tcol, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, s);
   c->launches += n;
 }
 
-// after all-reduce MAX: red[n] = l_n e^{m_n - gm_n}, red[M] = local sum of target logits
+// after all-reduce MAX: red[n] = l_n e^{m_n - gm_n} (non-target columns), red[M + n] = local z_t
 void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
   c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->red, s);
 }
@@ -348,8 +385,10 @@ void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
 void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
-  n += launch_finalize(sz, gmax, c->red, c->lse, loss_out, c->err_dev, s);
-  n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->tcol, c->ct, c->st, c->mp, c->G, s);
+  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->err_dev, s);
+  mark(c, 5, s);
+  n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G, s);
+  mark(c, 6, s);
   if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
   else
@@ -362,10 +401,12 @@ void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
   n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
+  mark(c, 8, s);
   if (c->use_tc)
     n += launch_dw_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, c->dWh, s);
   else
     n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
+  mark(c, 9, s);
   c->launches += n;
 }
 
@@ -395,6 +436,8 @@ pfc_status pfc_forward_backward(pfc_ctx* c, const float* x, const int64_t* label
   const bool multi = sz.world > 1;
   float* loss_out = loss ? loss : c->loss_dev;
 
+  prof_begin_step(c);
+  mark(c, 0, s);
   phase_a(c, x, labels, s);
   if (multi) {  // Alg.1 L2: X = allgather(x_i) (+ labels)
     NCCL_TRY(c, ncclGroupStart());
@@ -409,8 +452,9 @@ pfc_status pfc_forward_backward(pfc_ctx* c, const float* x, const int64_t* label
     gmax = c->gmax;
   }
   phase_c(c, gmax, s);
-  if (multi) NCCL_TRY(c, ncclAllReduce(c->red, c->red, sz.M + 1, ncclFloat, ncclSum, c->comm, s));
+  if (multi) NCCL_TRY(c, ncclAllReduce(c->red, c->red, 2 * sz.M, ncclFloat, ncclSum, c->comm, s));
   phase_d(c, gmax, loss_out, s);
+  mark(c, 7, s);
   const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
   if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
     NCCL_TRY(c, ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
@@ -435,6 +479,7 @@ pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* co
     if (a != PFC_OK) return a;
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  for (int r = 0; r < n; ++r) ctxs[r]->prof_cur = nullptr;  // no event timing in loopback groups
   const Sizes& sz = ctxs[0]->sz;
   const size_t rowbytes = (size_t)sz.B * sz.d * 4;
   pfc_ctx* c0 = ctxs[0];
@@ -453,7 +498,7 @@ pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* co
   c0->launches += launch_group_reduce(sz.M, src, 0, dst, n, n, 1, s);
   for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
   for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->red; dst.p[r] = ctxs[r]->red; }
-  c0->launches += launch_group_reduce(sz.M + 1, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
+  c0->launches += launch_group_reduce(2 * sz.M, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
   for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, s);
   for (int r = 0; r < n; ++r) src.p[r] = ctxs[r]->dXh;
   for (int r = 0; r < n; ++r) {  // reduce-scatter: owner r sums rows [rB, (r+1)B) over ranks
@@ -490,8 +535,13 @@ pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
   if (!c->fb_done) return set_err(c, PFC_ERR_CONTRACT, "pfc_step without a preceding pfc_forward_backward");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   c->last_stream = s;
+  if (c->prof) {
+    prof_begin_step(c);
+    mark(c, 9, s);
+  }
   c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, lr, c->cfg.momentum,
                             c->cfg.weight_decay, s);
+  if (c->prof) mark(c, 10, s);
   CUDA_TRY(c, cudaGetLastError());
   c->fb_done = false;
   if (c->sync_check) {
@@ -589,6 +639,41 @@ pfc_status pfc_set_step(pfc_ctx* c, uint64_t step) {
 }
 
 int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
+
+static const char* kSectionNames[PFC_PROF_SECTIONS] = {
+    "normalize_x", "sampler", "gather_w", "logits_gemm", "row_lse", "softmax_grad", "dx_gemm", "xnorm_backward",
+    "dw_gemm", "sgd"};
+
+const char* pfc_profile_section(int32_t i) { return (i >= 0 && i < PFC_PROF_SECTIONS) ? kSectionNames[i] : nullptr; }
+
+pfc_status pfc_profile_enable(pfc_ctx* c, int32_t enable) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  c->prof = enable != 0;
+  c->prof_used = 0;
+  c->prof_cur = nullptr;
+  return PFC_OK;
+}
+
+pfc_status pfc_profile_read(pfc_ctx* c, double* ms, int64_t* count) {
+  if (!c || !ms || !count) return set_err(c, PFC_ERR_CONTRACT, "NULL argument");
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  for (size_t st = 0; st < c->prof_used; ++st) {
+    auto& ev = c->prof_ev[st];
+    auto& set = c->prof_set[st];
+    for (int b = 0; b < PFC_PROF_SECTIONS; ++b) {
+      if (!set[b] || !set[b + 1]) continue;
+      float t = 0.f;
+      if (cudaEventElapsedTime(&t, ev[b], ev[b + 1]) == cudaSuccess) {
+        ms[b] += t;
+        count[b] += 1;
+      }
+    }
+  }
+  cudaGetLastError();
+  c->prof_used = 0;
+  c->prof_cur = nullptr;
+  return PFC_OK;
+}
 
 pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, uint64_t seed, uint64_t step,
                             const int64_t* labels, int32_t M, int64_t* idx_out, int64_t* k_out, void* stream) {

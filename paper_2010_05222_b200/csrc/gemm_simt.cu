@@ -117,19 +117,18 @@ __global__ void __launch_bounds__(256) k_gemm(int Mdim, int64_t Ndim, int64_t Kd
         } else {
           if (rv && p < Ndim) ((float*)e.cosv)[n * Ndim + p] = c;
         }
-        float zz = mp.s * c;
-        if (p == tc) zz = mp.s * margin_phi(mp, e.ct[n]);
-        z[j] = (p < Nlim) ? zz : -INFINITY;
+        // the target column is excluded from the partials (finalize adds it exactly, see rows.cu)
+        z[j] = (p < Nlim && p != tc) ? mp.s * c : -INFINITY;
         zmax = fmaxf(zmax, z[j]);
       }
 #pragma unroll
       for (int o = 8; o; o >>= 1) zmax = fmaxf(zmax, __shfl_xor_sync(0xffffffffu, zmax, o));
       float l = 0.f;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) l += (z[j] > -INFINITY) ? __expf(z[j] - zmax) : 0.f;
+      for (int j = 0; j < 4; ++j) l += (z[j] > -INFINITY) ? __expf(z[j] - zmax) : 0.f;  // zmax finite here
 #pragma unroll
       for (int o = 8; o; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-      if (rv && tx == 0) e.partials[n * e.ntiles + blockIdx.x] = make_float2(zmax, l);
+      if (rv && tx == 0) e.partials[n * e.ntiles + blockIdx.x] = make_float2(zmax, zmax > -INFINITY ? l : 0.f);
     }
   } else if (MODE == MODE_ATOMIC) {
 #pragma unroll

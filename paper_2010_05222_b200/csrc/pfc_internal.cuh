@@ -125,10 +125,11 @@ int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* t
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
                     float* red, cudaStream_t s);
-int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* loss_out, int* err,
-                    cudaStream_t s);
-int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const int32_t* tcol,
-                        const float* ct, const SamplerState* st, MarginParams mp, void* G, cudaStream_t s);
+int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
+                    int* err, cudaStream_t s);
+int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
+                        const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
+                        cudaStream_t s);
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
                           float* grad_x, cudaStream_t s);
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,

@@ -139,36 +139,45 @@ __global__ void k_row_combine(int M, int ntiles, int ltile, const float2* __rest
   }
 }
 
-// red[n] = rowsum[n] e^{rowmax[n] - gmax[n]} (n < M); red[M] = sum of the local target logits.
-__global__ void __launch_bounds__(1024) k_prep_sum(int M, const float* __restrict__ rowmax,
-                                                   const float* __restrict__ gmax, const float* __restrict__ rowsum,
-                                                   const float* __restrict__ zt, float* __restrict__ red) {
-  __shared__ float sh[32];
-  float acc = 0.f;
-  for (int n = threadIdx.x; n < M; n += blockDim.x) {
-    float rm = rowmax[n];
-    red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
-    acc += zt[n];
-  }
-  acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
-  __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[M] = v;
-  }
+// The per-tile partials exclude each row's target column (its logit z_t = s phi(c_t) is known exactly
+// from K5b), so that the loss and the target gradient can be formed without cancellation when p_t -> 1:
+//   q_n = sum_{j != t} e^{z_j - z_t},  loss_n = log1p(q_n),  p_t - 1 = -q_n / (1 + q_n).
+// red[n] = l_n e^{m_n - gm_n} (sum over non-target columns relative to the global non-target max);
+// red[M + n] = z_t of row n if its class is on this rank, else 0 (the all-reduce SUM gathers it).
+__global__ void k_prep_sum(int M, const float* __restrict__ rowmax, const float* __restrict__ gmax,
+                           const float* __restrict__ rowsum, const float* __restrict__ zt, float* __restrict__ red) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= M) return;
+  const float rm = rowmax[n];
+  red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
+  red[M + n] = zt[n];
 }
 
-// LSE_n = gmax_n + log(gsum_n); loss = (sum_n LSE_n - sum_n z_t) / M   (Eq.5 over the global batch, R13)
+// Global LSE_n, loss (Eq.5 over the global batch, R13) and g_t[n] = p_t - 1 for K8.
 __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restrict__ gmax, const float* __restrict__ red,
-                                                   float* __restrict__ lse, float* __restrict__ loss_out, int* err) {
+                                                   float* __restrict__ lse, float* __restrict__ gt,
+                                                   float* __restrict__ loss_out, int* err) {
   __shared__ float sh[32];
   float acc = 0.f;
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
-    float v = gmax[n] + __logf(red[n]);
-    lse[n] = v;
-    acc += v;
+    const float gm = gmax[n], S = red[n], z = red[M + n];
+    float L, g, ls;
+    if (!(gm > -INFINITY) || S == 0.f) {          // no negative in the sampled set: p_t = 1
+      ls = z; L = 0.f; g = 0.f;
+    } else if (z >= gm) {
+      const float q = S * __expf(gm - z);
+      L = log1pf(q);
+      ls = z + L;
+      g = -q / (1.f + q);
+    } else {
+      const float t = __expf(z - gm);
+      ls = gm + __logf(S + t);
+      L = ls - z;
+      g = t / (S + t) - 1.f;
+    }
+    lse[n] = ls;
+    gt[n] = g;
+    acc += L;
   }
   acc = warp_sum(acc);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
@@ -177,9 +186,9 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
     float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
     v = warp_sum(v);
     if (threadIdx.x == 0) {
-      float L = (v - red[M]) / (float)M;
-      if (loss_out) *loss_out = L;
-      if (!isfinite(L)) atomicOr(err, ERR_NUMERIC);
+      float Lm = v / (float)M;
+      if (loss_out) *loss_out = Lm;
+      if (!isfinite(Lm)) atomicOr(err, ERR_NUMERIC);
     }
   }
 }
@@ -187,9 +196,9 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
 // ---------------------------------------------------------------- K8: softmax gradient, 8 columns per thread
 template <bool BF16>
 __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, const void* __restrict__ cosv,
-                                                      const float* __restrict__ lse, const int32_t* __restrict__ tcol,
-                                                      const float* __restrict__ ct, const SamplerState* st,
-                                                      MarginParams mp, void* __restrict__ G) {
+                                                      const float* __restrict__ lse, const float* __restrict__ gt,
+                                                      const int32_t* __restrict__ tcol, const float* __restrict__ ct,
+                                                      const SamplerState* st, MarginParams mp, void* __restrict__ G) {
   const int n = blockIdx.y;
   const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
   if (c0 >= k_pad) return;
@@ -217,9 +226,7 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, cons
     const int64_t col = c0 + i;
     if (col < k) {
       if (col == tc) {
-        float ctv = ct[n];
-        float p = exp2f(mp.s * margin_phi(mp, ctv) * L2E - off);
-        g[i] = gs * (p - 1.f) * margin_dphi(mp, ctv);
+        g[i] = gs * gt[n] * margin_dphi(mp, ct[n]);   // (p_t - 1) phi'(c_t), cancellation-free
       } else {
         g[i] = gs * exp2f(c[i] * sl - off);
       }
@@ -334,21 +341,22 @@ int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* t
 
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
                     float* red, cudaStream_t s) {
-  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, rowmax, gmax, rowsum, zt, red);
+  k_prep_sum<<<(sz.M + 255) / 256, 256, 0, s>>>(sz.M, rowmax, gmax, rowsum, zt, red);
   return 1;
 }
 
-int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* loss_out, int* err,
-                    cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, loss_out, err);
+int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
+                    int* err, cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, err);
   return 1;
 }
 
-int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const int32_t* tcol,
-                        const float* ct, const SamplerState* st, MarginParams mp, void* G, cudaStream_t s) {
+int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
+                        const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
+                        cudaStream_t s) {
   dim3 grid((unsigned)((sz.k_pad / 8 + 255) / 256), sz.M);
-  if (bf16) k_softmax_grad<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, tcol, ct, st, mp, G);
-  else k_softmax_grad<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, tcol, ct, st, mp, G);
+  if (bf16) k_softmax_grad<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G);
+  else k_softmax_grad<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G);
   return 1;
 }
 
