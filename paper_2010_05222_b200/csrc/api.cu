@@ -268,7 +268,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->G, M * kp * esz);
   ALLOC(c->dXh, Mp * d * 4);
   ALLOC(c->dxh_local, B * d * 4);
-  ALLOC(c->split_ws, (size_t)64 * Mp * d * 4);
+  ALLOC(c->split_ws, (size_t)(c->use_tc ? dx_split_ws_floats(sz) : 1) * 4);
   ALLOC(c->dWh, kp * d * 4);
   ALLOC(c->err_dev, 16);
   ALLOC(c->x_in, B * d * 4);

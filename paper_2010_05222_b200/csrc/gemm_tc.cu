@@ -1,12 +1,561 @@
-// tcgen05 / TMEM / TMA bf16 contractions for sm_100a (placeholder until the tensor-core kernels land).
+// tcgen05 / TMEM / TMA bf16 contractions of the Partial FC step (sm_100a).
+//
+//   K6  logits  C[M x k]  = X_hat[M x d] . W_s[k x d]^T     A K-major, B K-major   (Alg.1 L3)
+//       epilogue: fp16 cosine store, margin-free scaled logits z = s c, per-(row, 128-column tile) max and
+//       sum of e^{z - max} excluding the row's target column (finalize adds it exactly; rows.cu)
+//   K9  dX      dX[M x d] = Gc[M x k] . W_s[k x d]          A K-major, B MN-major  (Alg.1 L12)
+//       split-K over the sampled classes, fp32 partial per split, deterministic reduction kernel
+//   K11 dW      dW[k x d] = Gc^T[k x M] . X_hat[M x d]      A MN-major, B MN-major (Alg.1 L10)
+//
+// One kernel template: a persistent, warp-specialised CTA (warp 0: TMA producer, warp 1: TMEM allocator and
+// single-thread MMA issuer, warps 2-5: epilogue reading the fp32 accumulator from TMEM with tcgen05.ld).
+// Operands are staged by TMA (cp.async.bulk.tensor, 128-byte swizzle) into a STAGES-deep smem ring guarded by
+// mbarriers; tcgen05.mma (kind::f16, bf16 x bf16 -> fp32, cta_group::1, M = 128 per instruction) accumulates
+// into TMEM; tcgen05.commit releases smem stages and signals the epilogue; the accumulator is double-buffered
+// in TMEM when it fits so that the epilogue of tile t overlaps the MMAs of tile t + 1.
+#include <cuda.h>
+#include <algorithm>
+#include <cstdio>
+#include <mutex>
+
 #include "pfc_internal.cuh"
 
 namespace pfc {
-bool tc_available() { return false; }
-int launch_logits_tc(const Sizes&, const __nv_bfloat16*, const __nv_bfloat16*, const int32_t*, const float*,
-                     const SamplerState*, MarginParams, __half*, float2*, cudaStream_t) { return 0; }
-int launch_dx_tc(const Sizes&, const __nv_bfloat16*, const __nv_bfloat16*, const SamplerState*, float*, float*,
-                 cudaStream_t) { return 0; }
-int launch_dw_tc(const Sizes&, const __nv_bfloat16*, const __nv_bfloat16*, const SamplerState*, float*,
-                 cudaStream_t) { return 0; }
+namespace {
+
+// ------------------------------------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ok = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::"r"(
+          smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tc_mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(
+          tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+
+// 32 lanes x 32 consecutive 32-bit columns: thread t of the warp gets lane (32*(warp%4) + t), columns col..col+31
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,"
+      "%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]), "=r"(v[8]),
+        "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]),
+        "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1 (sm_100).
+//   K-major   : rows of 64 bf16 (128 B), 8-row atoms 1024 B apart (SBO), LBO unused (16 B)
+//   MN-major  : 64-element MN chunks of BK rows; SBO = 1024 (8 K-rows), LBO = chunk stride
+__device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;   // descriptor version (Blackwell)
+  d |= (uint64_t)2 << 61;   // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N >> 3, M >> 4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                       // c_format = F32
+         | (1u << 7)                     // a_format = BF16
+         | (1u << 10)                    // b_format = BF16
+         | ((a_mn ? 1u : 0u) << 15)      // a_major
+         | ((b_mn ? 1u : 0u) << 16)      // b_major
+         | ((uint32_t)(N >> 3) << 17)    // n_dim
+         | ((uint32_t)(M >> 4) << 24);   // m_dim
+}
+
+// ------------------------------------------------------------------------------------------------ kernel
+enum Kind { LOGITS = 0, DX = 1, DW = 2, DX128 = 3, DW128 = 4 };  // *128: d-tile 128 (d % 256 != 0)
+__host__ __device__ constexpr int base_kind(int k) { return k == DX128 ? DX : k == DW128 ? DW : k; }
+
+constexpr int BK = 64;          // K elements per stage (128 B of bf16: one swizzle row)
+constexpr int NUM_THREADS = 192;
+
+template <int KIND>
+struct Cfg;
+template <>
+struct Cfg<LOGITS> {  // tile 256 x 128 (two M = 128 halves sharing the B tile), K = d
+  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 128, STAGES = 4, ACC = 2;
+  static constexpr bool A_MN = false, B_MN = false;
+};
+template <>
+struct Cfg<DX> {      // tile 256 x 256 (M halves x d half), K = a split of the sampled classes
+  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 256, STAGES = 3, ACC = 1;
+  static constexpr bool A_MN = false, B_MN = true;
+};
+template <>
+struct Cfg<DW> {      // tile 128 classes x 256 dims, K = M (the global batch)
+  static constexpr int MSUB = 1, NMMA = 1, UMMA_N = 256, STAGES = 4, ACC = 2;
+  static constexpr bool A_MN = true, B_MN = true;
+};
+template <>
+struct Cfg<DX128> : Cfg<DX> { static constexpr int UMMA_N = 128, STAGES = 4; };
+template <>
+struct Cfg<DW128> : Cfg<DW> { static constexpr int UMMA_N = 128; };
+
+template <int KIND>
+struct Smem {
+  using C = Cfg<KIND>;
+  static constexpr int A_BYTES = C::MSUB * 128 * BK * 2;            // per stage
+  static constexpr int B_BYTES = C::NMMA * C::UMMA_N * BK * 2;      // per stage
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int TMEM_COLS = C::MSUB * C::NMMA * C::UMMA_N * C::ACC;
+  static constexpr int TOTAL = C::STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static_assert(TMEM_COLS <= 512, "TMEM overflow");
+};
+
+struct TcParams {
+  int M;                 // global batch rows
+  int d;
+  int64_t k_pad;
+  const SamplerState* st;
+  // logits epilogue
+  const int32_t* tcol;
+  float s_log2e;         // s * log2(e)
+  __half* cosv;          // M x k_pad
+  float2* partials;      // M x n_ltiles
+  int n_ltiles;
+  // dx epilogue
+  float* split_ws;       // nsplit x M x d
+  int nsplit;
+  int kb_per_split;
+  // dw epilogue
+  float* dWh;            // k_pad x d
+};
+
+// Work decomposition shared by all roles (identical sequence on every warp of the CTA).
+template <int KIND_>
+struct Work {
+  static constexpr int KIND = base_kind(KIND_);
+  static constexpr int NT = Cfg<KIND_>::UMMA_N;
+  int n_units, n_kb;
+  int mt, nt;  // tiles along M / N (or units for DX)
+  __device__ Work(const TcParams& p, int k) {
+    using C = Cfg<KIND_>;
+    if (KIND == LOGITS) {
+      mt = (p.M + 255) / 256;
+      nt = (k + 127) / 128;
+      n_units = mt * nt;
+      n_kb = p.d / BK;
+    } else if (KIND == DX) {
+      mt = (p.M + 255) / 256;
+      nt = p.d / NT;
+      n_units = mt * nt * p.nsplit;
+      n_kb = (k + BK - 1) / BK;  // total k-blocks over the sampled classes
+    } else {
+      mt = (k + 127) / 128;      // class tiles
+      nt = p.d / NT;
+      n_units = mt * nt;
+      n_kb = (p.M + BK - 1) / BK;
+    }
+    (void)C::MSUB;
+  }
+  // unit -> (m0, n0, kb_begin, kb_end)
+  __device__ void decode(const TcParams& p, int u, int& m0, int& n0, int& kb0, int& kb1) const {
+    if (KIND == LOGITS) {
+      const int nb = u / mt, mb = u % mt;  // M fastest: concurrent CTAs share the B (W_s) tile in L2
+      m0 = mb * 256; n0 = nb * 128; kb0 = 0; kb1 = n_kb;
+    } else if (KIND == DX) {
+      const int sp = u / (mt * nt), r = u % (mt * nt);
+      const int nb = r / mt, mb = r % mt;
+      m0 = mb * 256; n0 = nb * NT;
+      kb0 = sp * p.kb_per_split;
+      kb1 = min(n_kb, kb0 + p.kb_per_split);
+    } else {
+      const int cb = u / nt, nb = u % nt;  // both d-halves of a class tile adjacent: A (G) slice hits L2
+      m0 = cb * 128; n0 = nb * NT; kb0 = 0; kb1 = n_kb;
+    }
+  }
+};
+
+template <int KIND_>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+    k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+  constexpr int KIND = base_kind(KIND_);
+  using C = Cfg<KIND_>;
+  using S = Smem<KIND_>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * S::STAGE_BYTES);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* acc_full = empty + C::STAGES;
+  uint64_t* acc_empty = acc_full + C::ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::ACC);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = p.st->k;
+  const Work<KIND_> w(p, k);
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < C::ACC; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(S::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------------ TMA producer (lane 0 issues)
+    {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
+        int m0, n0, kb0, kb1;
+        w.decode(p, u, m0, n0, kb0, kb1);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (lane == 0) {
+          mbar_expect_tx(&full[stage], S::STAGE_BYTES);
+          uint8_t* sa = smem + stage * S::STAGE_BYTES;
+          uint8_t* sb = sa + S::A_BYTES;
+          if (KIND == LOGITS) {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2d(sa + 128 * BK * 2, &tmA, &full[stage], kb * BK, m0 + 128);
+            tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
+          } else if (KIND == DX) {
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+            tma_load_2d(sa + 128 * BK * 2, &tmA, &full[stage], kb * BK, m0 + 128);
+#pragma unroll
+            for (int c = 0; c < C::UMMA_N / 64; ++c)
+              tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
+          } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) tma_load_2d(sa + c * BK * 128, &tmA, &full[stage], m0 + c * 64, kb * BK);
+#pragma unroll
+            for (int c = 0; c < C::UMMA_N / 64; ++c)
+              tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
+          }
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------------ MMA issuer (one thread)
+    constexpr uint32_t IDESC = make_idesc(128, C::UMMA_N, C::A_MN, C::B_MN);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
+      int m0, n0, kb0, kb1;
+      w.decode(p, u, m0, n0, kb0, kb1);
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + acc * (C::MSUB * C::NMMA * C::UMMA_N);
+      for (int kb = kb0; kb < kb1; ++kb) {
+        mbar_wait(&full[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * S::STAGE_BYTES);
+          const uint32_t sb = sa + S::A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < BK / 16; ++kk) {
+#pragma unroll
+            for (int ms = 0; ms < C::MSUB; ++ms) {
+              uint64_t ad, bd;
+              if (C::A_MN) ad = make_desc(sa + kk * 16 * 128, BK * 128, 1024);
+              else ad = make_desc(sa + ms * 128 * BK * 2 + kk * 32, 16, 1024);
+              if (C::B_MN) bd = make_desc(sb + kk * 16 * 128, BK * 128, 1024);
+              else bd = make_desc(sb + kk * 32, 16, 1024);
+              tc_mma(tacc + ms * C::UMMA_N, ad, bd, IDESC, (kb > kb0 || kk > 0) ? 1u : 0u);
+            }
+          }
+          tc_commit(&empty[stage]);     // frees the smem stage once these MMAs have read it
+        }
+        __syncwarp();
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(&acc_full[acc]);   // accumulator complete
+      __syncwarp();
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else {
+    // ------------------------------------------------------------------ epilogue (warps 2..5)
+    const int lg = warp & 3;                 // TMEM lane group this warp may access
+    const int row_in = lg * 32 + lane;       // accumulator row (TMEM lane) of this thread
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
+      int m0, n0, kb0, kb1;
+      w.decode(p, u, m0, n0, kb0, kb1);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * (C::MSUB * C::NMMA * C::UMMA_N);
+#pragma unroll 1
+      for (int ms = 0; ms < C::MSUB; ++ms) {
+        const int row = m0 + ms * 128 + row_in;
+        if (KIND == LOGITS) {
+          const bool rv = row < p.M;
+          const int tc = rv ? p.tcol[row] : -1;
+          float mx = -INFINITY, sum = 0.f;
+#pragma unroll 1
+          for (int c = 0; c < C::UMMA_N / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tacc + ms * C::UMMA_N + c * 32, v);
+            const int col0 = n0 + c * 32;
+            __half h[32];
+            float z[32];
+            float cmx = -INFINITY;
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              h[j] = __float2half_rn(__uint_as_float(v[j]));
+              const int col = col0 + j;
+              const bool ok = (col < k) && (col != tc);
+              z[j] = ok ? __half2float(h[j]) * p.s_log2e : -INFINITY;
+              cmx = fmaxf(cmx, z[j]);
+            }
+            const float nmx = fmaxf(mx, cmx);
+            if (nmx > -INFINITY) {
+              float cs = 0.f;
+#pragma unroll
+              for (int j = 0; j < 32; ++j) cs += exp2f(z[j] - nmx);
+              sum = (mx > -INFINITY ? sum * exp2f(mx - nmx) : 0.f) + cs;
+              mx = nmx;
+            }
+            if (rv) {
+              uint4* dst = reinterpret_cast<uint4*>(p.cosv + (int64_t)row * p.k_pad + col0);
+#pragma unroll
+              for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4*>(&h[q * 8]);
+            }
+          }
+          if (rv)
+            p.partials[(int64_t)row * p.n_ltiles + n0 / 128] =
+                make_float2(mx > -INFINITY ? mx * 0.69314718055994531f : -INFINITY, sum);
+        } else if (KIND == DX) {
+          const int sp = u / (w.mt * w.nt);
+          const bool rv = row < p.M;
+          const bool none = kb1 <= kb0;  // split past k_i: the accumulator was not written
+          float* dst = p.split_ws + ((int64_t)sp * p.M + row) * p.d + n0;
+#pragma unroll 1
+          for (int c = 0; c < C::UMMA_N / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tacc + ms * C::UMMA_N + c * 32, v);
+            if (none) {
+#pragma unroll
+              for (int j = 0; j < 32; ++j) v[j] = 0u;
+            }
+            if (rv) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                reinterpret_cast<uint4*>(dst + c * 32)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          }
+        } else {
+          const bool rv = row < k;
+          float* dst = p.dWh + (int64_t)row * p.d + n0;
+#pragma unroll 1
+          for (int c = 0; c < C::UMMA_N / 32; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tacc + c * 32, v);
+            if (rv) {
+#pragma unroll
+              for (int q = 0; q < 8; ++q)
+                reinterpret_cast<uint4*>(dst + c * 32)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[acc]);
+      if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(S::TMEM_COLS));
+  }
+}
+
+// Deterministic split-K reduction: dX[r][c] = sum_s ws[s][r][c] (fixed split order).
+__global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, const float* __restrict__ ws,
+                                float* __restrict__ out) {
+  int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= n) return;
+  float4 acc = *reinterpret_cast<const float4*>(ws + i);
+  for (int s = 1; s < nsplit; ++s) {
+    float4 v = *reinterpret_cast<const float4*>(ws + s * stride + i);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  *reinterpret_cast<float4*>(out + i) = acc;
+}
+
+// ------------------------------------------------------------------------------------------------ host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  return fn;
+}
+
+// 2D bf16 tensor [rows][cols] (cols contiguous), box {box_cols, box_rows}, 128-byte swizzle.
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fprintf(stderr, "pfc: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+  return m;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+template <int KIND>
+void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int grid, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_tc_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<KIND>::TOTAL);
+    attr = true;
+  }
+  k_tc_gemm<KIND><<<grid, NUM_THREADS, Smem<KIND>::TOTAL, s>>>(a, b, p);
+}
+
+}  // namespace
+
+bool tc_available() {
+  int dev = 0, major = 0, minor = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev);
+  cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev);
+  return major == 10 && minor == 0 && encode_fn() != nullptr;
+}
+
+int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+                     const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
+                     cudaStream_t s) {
+  (void)ct;
+  CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  TcParams p{};
+  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.tcol = tcol;
+  p.s_log2e = mp.s * 1.4426950408889634f; p.cosv = cosv; p.partials = partials; p.n_ltiles = sz.n_ltiles;
+  const int64_t units = ((sz.M + 255) / 256) * ((sz.k_pad + 127) / 128);
+  launch<LOGITS>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  return 1;
+}
+
+static int dtile(const Sizes& sz) { return sz.d % 256 == 0 ? 256 : 128; }
+
+static void dx_split(const Sizes& sz, int& nsplit, int& kb_per_split) {
+  const int tiles = ((sz.M + 255) / 256) * (sz.d / dtile(sz));
+  const int64_t n_kb = sz.k_pad / 64;
+  nsplit = (int)std::max<int64_t>(1, std::min<int64_t>({(int64_t)num_sms() / tiles, n_kb, (int64_t)kMaxSplits}));
+  kb_per_split = (int)((n_kb + nsplit - 1) / nsplit);
+  nsplit = (int)((n_kb + kb_per_split - 1) / kb_per_split);
+}
+
+int64_t dx_split_ws_floats(const Sizes& sz) {
+  int ns, kbs;
+  dx_split(sz, ns, kbs);
+  return (int64_t)ns * sz.M * sz.d;
+}
+
+int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st, float* dXh,
+                 float* split_ws, cudaStream_t s) {
+  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 128);
+  CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 64);
+  TcParams p{};
+  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.split_ws = split_ws;
+  const int tiles = ((sz.M + 255) / 256) * (sz.d / dtile(sz));
+  int nsplit;
+  dx_split(sz, nsplit, p.kb_per_split);
+  p.nsplit = nsplit;
+  if (dtile(sz) == 256) launch<DX>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
+  else launch<DX128>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
+  const int64_t n = (int64_t)sz.M * sz.d;
+  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, split_ws, dXh);
+  return 2;
+}
+
+int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st, float* dWh,
+                 cudaStream_t s) {
+  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 64);
+  CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
+  TcParams p{};
+  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.dWh = dWh;
+  const int64_t units = (sz.k_pad / 128) * (sz.d / dtile(sz));
+  if (dtile(sz) == 256) launch<DW>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  else launch<DW128>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  return 1;
+}
+
 }  // namespace pfc

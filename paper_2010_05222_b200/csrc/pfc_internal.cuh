@@ -155,7 +155,9 @@ int launch_dw_simt(const Sizes& sz, bool bf16, const void* G, const void* X, con
                    cudaStream_t s);
 
 // gemm_tc.cu — tcgen05 / TMEM / TMA bf16 contractions (sm_100a)
+constexpr int kMaxSplits = 64;   // split-K bound of the dx contraction
 bool tc_available();
+int64_t dx_split_ws_floats(const Sizes& sz);
 int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
                      const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
                      cudaStream_t s);
