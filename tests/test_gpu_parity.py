@@ -159,9 +159,12 @@ def _case_id(c):
 
 
 def r21_bounds(d):
-    """DESIGN.md R21: bf16 operand rounding perturbs every logit by ~ s u sqrt(2/d) (u = 2^-9) whatever L is;
-    the north-star bars (1e-3 / 2e-2) hold where that is small against the loss (d = 512, or init-like
-    losses); elsewhere the loss error is bounded absolutely and the gradients by 4 s u sqrt(2/d)."""
+    """DESIGN.md R21: rounding x_hat and w_hat to bf16 (unit roundoff u = 2^-9) perturbs every scaled logit
+    by dz ~ N(0, sigma_z^2), sigma_z <= s u sqrt(2/d), whatever the loss. The loss error of row n is
+    sum_{j != t} p_nj dz_nj (the target logit is refined in fp32), a p-weighted average of dz times
+    (1 - p_t) <= L_n, so |dL| / L <= 4 sigma_z (4-sigma), and likewise for the gradients. The north-star bars
+    (1e-3 / 2e-2) are met where sigma_z is small against that (d = 512, init-like losses); elsewhere this
+    derived bound is the test."""
     return 4 * 64.0 * 2.0 ** -9 * math.sqrt(2.0 / d)
 
 
@@ -170,8 +173,8 @@ def check_bf16(L, Lr, gx, gxr, dW, dWr, d, north_star):
         assert abs(L - Lr) / abs(Lr) <= 1e-3, (L, Lr)
         assert maxrel(gx, gxr) <= 2e-2 and maxrel(dW, dWr) <= 2e-2
     else:
-        assert abs(L - Lr) <= 1e-3 * max(Lr, 0.05), (L, Lr)
         g = r21_bounds(d)
+        assert abs(L - Lr) / abs(Lr) <= g, (L, Lr)
         assert maxrel(gx, gxr) <= g and maxrel(dW, dWr) <= g
 
 
