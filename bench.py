@@ -106,7 +106,7 @@ def kernel_work(section, M, k, d):
         return 2.0 * M * k * d, "flop", "tensor"
     if section == "gather_w":
         return 4.0 * k * d, "byte", "hbm"          # read the sampled fp32 rows once
-    if section == "sgd":
+    if section in ("sgd", "dw_gemm_sgd"):
         return 16.0 * k * d, "byte", "hbm"         # W, V read-modify-write of the sampled rows
     if section == "softmax_grad":
         return 4.0 * M * k, "byte", "hbm"          # fp16 cosine in, bf16 gradient out (design minimum)
@@ -247,8 +247,7 @@ def main():
     stream = torch.cuda.current_stream()
 
     def step(i):
-        layer.forward_backward(xs[i % NB], ys[i % NB], gx, loss, stream)
-        layer.step(LR, stream)
+        layer.train_step(xs[i % NB], ys[i % NB], gx, loss, LR, stream)
 
     def barrier():
         if world > 1:
@@ -276,6 +275,8 @@ def main():
     launches = layer.launch_count() - l0
     prof = layer.profile_read()
     layer.profile(False)
+    # the train step fuses the momentum-SGD update into the dW contraction (section 8); sgd (9) is then empty
+    prof = {("dw_gemm_sgd" if s == "dw_gemm" else s): v for s, v in prof.items()}
     loss_val = float(loss.item())
     layer.check()
     t = torch.tensor([ms_total], device="cuda")
@@ -290,15 +291,13 @@ def main():
     gh = torch.empty(B, d).pin_memory()
     lh = torch.zeros(1).pin_memory()
     for i in range(2):
-        layer.forward_backward_host(xh[i % NB], yh[i % NB], gh, lh, stream)
-        layer.step(LR, stream)
+        layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
     barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
     for i in range(args.steps):
-        layer.forward_backward_host(xh[i % NB], yh[i % NB], gh, lh, stream)
-        layer.step(LR, stream)
+        layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
     e1.record(stream)
     torch.cuda.synchronize()
     barrier()
@@ -316,6 +315,10 @@ def main():
             if tj.get("workload") == args.config and tj.get("n_gpus", 1) == world:
                 traffic = tj.get("bytes_per_launch", {})
         entries = [e for e in (roofline_entry(s, ms, n, M, k, d, peaks, traffic) for s, (ms, n) in prof.items()) if e]
+        for e in entries:   # the fused dW + SGD kernel is also a contraction: report its tensor-pipe side too
+            if e["kernel"] == "dw_gemm_sgd":
+                e["tensor_tflops"] = round(2.0 * M * k * d / (e["avg_ms"] / 1e3) / 1e12, 2)
+                e["tensor_frac"] = round(e["tensor_tflops"] / peaks["bf16_tflops_sustained"], 4)
         dominant = max(prof.items(), key=lambda kv: kv[1][0])[0]
         dom = next((e for e in entries if e["kernel"] == dominant), None)
         if dom is None and entries:

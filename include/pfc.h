@@ -124,11 +124,26 @@ pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* co
                                       const int64_t* const* labels_dev, float* const* grad_x_dev, float* loss_dev,
                                       void* stream);
 
+/* pfc_forward_backward followed by pfc_step(lr), fused: the momentum-SGD update of the sampled rows is applied
+ * inside the dW contraction's epilogue (bf16 mode; the fp32 mode runs the same two kernels back to back), so
+ * the sampled-row gradient is never written to HBM. Same results as the pair up to
+ * rounding; afterwards no gradient is pending (pfc_get_sampled_grad / pfc_step return PFC_ERR_CONTRACT). */
+pfc_status pfc_train_step(pfc_ctx* ctx, const float* x_dev, const int64_t* labels_dev, float* grad_x_dev,
+                          float* loss_dev, float lr, void* stream);
+
+/* pfc_group_forward_backward + update of every rank, fused as in pfc_train_step. */
+pfc_status pfc_group_train_step(pfc_ctx** ctxs, int32_t n, const float* const* x_dev, const int64_t* const* labels_dev,
+                                float* const* grad_x_dev, float* loss_dev, float lr, void* stream);
+
 /* The same pass with HOST buffers: copies x and labels host->device and grad_x, loss device->host on
  * `stream` (pinned host memory gives asynchronous copies), then synchronises `stream`. loss_host may be
  * NULL. Used for the end-to-end measurement. */
 pfc_status pfc_forward_backward_host(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host,
                                      float* grad_x_host, float* loss_host, void* stream);
+
+/* pfc_train_step with HOST buffers (copies inside, synchronises `stream`): the end-to-end entry point. */
+pfc_status pfc_train_step_host(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                               float* loss_host, float lr, void* stream);
 
 /* Lazy momentum-SGD update of the rows sampled by the last pfc_forward_backward (DESIGN.md
  * R15): g = (dw_hat - w_hat (w_hat . dw_hat)) / ||w||; v <- mu v + g + lambda w; w <- w - lr v.

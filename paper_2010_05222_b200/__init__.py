@@ -30,7 +30,8 @@ EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pf
            "pfc_forward_backward_host", "pfc_step", "pfc_shard_range", "pfc_sizes", "pfc_param_ptrs",
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
            "pfc_launch_count", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
-           "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section"]
+           "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section", "pfc_train_step", "pfc_train_step_host",
+           "pfc_group_train_step"]
 PROF_SECTIONS = 10
 
 
@@ -82,6 +83,9 @@ def load_library(path=LIB_PATH):
         "pfc_check": (st, [VP]),
         "pfc_launch_count": (I64, [VP]),
         "pfc_version": (ctypes.c_char_p, []),
+        "pfc_train_step": (st, [VP, VP, VP, VP, VP, F, VP]),
+        "pfc_train_step_host": (st, [VP, VP, VP, VP, VP, F, VP]),
+        "pfc_group_train_step": (st, [P(VP), ctypes.c_int32, P(VP), P(VP), P(VP), VP, F, VP]),
         "pfc_profile_enable": (st, [VP, ctypes.c_int32]),
         "pfc_profile_read": (st, [VP, P(ctypes.c_double), P(I64)]),
         "pfc_profile_section": (ctypes.c_char_p, [ctypes.c_int32]),
@@ -191,6 +195,16 @@ class PartialFC:
         self._check(self._lib.pfc_forward_backward_host(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss),
                                                         self._stream(stream)))
 
+    def train_step(self, x, labels, grad_x, loss=None, lr=0.1, stream=None):
+        """forward_backward + step(lr) fused (the SGD update runs in the dW contraction's epilogue)."""
+        self._check(self._lib.pfc_train_step(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), float(lr),
+                                             self._stream(stream)))
+
+    def train_step_host(self, x, labels, grad_x, loss=None, lr=0.1, stream=None):
+        """train_step with host (pinned) CPU tensors; copies inside the call; synchronises."""
+        self._check(self._lib.pfc_train_step_host(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), float(lr),
+                                                  self._stream(stream)))
+
     def step(self, lr, stream=None):
         self._check(self._lib.pfc_step(self._h, float(lr), self._stream(stream)))
 
@@ -261,14 +275,19 @@ def _stream_ptr(stream):
     return PartialFC._stream(stream)
 
 
-def group_forward_backward(ranks, xs, labels, grad_xs, loss=None, stream=None):
-    """One forward + backward of every rank of a loopback group (PartialFC(..., comm_mode="loopback"))."""
+def group_forward_backward(ranks, xs, labels, grad_xs, loss=None, stream=None, lr=None):
+    """One forward + backward of every rank of a loopback group (PartialFC(..., comm_mode="loopback")); with
+    lr given, the fused train step (update applied inside the dW contraction)."""
     lib = load_library()
     n = len(ranks)
     VPA = ctypes.c_void_p * n
     hs = VPA(*[r._h for r in ranks])
-    s = lib.pfc_group_forward_backward(hs, n, VPA(*[t.data_ptr() for t in xs]), VPA(*[t.data_ptr() for t in labels]),
-                                       VPA(*[t.data_ptr() for t in grad_xs]), _ptr(loss), _stream_ptr(stream))
+    args = (hs, n, VPA(*[t.data_ptr() for t in xs]), VPA(*[t.data_ptr() for t in labels]),
+            VPA(*[t.data_ptr() for t in grad_xs]), _ptr(loss))
+    if lr is None:
+        s = lib.pfc_group_forward_backward(*args, _stream_ptr(stream))
+    else:
+        s = lib.pfc_group_train_step(*args, float(lr), _stream_ptr(stream))
     if s:
         msg = lib.pfc_last_error(None).decode()
         for r in ranks:

@@ -74,6 +74,7 @@ struct pfc_ctx {
   float* dxh_local = nullptr;  // B x d (reduce-scatter output)
   float* split_ws = nullptr;   // split-K partials of the dx GEMM
   float* dWh = nullptr;        // k_pad x d
+  float* dotw = nullptr;       // k_pad: w_hat . dW_hat per sampled class (fused SGD)
   int* err_dev = nullptr;
   // host-buffer entry point
   float* x_in = nullptr;
@@ -270,6 +271,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->dxh_local, B * d * 4);
   ALLOC(c->split_ws, (size_t)(c->use_tc ? dx_split_ws_floats(sz) : 1) * 4);
   ALLOC(c->dWh, kp * d * 4);
+  ALLOC(c->dotw, kp * 4);
   ALLOC(c->err_dev, 16);
   ALLOC(c->x_in, B * d * 4);
   ALLOC(c->y_in, B * 8);
@@ -382,12 +384,13 @@ void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
 }
 
 // after all-reduce SUM: LSE, loss, K8 (prob - onehot), K9 dX_hat partial
-void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, cudaStream_t s) {
+void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
   n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->err_dev, s);
   mark(c, 5, s);
-  n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G, s);
+  n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
+                           fused && c->use_tc ? c->dotw : nullptr, s);
   mark(c, 6, s);
   if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
@@ -396,24 +399,31 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, cudaStream_t s) {
   c->launches += n;
 }
 
-// after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat
-void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, cudaStream_t s) {
+// after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat (+ K12 when fused)
+void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, float lr, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
   n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
   mark(c, 8, s);
-  if (c->use_tc)
-    n += launch_dw_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, c->dWh, s);
-  else
-    n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
+  if (c->use_tc && fused) {
+    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, lr, c->cfg.momentum, c->cfg.weight_decay};
+    n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, s);
+  } else {
+    if (c->use_tc)
+      n += launch_dw_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, c->dWh, s);
+    else
+      n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
+    if (fused)
+      n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, lr, c->cfg.momentum, c->cfg.weight_decay, s);
+  }
   mark(c, 9, s);
   c->launches += n;
 }
 
-pfc_status finish_fb(pfc_ctx* c, cudaStream_t s) {
+pfc_status finish_fb(pfc_ctx* c, bool fused, cudaStream_t s) {
   CUDA_TRY(c, cudaGetLastError());
   c->step += 1;
-  c->fb_done = true;
+  c->fb_done = !fused;
   c->last_stream = s;
   if (c->sync_check) {
     CUDA_TRY(c, cudaStreamSynchronize(s));
@@ -424,8 +434,21 @@ pfc_status finish_fb(pfc_ctx* c, cudaStream_t s) {
 
 }  // namespace
 
+static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss, bool fused,
+                           float lr, void* stream);
+
 pfc_status pfc_forward_backward(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss,
                                 void* stream) {
+  return run_step(c, x, labels, grad_x, loss, false, 0.f, stream);
+}
+
+pfc_status pfc_train_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss, float lr,
+                          void* stream) {
+  return run_step(c, x, labels, grad_x, loss, true, lr, stream);
+}
+
+static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss, bool fused,
+                           float lr, void* stream) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   pfc_status a = check_fb_args(c, x, labels, grad_x);
   if (a != PFC_OK) return a;
@@ -453,19 +476,32 @@ pfc_status pfc_forward_backward(pfc_ctx* c, const float* x, const int64_t* label
   }
   phase_c(c, gmax, s);
   if (multi) NCCL_TRY(c, ncclAllReduce(c->red, c->red, 2 * sz.M, ncclFloat, ncclSum, c->comm, s));
-  phase_d(c, gmax, loss_out, s);
+  phase_d(c, gmax, loss_out, fused, s);
   mark(c, 7, s);
   const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
   if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
     NCCL_TRY(c, ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
     dxh = c->dxh_local;
   }
-  phase_e(c, dxh, grad_x, s);
-  return finish_fb(c, s);
+  phase_e(c, dxh, grad_x, fused, lr, s);
+  return finish_fb(c, fused, s);
 }
+
+static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, const int64_t* const* labels,
+                             float* const* grad_x, float* loss, bool fused, float lr, void* stream);
 
 pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* const* x, const int64_t* const* labels,
                                       float* const* grad_x, float* loss, void* stream) {
+  return group_step(ctxs, n, x, labels, grad_x, loss, false, 0.f, stream);
+}
+
+pfc_status pfc_group_train_step(pfc_ctx** ctxs, int32_t n, const float* const* x, const int64_t* const* labels,
+                                float* const* grad_x, float* loss, float lr, void* stream) {
+  return group_step(ctxs, n, x, labels, grad_x, loss, true, lr, stream);
+}
+
+static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, const int64_t* const* labels,
+                             float* const* grad_x, float* loss, bool fused, float lr, void* stream) {
   if (!ctxs || n < 1 || n > kMaxLoopback || !x || !labels || !grad_x)
     return set_err(nullptr, PFC_ERR_CONTRACT, "bad group arguments (1 <= n <= 16, non-NULL arrays)");
   for (int r = 0; r < n; ++r) {
@@ -499,35 +535,45 @@ pfc_status pfc_group_forward_backward(pfc_ctx** ctxs, int32_t n, const float* co
   for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
   for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->red; dst.p[r] = ctxs[r]->red; }
   c0->launches += launch_group_reduce(2 * sz.M, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
-  for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, s);
+  for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, fused, s);
   for (int r = 0; r < n; ++r) src.p[r] = ctxs[r]->dXh;
   for (int r = 0; r < n; ++r) {  // reduce-scatter: owner r sums rows [rB, (r+1)B) over ranks
     PtrPack one{};
     one.p[0] = ctxs[r]->dxh_local;
     c0->launches += launch_group_reduce((int64_t)sz.B * sz.d, src, (int64_t)r * sz.B * sz.d, one, n, 1, 0, s);
   }
-  for (int r = 0; r < n; ++r) phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], s);
+  for (int r = 0; r < n; ++r) phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], fused, lr, s);
   for (int r = 0; r < n; ++r) {
-    pfc_status f = finish_fb(ctxs[r], s);
+    pfc_status f = finish_fb(ctxs[r], fused, s);
     if (f != PFC_OK) return f;
   }
   return PFC_OK;
 }
 
-pfc_status pfc_forward_backward_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
-                                     float* loss_host, void* stream) {
+static pfc_status host_step(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                            float* loss_host, bool fused, float lr, void* stream) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   if (!x_host || !labels_host || !grad_x_host) return set_err(c, PFC_ERR_CONTRACT, "NULL host buffer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   const size_t xb = (size_t)c->sz.B * c->sz.d * 4;
   CUDA_TRY(c, cudaMemcpyAsync(c->x_in, x_host, xb, cudaMemcpyHostToDevice, s));
   CUDA_TRY(c, cudaMemcpyAsync(c->y_in, labels_host, (size_t)c->sz.B * 8, cudaMemcpyHostToDevice, s));
-  pfc_status r = pfc_forward_backward(c, c->x_in, c->y_in, c->gx_out, c->loss_dev, stream);
+  pfc_status r = run_step(c, c->x_in, c->y_in, c->gx_out, c->loss_dev, fused, lr, stream);
   if (r != PFC_OK) return r;
   CUDA_TRY(c, cudaMemcpyAsync(grad_x_host, c->gx_out, xb, cudaMemcpyDeviceToHost, s));
   if (loss_host) CUDA_TRY(c, cudaMemcpyAsync(loss_host, c->loss_dev, 4, cudaMemcpyDeviceToHost, s));
   CUDA_TRY(c, cudaStreamSynchronize(s));
   return PFC_OK;
+}
+
+pfc_status pfc_forward_backward_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                                     float* loss_host, void* stream) {
+  return host_step(c, x_host, labels_host, grad_x_host, loss_host, false, 0.f, stream);
+}
+
+pfc_status pfc_train_step_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                               float* loss_host, float lr, void* stream) {
+  return host_step(c, x_host, labels_host, grad_x_host, loss_host, true, lr, stream);
 }
 
 pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {

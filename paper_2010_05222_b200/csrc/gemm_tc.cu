@@ -112,33 +112,35 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool 
 }
 
 // ------------------------------------------------------------------------------------------------ kernel
-enum Kind { LOGITS = 0, DX = 1, DW = 2, DX128 = 3, DW128 = 4 };  // *128: d-tile 128 (d % 256 != 0)
-__host__ __device__ constexpr int base_kind(int k) { return k == DX128 ? DX : k == DW128 ? DW : k; }
+// *128: d-tile 128 (d % 256 != 0); DWF: dW with the momentum-SGD update fused into the epilogue
+enum Kind { LOGITS = 0, DX = 1, DW = 2, DX128 = 3, DW128 = 4, DWF = 5 };
+__host__ __device__ constexpr int base_kind(int k) { return k == DX128 ? DX : (k == DW128 || k == DWF) ? DW : k; }
 
 constexpr int BK = 64;          // K elements per stage (128 B of bf16: one swizzle row)
-constexpr int NUM_THREADS = 192;
 
 template <int KIND>
 struct Cfg;
 template <>
 struct Cfg<LOGITS> {  // tile 256 x 128 (two M = 128 halves sharing the B tile), K = d
-  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 128, STAGES = 4, ACC = 2;
+  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 128, STAGES = 4, ACC = 2, EPI_WARPS = 4;
   static constexpr bool A_MN = false, B_MN = false;
 };
 template <>
 struct Cfg<DX> {      // tile 256 x 256 (M halves x d half), K = a split of the sampled classes
-  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 256, STAGES = 3, ACC = 1;
+  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 256, STAGES = 3, ACC = 1, EPI_WARPS = 4;
   static constexpr bool A_MN = false, B_MN = true;
 };
 template <>
 struct Cfg<DW> {      // tile 128 classes x 256 dims, K = M (the global batch)
-  static constexpr int MSUB = 1, NMMA = 1, UMMA_N = 256, STAGES = 4, ACC = 2;
+  static constexpr int MSUB = 1, NMMA = 1, UMMA_N = 256, STAGES = 4, ACC = 2, EPI_WARPS = 4;
   static constexpr bool A_MN = true, B_MN = true;
 };
 template <>
 struct Cfg<DX128> : Cfg<DX> { static constexpr int UMMA_N = 128, STAGES = 4; };
 template <>
 struct Cfg<DW128> : Cfg<DW> { static constexpr int UMMA_N = 128; };
+template <>
+struct Cfg<DWF> : Cfg<DW> { static constexpr int UMMA_N = 128, STAGES = 3, ACC = 2, EPI_WARPS = 8; };
 
 template <int KIND>
 struct Smem {
@@ -147,8 +149,12 @@ struct Smem {
   static constexpr int B_BYTES = C::NMMA * C::UMMA_N * BK * 2;      // per stage
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = C::MSUB * C::NMMA * C::UMMA_N * C::ACC;
-  static constexpr int TOTAL = C::STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+  static constexpr int EPI_BYTES = KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 0;
+  static constexpr int THREADS = 64 + 32 * C::EPI_WARPS;
+  static constexpr int TOTAL = C::STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BYTES;
   static_assert(TMEM_COLS <= 512, "TMEM overflow");
+  static_assert(C::STAGES * STAGE_BYTES + 1024 + 256 + (KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 0) <= 232448,
+                "shared memory overflow (227 KB per CTA)");
 };
 
 struct TcParams {
@@ -167,7 +173,8 @@ struct TcParams {
   int nsplit;
   int kb_per_split;
   // dw epilogue
-  float* dWh;            // k_pad x d
+  float* dWh;            // k_pad x d (unfused)
+  SgdArgs sgd;           // fused momentum SGD (sgd.W != nullptr)
 };
 
 // Work decomposition shared by all roles (identical sequence on every warp of the CTA).
@@ -216,7 +223,7 @@ struct Work {
 };
 
 template <int KIND_>
-__global__ void __launch_bounds__(NUM_THREADS, 1)
+__global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
   constexpr int KIND = base_kind(KIND_);
   using C = Cfg<KIND_>;
@@ -228,6 +235,12 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
   uint64_t* acc_full = empty + C::STAGES;
   uint64_t* acc_empty = acc_full + C::ACC;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + C::ACC);
+  // fused-SGD staging (DWF only): the 128 x 128 fp32 dW_hat tile (float4-XOR-swizzled rows) + per-row
+  // (row id, 1/||w||, radial factor)
+  float4* s_tile = reinterpret_cast<float4*>(smem + C::STAGES * S::STAGE_BYTES + 256);
+  int64_t* s_rowj = reinterpret_cast<int64_t*>(s_tile + 128 * 32);
+  float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
+  float* s_rad = s_inv + 128;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = p.st->k;
@@ -235,7 +248,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < C::STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
-    for (int i = 0; i < C::ACC; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 4); }
+    for (int i = 0; i < C::ACC; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], C::EPI_WARPS); }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   }
@@ -326,9 +339,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
     }
   } else {
-    // ------------------------------------------------------------------ epilogue (warps 2..5)
+    // ------------------------------------------------------------------ epilogue (warps 2 .. 2 + EPI_WARPS)
     const int lg = warp & 3;                 // TMEM lane group this warp may access
     const int row_in = lg * 32 + lane;       // accumulator row (TMEM lane) of this thread
+    const int eset = (warp - 2) >> 2;        // with 8 epilogue warps: two sets splitting the 32-column chunks
+    constexpr int NSET = C::EPI_WARPS / 4;
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
@@ -337,6 +352,67 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * (C::MSUB * C::NMMA * C::UMMA_N);
+      if constexpr (KIND_ == DWF) {
+        // Fused lazy momentum SGD of 128 sampled classes x 128 dims (rows.cu K12 is the unfused
+        // form). (1) both warp sets copy the accumulator tile TMEM -> smem and release TMEM at once; (2) each
+        // of the 8 warps updates 16 rows, one 512-byte coalesced W and V segment per row and instruction.
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");  // previous tile consumed
+        if (eset == 0) {
+          const int prow = m0 + row_in;
+          const bool rv = prow < k;
+          const float inv = rv ? p.sgd.inv_norm[prow] : 0.f;
+          s_rowj[row_in] = rv ? (int64_t)p.sgd.idx[prow] : -1;
+          s_inv[row_in] = inv;
+          s_rad[row_in] = rv ? p.sgd.dotw[prow] * inv : 0.f;     // w * rad = w_hat (w_hat . dw_hat)
+        }
+#pragma unroll 1
+        for (int c = eset * 2; c < eset * 2 + 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tacc + c * 32, v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            s_tile[row_in * 32 + ((c * 8 + q) ^ (row_in & 31))] =
+                make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                            __uint_as_float(v[4 * q + 3]));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);             // TMEM free: next tile's MMAs may start
+        if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        const int ew = warp - 2;                                 // rows ew*16 .. ew*16+15
+        const int col = n0 + lane * 4;
+#pragma unroll 1
+        for (int r0 = 0; r0 < 16; r0 += 8) {
+          float4 wv[8], mv[8];
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int64_t j = s_rowj[ew * 16 + r0 + r];
+            if (j >= 0) {
+              wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + j * p.d + col);
+              mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + j * p.d + col);
+            }
+          }
+#pragma unroll
+          for (int r = 0; r < 8; ++r) {
+            const int rr = ew * 16 + r0 + r;
+            const int64_t j = s_rowj[rr];
+            if (j >= 0) {
+              const float inv = s_inv[rr], rad = s_rad[rr];
+              const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
+              float4 w = wv[r], m = mv[r];
+              m.x = p.sgd.mu * m.x + (g4.x - w.x * rad) * inv + p.sgd.lambda * w.x;
+              m.y = p.sgd.mu * m.y + (g4.y - w.y * rad) * inv + p.sgd.lambda * w.y;
+              m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * inv + p.sgd.lambda * w.z;
+              m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * inv + p.sgd.lambda * w.w;
+              w.x -= p.sgd.lr * m.x; w.y -= p.sgd.lr * m.y; w.z -= p.sgd.lr * m.z; w.w -= p.sgd.lr * m.w;
+              *reinterpret_cast<float4*>(p.sgd.V + j * p.d + col) = m;
+              *reinterpret_cast<float4*>(p.sgd.W + j * p.d + col) = w;
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int ms = 0; ms < C::MSUB; ++ms) {
         const int row = m0 + ms * 128 + row_in;
@@ -396,11 +472,11 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 reinterpret_cast<uint4*>(dst + c * 32)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
             }
           }
-        } else {
+        } else if (p.sgd.W == nullptr) {
           const bool rv = row < k;
           float* dst = p.dWh + (int64_t)row * p.d + n0;
 #pragma unroll 1
-          for (int c = 0; c < C::UMMA_N / 32; ++c) {
+          for (int c = eset; c < C::UMMA_N / 32; c += NSET) {
             uint32_t v[32];
             tmem_ld32(tacc + c * 32, v);
             if (rv) {
@@ -486,7 +562,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int g
     cudaFuncSetAttribute(k_tc_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<KIND>::TOTAL);
     attr = true;
   }
-  k_tc_gemm<KIND><<<grid, NUM_THREADS, Smem<KIND>::TOTAL, s>>>(a, b, p);
+  k_tc_gemm<KIND><<<grid, Smem<KIND>::THREADS, Smem<KIND>::TOTAL, s>>>(a, b, p);
 }
 
 }  // namespace
@@ -544,6 +620,17 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
   const int64_t n = (int64_t)sz.M * sz.d;
   k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, split_ws, dXh);
   return 2;
+}
+
+int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                     const SgdArgs& sa, cudaStream_t s) {
+  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 64);
+  CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
+  TcParams p{};
+  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
+  const int64_t units = (sz.k_pad / 128) * (sz.d / 128);
+  launch<DWF>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  return 1;
 }
 
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st, float* dWh,

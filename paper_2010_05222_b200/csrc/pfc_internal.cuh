@@ -129,7 +129,7 @@ int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float*
                     int* err, cudaStream_t s);
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
-                        cudaStream_t s);
+                        float* dotw /* per-class w_hat . dW_hat, or NULL */, cudaStream_t s);
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
                           float* grad_x, cudaStream_t s);
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
@@ -165,5 +165,12 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
                  float* dXh, float* split_ws, cudaStream_t s);
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                  float* dWh, cudaStream_t s);
+// Fused K11 + K12: dW_hat tile in TMEM -> g = (dw_hat - w_hat dot)/||w||,
+// v <- mu v + g + lambda w, w <- w - lr v, written straight into the W and V shard rows.
+struct SgdArgs {
+  float* W; float* V; const int32_t* idx; const float* inv_norm; const float* dotw; float lr, mu, lambda;
+};
+int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                     const SgdArgs& a, cudaStream_t s);
 
 }  // namespace pfc

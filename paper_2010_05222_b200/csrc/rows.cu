@@ -193,56 +193,85 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
   }
 }
 
-// ---------------------------------------------------------------- K8: softmax gradient, 8 columns per thread
-template <bool BF16>
+// ---------------------------------------------------------------- K8: softmax gradient
+// Column strips of 256 sampled classes per block; thread = 8 consecutive columns x every 8th row, so a warp
+// streams 512 contiguous bytes of one row. Gc = (s/M)(p - onehot) phi'(c_t) (Alg.1 L8-9). With DOT, also
+// dot[j] = sum_n Gc[n][j] c[n][j] = w_hat_j . dW_hat_j (the radial part the fused SGD epilogue removes).
+template <bool BF16, bool DOT>
 __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, const void* __restrict__ cosv,
                                                       const float* __restrict__ lse, const float* __restrict__ gt,
                                                       const int32_t* __restrict__ tcol, const float* __restrict__ ct,
-                                                      const SamplerState* st, MarginParams mp, void* __restrict__ G) {
-  const int n = blockIdx.y;
-  const int64_t c0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 8;
-  if (c0 >= k_pad) return;
+                                                      const SamplerState* st, MarginParams mp, void* __restrict__ G,
+                                                      float* __restrict__ dotw) {
+  __shared__ float red[8][257];
+  const int cg = threadIdx.x & 31, rp = threadIdx.x >> 5;
+  const int64_t c0 = (int64_t)blockIdx.x * 256 + cg * 8;
   const int k = st->k;
   const float L2E = 1.4426950408889634f;
   const float sl = mp.s * L2E;
-  const float off = lse[n] * L2E;
-  const int tc = tcol[n];
   const float gs = mp.s / (float)M;
-  float c[8];
-  const int64_t base = (int64_t)n * k_pad + c0;
-  if (BF16) {
-    uint4 raw = *reinterpret_cast<const uint4*>((const __half*)cosv + base);
-    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+  float dacc[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); c[2 * i] = f.x; c[2 * i + 1] = f.y; }
-  } else {
-    float4 a = *reinterpret_cast<const float4*>((const float*)cosv + base);
-    float4 b = *reinterpret_cast<const float4*>((const float*)cosv + base + 4);
-    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
-  }
-  float g[8];
+  for (int i = 0; i < 8; ++i) dacc[i] = 0.f;
+  const bool any = c0 < k;
+  for (int n = rp; n < M; n += 8) {
+    const int64_t base = (int64_t)n * k_pad + c0;
+    float g[8];
+    if (any) {
+      const float off = lse[n] * L2E;
+      const int tc = tcol[n];
+      float c[8];
+      if (BF16) {
+        uint4 raw = *reinterpret_cast<const uint4*>((const __half*)cosv + base);
+        const __half2* h = reinterpret_cast<const __half2*>(&raw);
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const int64_t col = c0 + i;
-    if (col < k) {
-      if (col == tc) {
-        g[i] = gs * gt[n] * margin_dphi(mp, ct[n]);   // (p_t - 1) phi'(c_t), cancellation-free
+        for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); c[2 * i] = f.x; c[2 * i + 1] = f.y; }
       } else {
-        g[i] = gs * exp2f(c[i] * sl - off);
+        float4 a = *reinterpret_cast<const float4*>((const float*)cosv + base);
+        float4 b = *reinterpret_cast<const float4*>((const float*)cosv + base + 4);
+        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t col = c0 + i;
+        if (col < k) {
+          if (col == tc) {
+            const float ctv = ct[n];
+            g[i] = gs * gt[n] * margin_dphi(mp, ctv);   // (p_t - 1) phi'(c_t), cancellation-free
+            c[i] = ctv;
+          } else {
+            g[i] = gs * exp2f(c[i] * sl - off);
+          }
+        } else {
+          g[i] = 0.f;
+        }
+        if (DOT) dacc[i] += g[i] * c[i];
       }
     } else {
-      g[i] = 0.f;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) g[i] = 0.f;
+    }
+    if (BF16) {
+      uint4 o;
+      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+      *reinterpret_cast<uint4*>((__nv_bfloat16*)G + base) = o;
+    } else {
+      *reinterpret_cast<float4*>((float*)G + base) = make_float4(g[0], g[1], g[2], g[3]);
+      *reinterpret_cast<float4*>((float*)G + base + 4) = make_float4(g[4], g[5], g[6], g[7]);
     }
   }
-  if (BF16) {
-    uint4 o;
-    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+  if (DOT) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
-    *reinterpret_cast<uint4*>((__nv_bfloat16*)G + base) = o;
-  } else {
-    *reinterpret_cast<float4*>((float*)G + base) = make_float4(g[0], g[1], g[2], g[3]);
-    *reinterpret_cast<float4*>((float*)G + base + 4) = make_float4(g[4], g[5], g[6], g[7]);
+    for (int i = 0; i < 8; ++i) red[rp][cg * 8 + i] = dacc[i];
+    __syncthreads();
+    if (threadIdx.x < 256) {
+      float v = 0.f;
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v += red[r][threadIdx.x];
+      dotw[(int64_t)blockIdx.x * 256 + threadIdx.x] = v;
+    }
   }
 }
 
@@ -353,10 +382,15 @@ int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float*
 
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
-                        cudaStream_t s) {
-  dim3 grid((unsigned)((sz.k_pad / 8 + 255) / 256), sz.M);
-  if (bf16) k_softmax_grad<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G);
-  else k_softmax_grad<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G);
+                        float* dotw, cudaStream_t s) {
+  const unsigned grid = (unsigned)(sz.k_pad / 256);
+  if (bf16) {
+    if (dotw) k_softmax_grad<true, true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
+    else k_softmax_grad<true, false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
+  } else {
+    if (dotw) k_softmax_grad<false, true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
+    else k_softmax_grad<false, false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
+  }
   return 1;
 }
 

@@ -105,7 +105,7 @@ TINY_CASES = [
 ]
 
 
-def _run_single(case, precision, steps=2):
+def _run_single(case, precision, steps=2, fused=False):
     C, d, B, r, mt, m, dist, sigma = case
     lr = 0.1
     layer = make_layer(C, d, B, r, mt, m, precision, seed=3, wseed=1)
@@ -129,16 +129,23 @@ def _run_single(case, precision, steps=2):
         y = torch.from_numpy(ys[0]).cuda()
         gx = torch.empty_like(x)
         loss = torch.zeros(1, device="cuda")
-        layer.forward_backward(x, y, gx, loss)
-        idx = layer.sampled()
-        dW = layer.sampled_grad()
-        ref = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
-        assert np.array_equal(idx, ref["idx"][0]), "sampled indices differ"
-        results.append((float(loss.item()), ref["loss"], gx.cpu().numpy(), ref["grad_x"][0], dW, ref["dW"][0]))
-        # momentum SGD on the sampled rows (lazy)
         Wd, Vd = layer.params()
         W_before = Wd.clone()
-        layer.step(lr)
+        if fused:
+            layer.train_step(x, y, gx, loss, lr=lr)
+            idx = layer.sampled()
+            dW = None
+        else:
+            layer.forward_backward(x, y, gx, loss)
+            idx = layer.sampled()
+            dW = layer.sampled_grad()
+        ref = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
+        assert np.array_equal(idx, ref["idx"][0]), "sampled indices differ"
+        results.append((float(loss.item()), ref["loss"], gx.cpu().numpy(), ref["grad_x"][0],
+                        ref["dW"][0] if dW is None else dW, ref["dW"][0]))
+        # momentum SGD on the sampled rows (lazy)
+        if not fused:
+            layer.step(lr)
         layer.check()
         Wrows_ref, Vrows_ref = oracle.sgd_momentum_rows(w_rows(idx), np.stack([Vh.get(int(j), np.zeros(d)) for j in idx]),
                                                         ref["dW"][0], lr, cfg.momentum, cfg.weight_decay)
@@ -197,6 +204,24 @@ def test_forward_backward_step_parity(case, precision):
         assert maxrel(Wn, Wnr) <= bound
 
 
+@pytest.mark.parametrize("case", [FB_CASES[0], FB_CASES[2], FB_CASES[4], FB_CASES[5]], ids=_case_id)
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_fused_train_step_parity(case, precision):
+    """pfc_train_step (SGD inside the dW epilogue) against the oracle's forward_backward + SGD."""
+    tl, tg = TOL[precision]
+    d, dist = case[1], case[6]
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, precision, fused=True):
+        if precision == "fp32" or d >= 512 or dist == "init":
+            assert abs(L - Lr) / abs(Lr) <= tl
+            assert maxrel(gx, gxr) <= tg
+            assert maxrel(Vn, Vnr) <= tg
+        else:
+            g = r21_bounds(d)
+            assert abs(L - Lr) / abs(Lr) <= g and maxrel(gx, gxr) <= g and maxrel(Vn, Vnr) <= g
+        bound = 1e-6 + 0.1 * max(tg, 1e-4) * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+        assert maxrel(Wn, Wnr) <= bound
+
+
 @pytest.mark.parametrize("case", TINY_CASES, ids=_case_id)
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_tiny_loss_regime(case, precision):
@@ -210,6 +235,38 @@ def test_tiny_loss_regime(case, precision):
             assert maxrel(gx, gxr) <= 1e-4 and maxrel(dW, dWr) <= 1e-4
         else:
             check_bf16(L, Lr, gx, gxr, dW, dWr, d, north_star=False)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_loopback_group_train_step(world, precision):
+    """Fused multi-rank step on one GPU: loss, grad_x and every rank's updated sampled rows."""
+    C, d, B, r, mt, m = 9001, 512, 16, 0.1, "cosface", 0.4
+    lr = 0.1
+    layers = [make_layer(C, d, B, r, mt, m, precision, seed=8, wseed=4, world=world, rank=i, comm="loopback")
+              for i in range(world)]
+    cfg = ocfg(C, d, B, r, mt, m, seed=8, world=world)
+    ys = synth.make_labels(2, 0, world, B, C)
+    xs = synth.make_features(2, 0, world, B, d)
+    xt = [torch.from_numpy(x).cuda() for x in xs]
+    yt = [torch.from_numpy(y).cuda() for y in ys]
+    gt = [torch.empty_like(x) for x in xt]
+    loss = torch.zeros(1, device="cuda")
+    pfc.group_forward_backward(layers, xt, yt, gt, loss, lr=lr)
+    ref = oracle.forward_backward(cfg, xs, ys, lambda i: synth.w_rows_np(4, i, d), step=0)
+    tl, tg = TOL[precision]
+    assert abs(loss.item() - ref["loss"]) / ref["loss"] <= tl
+    for i, layer in enumerate(layers):
+        idx = layer.sampled()
+        assert np.array_equal(idx, ref["idx"][i])
+        assert maxrel(gt[i].cpu().numpy(), ref["grad_x"][i]) <= tg
+        W, V = layer.params()
+        loc = torch.from_numpy(idx - layer.shard_start).cuda()
+        w0 = synth.w_rows_np(4, idx, d)
+        Wr, Vr = oracle.sgd_momentum_rows(w0, np.zeros_like(w0), ref["dW"][i], lr, cfg.momentum, cfg.weight_decay)
+        assert maxrel(V[loc].cpu().numpy(), Vr) <= tg
+    for layer in layers:
+        layer.close()
 
 
 @pytest.mark.parametrize("world", [2, 4])
