@@ -8,5 +8,5 @@ from .philox import philox4x32_10, class_key  # noqa: F401
 from .pfc import (  # noqa: F401
     OracleConfig, MARGIN_NONE, MARGIN_ARCFACE, MARGIN_COSFACE,
     shard_range, sample_budget, positives, sample_shard, normalize_rows, margin_phi, margin_dphi,
-    forward_backward, sgd_momentum_rows, spot_rows,
+    forward_backward, sgd_momentum_rows, spot_rows, spot_cols,
 )

@@ -246,3 +246,32 @@ def spot_rows(cfg, X, Y, S, w_rows, rows, step_unused=None):
         gx = (dxh - xh[0] * np.dot(xh[0], dxh)) / max(xn[0], NORM_EPS)
         res.append((lse, lse - z[t], gx))
     return res
+
+
+def spot_cols(cfg, X, Y, S, w_rows, cols):
+    """Gradient w.r.t. the raw W rows of the sampled classes S[cols] (same definitions as forward_backward:
+    Alg.1 L10 grad w = X^T grad logits, then the l2-norm backprop R14), for sizes where only a few columns are
+    wanted. The row log-sum-exps need every row over the whole sampled set S, computed as one product."""
+    s, mt, m = float(cfg.scale), cfg.margin_type, float(cfg.margin)
+    M = X.shape[0]
+    Xh, _ = normalize_rows(X)
+    Wh, _ = normalize_rows(w_rows(S))
+    cos = Xh @ Wh.T                                                  # M x |S|
+    pos = {int(g): t for t, g in enumerate(S)}
+    tcol = np.array([pos[int(y)] for y in Y])
+    rows = np.arange(M)
+    ct = cos[rows, tcol]
+    cos[rows, tcol] = margin_phi(ct, mt, m)                          # z / s (margin at the target, R11)
+    zmax = s * cos.max(axis=1)
+    lse = zmax + np.log(np.sum(np.exp(s * cos - zmax[:, None]), axis=1))
+    out = []
+    for t in cols:
+        gc = s * np.exp(s * cos[:, t] - lse) / M                    # dL/dcos for non-target rows
+        hit = tcol == t
+        gc[hit] = s * (np.exp(s * cos[hit, t] - lse[hit]) - 1.0) / M * margin_dphi(ct[hit], mt, m)
+        dwh = gc @ Xh
+        wr = np.asarray(w_rows(S[t:t + 1]), dtype=np.float64)[0]
+        wn = np.sqrt(np.sum(wr * wr))
+        wh = wr / max(wn, NORM_EPS)
+        out.append((dwh - wh * np.dot(wh, dwh)) / max(wn, NORM_EPS))
+    return np.array(out), lse

@@ -228,8 +228,8 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
   constexpr int KIND = base_kind(KIND_);
   using C = Cfg<KIND_>;
   using S = Smem<KIND_>;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);   // stays in the shared window
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * S::STAGE_BYTES);
   uint64_t* empty = full + C::STAGES;
   uint64_t* acc_full = empty + C::STAGES;
@@ -238,7 +238,7 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
   // fused-SGD staging (DWF only): the 128 x 128 fp32 dW_hat tile (float4-XOR-swizzled rows) + per-row
   // (row id, 1/||w||, radial factor)
   float4* s_tile = reinterpret_cast<float4*>(smem + C::STAGES * S::STAGE_BYTES + 256);
-  int64_t* s_rowj = reinterpret_cast<int64_t*>(s_tile + 128 * 32);
+  int32_t* s_rowj = reinterpret_cast<int32_t*>(s_tile + 128 * 32);
   float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
   float* s_rad = s_inv + 128;
 
@@ -344,27 +344,38 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
     const int row_in = lg * 32 + lane;       // accumulator row (TMEM lane) of this thread
     const int eset = (warp - 2) >> 2;        // with 8 epilogue warps: two sets splitting the 32-column chunks
     constexpr int NSET = C::EPI_WARPS / 4;
+    int32_t nx_j = -1;                       // DWF: per-row scalars of the next tile (prefetched)
+    float nx_inv = 0.f, nx_rad = 0.f;
+    if (KIND_ == DWF && eset == 0 && (int)blockIdx.x < w.n_units) {
+      int m1, n1, k0_, k1_;
+      w.decode(p, blockIdx.x, m1, n1, k0_, k1_);
+      const int prow = m1 + row_in;
+      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+    }
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
       int m0, n0, kb0, kb1;
       w.decode(p, u, m0, n0, kb0, kb1);
-      mbar_wait(&acc_full[acc], acc_phase);
-      tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * (C::MSUB * C::NMMA * C::UMMA_N);
+      if constexpr (KIND_ != DWF) {
+        mbar_wait(&acc_full[acc], acc_phase);
+        tc_fence_after();
+      }
       if constexpr (KIND_ == DWF) {
         // Fused lazy momentum SGD of 128 sampled classes x 128 dims (rows.cu K12 is the unfused
-        // form). (1) both warp sets copy the accumulator tile TMEM -> smem and release TMEM at once; (2) each
-        // of the 8 warps updates 16 rows, one 512-byte coalesced W and V segment per row and instruction.
+        // form). (1) two warp sets copy two 32-column chunks each of the accumulator TMEM -> smem, then TMEM is
+        // released; (2) each of the 8 warps updates 16 rows, one 512-byte coalesced W and V segment per row and
+        // instruction, 16 loads per lane in flight. The per-row scalars of tile u + gridDim are prefetched into
+        // registers during tile u so that no tile starts with a dependent global load.
         asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");  // previous tile consumed
         if (eset == 0) {
-          const int prow = m0 + row_in;
-          const bool rv = prow < k;
-          const float inv = rv ? p.sgd.inv_norm[prow] : 0.f;
-          s_rowj[row_in] = rv ? (int64_t)p.sgd.idx[prow] : -1;
-          s_inv[row_in] = inv;
-          s_rad[row_in] = rv ? p.sgd.dotw[prow] * inv : 0.f;     // w * rad = w_hat (w_hat . dw_hat)
+          s_rowj[row_in] = nx_j;
+          s_inv[row_in] = nx_inv;
+          s_rad[row_in] = nx_rad;
         }
+        mbar_wait(&acc_full[acc], acc_phase);
+        tc_fence_after();
 #pragma unroll 1
         for (int c = eset * 2; c < eset * 2 + 2; ++c) {
           uint32_t v[32];
@@ -380,25 +391,39 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
         if (lane == 0) mbar_arrive(&acc_empty[acc]);             // TMEM free: next tile's MMAs may start
         if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
         asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        if (eset == 0) {                                         // prefetch the next tile's per-row scalars
+          const int un = u + gridDim.x;
+          nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
+          if (un < w.n_units) {
+            int m1, n1, k0_, k1_;
+            w.decode(p, un, m1, n1, k0_, k1_);
+            const int prow = m1 + row_in;
+            if (prow < k) {
+              nx_j = p.sgd.idx[prow];
+              nx_inv = p.sgd.inv_norm[prow];
+              nx_rad = p.sgd.dotw[prow];
+            }
+          }
+        }
         const int ew = warp - 2;                                 // rows ew*16 .. ew*16+15
         const int col = n0 + lane * 4;
 #pragma unroll 1
         for (int r0 = 0; r0 < 16; r0 += 8) {
           float4 wv[8], mv[8];
+          int32_t jr[8];
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
-            const int64_t j = s_rowj[ew * 16 + r0 + r];
-            if (j >= 0) {
-              wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + j * p.d + col);
-              mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + j * p.d + col);
+            jr[r] = s_rowj[ew * 16 + r0 + r];
+            if (jr[r] >= 0) {
+              wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
+              mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
             }
           }
 #pragma unroll
           for (int r = 0; r < 8; ++r) {
             const int rr = ew * 16 + r0 + r;
-            const int64_t j = s_rowj[rr];
-            if (j >= 0) {
-              const float inv = s_inv[rr], rad = s_rad[rr];
+            if (jr[r] >= 0) {
+              const float inv = s_inv[rr], rad = s_rad[rr] * inv;  // w * rad = w_hat (w_hat . dw_hat)
               const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
               float4 w = wv[r], m = mv[r];
               m.x = p.sgd.mu * m.x + (g4.x - w.x * rad) * inv + p.sgd.lambda * w.x;
@@ -406,8 +431,8 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
               m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * inv + p.sgd.lambda * w.z;
               m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * inv + p.sgd.lambda * w.w;
               w.x -= p.sgd.lr * m.x; w.y -= p.sgd.lr * m.y; w.z -= p.sgd.lr * m.z; w.w -= p.sgd.lr * m.w;
-              *reinterpret_cast<float4*>(p.sgd.V + j * p.d + col) = m;
-              *reinterpret_cast<float4*>(p.sgd.W + j * p.d + col) = w;
+              *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
+              *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
             }
           }
         }

@@ -442,3 +442,18 @@ def test_spot_rows_agree_with_full_forward_backward():
     for (lse, lt, g), n in zip(res, [0, 5, 7]):
         assert lse == pytest.approx(out["lse"][n], rel=1e-13)
         assert np.allclose(g, gx[n], rtol=1e-10, atol=1e-16)
+
+
+def test_spot_cols_agree_with_full_forward_backward():
+    C, d, B, k = 400, 16, 5, 2
+    ys = make_labels(6, 0, k, B, C)
+    xs = make_features(6, 0, k, B, d, labels=ys, dist="trained", sigma=0.3, w_seed=0)
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, world_size=k, sample_rate=0.2, margin_type=MARGIN_ARCFACE, margin=0.5)
+    out = oracle.forward_backward(cfg, xs, ys, lambda i: w_rows_np(0, i, d), step=1)
+    S = np.concatenate(out["idx"])
+    X = np.concatenate(xs).astype(np.float64); Y = np.concatenate(ys)
+    cols = [0, 3, len(S) // 2, int(np.searchsorted(S, Y[0]))]
+    dW, lse = oracle.spot_cols(cfg, X, Y, S, lambda i: w_rows_np(0, i, d), cols)
+    full = np.concatenate(out["dW"])
+    assert np.allclose(lse, out["lse"], rtol=1e-13)
+    assert np.allclose(dW, full[cols], rtol=1e-10, atol=1e-16)
