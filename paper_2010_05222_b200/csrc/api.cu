@@ -256,7 +256,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->Ws, kp * d * esz);
   ALLOC(c->inv_norm, kp * 4);
   ALLOC(c->ct, M * 4);
-  ALLOC(c->cosv, M * kp * esz);
+  ALLOC(c->cosv, Mp * kp * esz);   // class-major [k_pad][M_pad]
   ALLOC(c->partials, M * (size_t)sz.n_ltiles * sizeof(float2));
   ALLOC(c->rowmax, M * 4);
   ALLOC(c->gmax, M * 4);
@@ -266,7 +266,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->gt, M * 4);
   ALLOC(c->lse, M * 4);
   ALLOC(c->loss_dev, 16);
-  ALLOC(c->G, M * kp * esz);
+  ALLOC(c->G, Mp * kp * esz);      // class-major [k_pad][M_pad]
   ALLOC(c->dXh, Mp * d * 4);
   ALLOC(c->dxh_local, B * d * 4);
   ALLOC(c->split_ws, (size_t)(c->use_tc ? dx_split_ws_floats(sz) : 1) * 4);

@@ -18,8 +18,8 @@ __device__ __forceinline__ float to_f(float v) { return v; }
 __device__ __forceinline__ float to_f(__nv_bfloat16 v) { return __bfloat162float(v); }
 
 struct Epi {
-  // logits
-  const int32_t* tcol; const float* ct; MarginParams mp; void* cosv; float2* partials; int ntiles; int bf16;
+  // logits (cos stored class-major: cosv[p * ldm + n])
+  const int32_t* tcol; const float* ct; MarginParams mp; void* cosv; float2* partials; int ntiles; int bf16; int ldm;
   // generic output
   float* C; int64_t ldc;
   int rows_valid;  // M for logits / dx; k for dw (read from st when < 0)
@@ -37,7 +37,7 @@ __global__ void __launch_bounds__(256) k_gemm(int Mdim, int64_t Ndim, int64_t Kd
   const int64_t n_base = (int64_t)blockIdx.x * BN;
   // data-dependent bounds: logits cols < k; dw rows < k; dx K-range < k
   int64_t Mlim = Mdim, Nlim = Ndim, Klo = 0, Khi = Kdim;
-  if (MODE == MODE_LOGITS) Nlim = k_sampled;
+  if (MODE == MODE_LOGITS) { Nlim = k_sampled; Mlim = e.ldm; }   // padding rows [M, M_pad) are stored as 0
   if (MODE == MODE_STORE) Mlim = k_sampled;
   if (MODE == MODE_ATOMIC) { Klo = (int64_t)blockIdx.z * k_chunk; Khi = min(Klo + k_chunk, (int64_t)k_sampled); }
   if (m_base >= Mlim || n_base >= Nlim || Klo >= Khi) return;
@@ -110,12 +110,13 @@ __global__ void __launch_bounds__(256) k_gemm(int Mdim, int64_t Ndim, int64_t Kd
       for (int j = 0; j < 4; ++j) {
         const int64_t p = n_base + tx + 16 * j;
         float c = acc[i][j];
+        const bool in = n < e.ldm && p < Ndim;     // rows [M, M_pad) get 0: K8 reads every stored cosine
         if (e.bf16) {
-          __half h = __float2half_rn(c);
+          __half h = __float2half_rn(rv ? c : 0.f);
           c = __half2float(h);
-          if (rv && p < Ndim) ((__half*)e.cosv)[n * Ndim + p] = h;
+          if (in) ((__half*)e.cosv)[p * e.ldm + n] = h;
         } else {
-          if (rv && p < Ndim) ((float*)e.cosv)[n * Ndim + p] = c;
+          if (in) ((float*)e.cosv)[p * e.ldm + n] = rv ? c : 0.f;
         }
         // the target column is excluded from the partials (finalize adds it exactly, see rows.cu)
         z[j] = (p < Nlim && p != tc) ? mp.s * c : -INFINITY;
@@ -161,7 +162,8 @@ int launch_logits_simt(const Sizes& sz, bool bf16, const void* X, const void* Ws
                        const SamplerState* st, MarginParams mp, void* cosv, float2* partials, cudaStream_t s) {
   Epi e{};
   e.tcol = tcol; e.ct = ct; e.mp = mp; e.cosv = cosv; e.partials = partials; e.ntiles = sz.n_ltiles; e.bf16 = bf16;
-  dim3 grid((unsigned)(sz.k_pad / BN), (unsigned)((sz.M + BM - 1) / BM));
+  e.ldm = sz.M_pad;
+  dim3 grid((unsigned)(sz.k_pad / BN), (unsigned)(sz.M_pad / BM));
   if (bf16)
     k_gemm<__nv_bfloat16, true, true, MODE_LOGITS><<<grid, 256, 0, s>>>(
         sz.M, sz.k_pad, sz.d, (const __nv_bfloat16*)X, sz.d, (const __nv_bfloat16*)Ws, sz.d, st, 0, e);
@@ -183,11 +185,11 @@ int launch_dx_simt(const Sizes& sz, bool bf16, const void* G, const void* Ws, co
   nsplit = (sz.k_pad + chunk - 1) / chunk;
   dim3 grid((unsigned)(sz.d / BN), (unsigned)((sz.M + BM - 1) / BM), (unsigned)nsplit);
   if (bf16)
-    k_gemm<__nv_bfloat16, true, false, MODE_ATOMIC><<<grid, 256, 0, s>>>(
-        sz.M, sz.d, sz.k_pad, (const __nv_bfloat16*)G, sz.k_pad, (const __nv_bfloat16*)Ws, sz.d, st, chunk, e);
+    k_gemm<__nv_bfloat16, false, false, MODE_ATOMIC><<<grid, 256, 0, s>>>(
+        sz.M, sz.d, sz.k_pad, (const __nv_bfloat16*)G, sz.M_pad, (const __nv_bfloat16*)Ws, sz.d, st, chunk, e);
   else
-    k_gemm<float, true, false, MODE_ATOMIC><<<grid, 256, 0, s>>>(sz.M, sz.d, sz.k_pad, (const float*)G, sz.k_pad,
-                                                                 (const float*)Ws, sz.d, st, chunk, e);
+    k_gemm<float, false, false, MODE_ATOMIC><<<grid, 256, 0, s>>>(sz.M, sz.d, sz.k_pad, (const float*)G, sz.M_pad,
+                                                                  (const float*)Ws, sz.d, st, chunk, e);
   return 2;
 }
 
@@ -197,11 +199,11 @@ int launch_dw_simt(const Sizes& sz, bool bf16, const void* G, const void* X, con
   e.C = dWh; e.ldc = sz.d;
   dim3 grid((unsigned)(sz.d / BN), (unsigned)(sz.k_pad / BM));
   if (bf16)
-    k_gemm<__nv_bfloat16, false, false, MODE_STORE><<<grid, 256, 0, s>>>(
-        (int)sz.k_pad, sz.d, sz.M, (const __nv_bfloat16*)G, sz.k_pad, (const __nv_bfloat16*)X, sz.d, st, 0, e);
+    k_gemm<__nv_bfloat16, true, false, MODE_STORE><<<grid, 256, 0, s>>>(
+        (int)sz.k_pad, sz.d, sz.M, (const __nv_bfloat16*)G, sz.M_pad, (const __nv_bfloat16*)X, sz.d, st, 0, e);
   else
-    k_gemm<float, false, false, MODE_STORE><<<grid, 256, 0, s>>>((int)sz.k_pad, sz.d, sz.M, (const float*)G, sz.k_pad,
-                                                                 (const float*)X, sz.d, st, 0, e);
+    k_gemm<float, true, false, MODE_STORE><<<grid, 256, 0, s>>>((int)sz.k_pad, sz.d, sz.M, (const float*)G, sz.M_pad,
+                                                                (const float*)X, sz.d, st, 0, e);
   return 1;
 }
 

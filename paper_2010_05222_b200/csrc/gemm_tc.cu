@@ -3,9 +3,10 @@
 //   K6  logits  C[M x k]  = X_hat[M x d] . W_s[k x d]^T     A K-major, B K-major   (Alg.1 L3)
 //       epilogue: fp16 cosine store, margin-free scaled logits z = s c, per-(row, 128-column tile) max and
 //       sum of e^{z - max} excluding the row's target column (finalize adds it exactly; rows.cu)
-//   K9  dX      dX[M x d] = Gc[M x k] . W_s[k x d]          A K-major, B MN-major  (Alg.1 L12)
+//   K9  dX      dX[M x d] = Gc[M x k] . W_s[k x d]          A MN-major, B MN-major (Alg.1 L12)
 //       split-K over the sampled classes, fp32 partial per split, deterministic reduction kernel
-//   K11 dW      dW[k x d] = Gc^T[k x M] . X_hat[M x d]      A MN-major, B MN-major (Alg.1 L10)
+//   K11 dW      dW[k x d] = Gc^T[k x M] . X_hat[M x d]      A K-major, B MN-major  (Alg.1 L10)
+// cos and Gc are stored class-major ([k_pad][M_pad]): per sampled class the batch entries are contiguous.
 //
 // One kernel template: a persistent, warp-specialised CTA (warp 0: TMA producer, warp 1: TMEM allocator and
 // single-thread MMA issuer, warps 2-5: epilogue reading the fp32 accumulator from TMEM with tcgen05.ld).
@@ -128,12 +129,12 @@ struct Cfg<LOGITS> {  // tile 256 x 128 (two M = 128 halves sharing the B tile),
 template <>
 struct Cfg<DX> {      // tile 256 x 256 (M halves x d half), K = a split of the sampled classes
   static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 256, STAGES = 3, ACC = 1, EPI_WARPS = 4;
-  static constexpr bool A_MN = false, B_MN = true;
+  static constexpr bool A_MN = true, B_MN = true;     // A = G class-major: batch rows contiguous
 };
 template <>
 struct Cfg<DW> {      // tile 128 classes x 256 dims, K = M (the global batch)
   static constexpr int MSUB = 1, NMMA = 1, UMMA_N = 256, STAGES = 4, ACC = 2, EPI_WARPS = 4;
-  static constexpr bool A_MN = true, B_MN = true;
+  static constexpr bool A_MN = false, B_MN = true;    // A = G class-major read as G^T: K (batch) contiguous
 };
 template <>
 struct Cfg<DX128> : Cfg<DX> { static constexpr int UMMA_N = 128, STAGES = 4; };
@@ -159,6 +160,7 @@ struct Smem {
 
 struct TcParams {
   int M;                 // global batch rows
+  int ldm;               // M rounded up to 128: leading dimension of the class-major cos / Gc
   int d;
   int64_t k_pad;
   const SamplerState* st;
@@ -282,14 +284,13 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
             tma_load_2d(sa + 128 * BK * 2, &tmA, &full[stage], kb * BK, m0 + 128);
             tma_load_2d(sb, &tmB, &full[stage], kb * BK, n0);
           } else if (KIND == DX) {
-            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
-            tma_load_2d(sa + 128 * BK * 2, &tmA, &full[stage], kb * BK, m0 + 128);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) tma_load_2d(sa + c * BK * 128, &tmA, &full[stage], m0 + c * 64, kb * BK);
 #pragma unroll
             for (int c = 0; c < C::UMMA_N / 64; ++c)
               tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
           } else {
-#pragma unroll
-            for (int c = 0; c < 2; ++c) tma_load_2d(sa + c * BK * 128, &tmA, &full[stage], m0 + c * 64, kb * BK);
+            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
 #pragma unroll
             for (int c = 0; c < C::UMMA_N / 64; ++c)
               tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
@@ -322,7 +323,7 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
 #pragma unroll
             for (int ms = 0; ms < C::MSUB; ++ms) {
               uint64_t ad, bd;
-              if (C::A_MN) ad = make_desc(sa + kk * 16 * 128, BK * 128, 1024);
+              if (C::A_MN) ad = make_desc(sa + ms * 128 * BK * 2 + kk * 16 * 128, BK * 128, 1024);
               else ad = make_desc(sa + ms * 128 * BK * 2 + kk * 32, 16, 1024);
               if (C::B_MN) bd = make_desc(sb + kk * 16 * 128, BK * 128, 1024);
               else bd = make_desc(sb + kk * 32, 16, 1024);
@@ -469,10 +470,23 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
               sum = (mx > -INFINITY ? sum * exp2f(mx - nmx) : 0.f) + cs;
               mx = nmx;
             }
-            if (rv) {
-              uint4* dst = reinterpret_cast<uint4*>(p.cosv + (int64_t)row * p.k_pad + col0);
+            // class-major store: lane pairs swap halves so that every 32-bit store covers rows (n, n+1)
+            // of one class; a warp instruction writes two 64-byte runs.
+            if (row < p.ldm) {
+              const bool odd = lane & 1;
+              __half* cb = p.cosv + (row & ~1);
 #pragma unroll
-              for (int q = 0; q < 4; ++q) dst[q] = *reinterpret_cast<const uint4*>(&h[q * 8]);
+              for (int i = 0; i < 16; ++i) {
+                const __half send = odd ? h[2 * i] : h[2 * i + 1];
+                const unsigned short rcv =
+                    (unsigned short)__shfl_xor_sync(0xffffffffu, (int)__half_as_ushort(send), 1);
+                const __half other = __ushort_as_half(rcv);
+                const __half2 pr = odd ? __halves2half2(other, h[2 * i + 1]) : __halves2half2(h[2 * i], other);
+                *reinterpret_cast<__half2*>(cb + (int64_t)(col0 + 2 * i + (odd ? 1 : 0)) * p.ldm) = pr;
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 16; ++i) __shfl_xor_sync(0xffffffffu, 0, 1);
             }
           }
           if (rv)
@@ -607,7 +621,7 @@ int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat
   CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
   TcParams p{};
-  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.tcol = tcol;
+  p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.tcol = tcol;
   p.s_log2e = mp.s * 1.4426950408889634f; p.cosv = cosv; p.partials = partials; p.n_ltiles = sz.n_ltiles;
   const int64_t units = ((sz.M + 255) / 256) * ((sz.k_pad + 127) / 128);
   launch<LOGITS>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
@@ -632,10 +646,10 @@ int64_t dx_split_ws_floats(const Sizes& sz) {
 
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st, float* dXh,
                  float* split_ws, cudaStream_t s) {
-  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 128);
+  CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 64);      // Gc class-major, MN-major A
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 64);
   TcParams p{};
-  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.split_ws = split_ws;
+  p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.split_ws = split_ws;
   const int tiles = ((sz.M + 255) / 256) * (sz.d / dtile(sz));
   int nsplit;
   dx_split(sz, nsplit, p.kb_per_split);
@@ -649,10 +663,10 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
 
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& sa, cudaStream_t s) {
-  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 64);
+  CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);     // Gc class-major, K-major A (= Gc^T)
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
   TcParams p{};
-  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
+  p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
   const int64_t units = (sz.k_pad / 128) * (sz.d / 128);
   launch<DWF>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
   return 1;
@@ -660,10 +674,10 @@ int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat1
 
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st, float* dWh,
                  cudaStream_t s) {
-  CUtensorMap a = make_map(G, sz.M, sz.k_pad, 64, 64);
+  CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
   TcParams p{};
-  p.M = sz.M; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.dWh = dWh;
+  p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.dWh = dWh;
   const int64_t units = (sz.k_pad / 128) * (sz.d / dtile(sz));
   if (dtile(sz) == 256) launch<DW>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
   else launch<DW128>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);

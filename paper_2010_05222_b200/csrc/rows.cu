@@ -7,6 +7,7 @@
 //   K8  softmax_grad     Gc = (s/M)(p - onehot) phi'(c_t) (Alg.1 L8-9)
 //   K10 xnorm_backward   dx = (dx_hat - x_hat (x_hat . dx_hat)) / ||x||
 //   K12 sgd              lazy momentum SGD of the sampled rows
+#include <algorithm>
 #include "pfc_internal.cuh"
 
 namespace pfc {
@@ -193,86 +194,134 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
   }
 }
 
-// ---------------------------------------------------------------- K8: softmax gradient
-// Column strips of 256 sampled classes per block; thread = 8 consecutive columns x every 8th row, so a warp
-// streams 512 contiguous bytes of one row. Gc = (s/M)(p - onehot) phi'(c_t) (Alg.1 L8-9). With DOT, also
-// dot[j] = sum_n Gc[n][j] c[n][j] = w_hat_j . dW_hat_j (the radial part the fused SGD epilogue removes).
+// ---------------------------------------------------------------- K8: softmax gradient (class-major)
+// cos and G are [k_pad][ldm] (ldm = M rounded up to 128): one warp streams one sampled class j at a time, a
+// lane owning 8 consecutive batch rows (16-byte loads/stores, 512 contiguous bytes per warp). Per-row data
+// (LSE, target column, target gradient) sits in shared memory.
+//   Gc[j][n] = (s/M) e^{z_nj - LSE_n}            j != t_n
+//            = (s/M) (p_t - 1) phi'(c_t)          j == t_n   (cancellation-free p_t - 1, rows.cu finalize)
+// With DOT: dot[j] = sum_n Gc[j][n] c[j][n] = w_hat_j . dW_hat_j (radial term of the fused SGD epilogue).
+template <bool BF16>
+__device__ __forceinline__ void load8(const void* cosv, int64_t base, float (&c)[8]) {
+  if (BF16) {
+    uint4 raw = __ldcs(reinterpret_cast<const uint4*>((const __half*)cosv + base));
+    const __half2* h = reinterpret_cast<const __half2*>(&raw);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); c[2 * i] = f.x; c[2 * i + 1] = f.y; }
+  } else {
+    float4 a = __ldcs(reinterpret_cast<const float4*>((const float*)cosv + base));
+    float4 b = __ldcs(reinterpret_cast<const float4*>((const float*)cosv + base + 4));
+    c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+  }
+}
+
+template <bool BF16>
+__device__ __forceinline__ void store8(void* G, int64_t base, const float (&g)[8]) {
+  if (BF16) {
+    uint4 o;
+    __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
+    *reinterpret_cast<uint4*>((__nv_bfloat16*)G + base) = o;
+  } else {
+    *reinterpret_cast<float4*>((float*)G + base) = make_float4(g[0], g[1], g[2], g[3]);
+    *reinterpret_cast<float4*>((float*)G + base + 4) = make_float4(g[4], g[5], g[6], g[7]);
+  }
+}
+
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// Every element as a non-target: Gc[j][n] = 2^min(c sl - off'_n, log2(s/M)) with off'_n = LSE_n log2 e -
+// log2(s/M) (the s/M factor folded into the exponent); padding rows have off' = +inf (their stored cosine is 0).
+// The target entries (one per row) are then rewritten by k_softmax_grad_targets.
 template <bool BF16, bool DOT>
-__global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, const void* __restrict__ cosv,
-                                                      const float* __restrict__ lse, const float* __restrict__ gt,
-                                                      const int32_t* __restrict__ tcol, const float* __restrict__ ct,
-                                                      const SamplerState* st, MarginParams mp, void* __restrict__ G,
+__global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int ldm, const void* __restrict__ cosv,
+                                                      const float* __restrict__ lse, const SamplerState* st,
+                                                      MarginParams mp, void* __restrict__ G,
                                                       float* __restrict__ dotw) {
-  __shared__ float red[8][257];
-  const int cg = threadIdx.x & 31, rp = threadIdx.x >> 5;
-  const int64_t c0 = (int64_t)blockIdx.x * 256 + cg * 8;
-  const int k = st->k;
+  extern __shared__ float s_off[];            // transposed: pos(n) = (n % 8) * (ldm / 8) + n / 8
   const float L2E = 1.4426950408889634f;
+  const float lgs = log2f(mp.s / (float)M);
+  const int l8 = ldm >> 3;
+  for (int n = threadIdx.x; n < ldm; n += blockDim.x) s_off[(n & 7) * l8 + (n >> 3)] = n < M ? lse[n] * L2E - lgs : INFINITY;
+  __syncthreads();
+  const int k = st->k;
   const float sl = mp.s * L2E;
-  const float gs = mp.s / (float)M;
-  float dacc[8];
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  constexpr int U = 2;
+  const int nit = (ldm + 255) / 256;
+  for (int it = 0; it < nit; ++it) {         // every lane runs every iteration (full-warp reductions)
+    const int n0 = it * 256 + lane * 8;
+    const bool act = n0 < ldm;
+    float off[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) dacc[i] = 0.f;
-  const bool any = c0 < k;
-  for (int n = rp; n < M; n += 8) {
-    const int64_t base = (int64_t)n * k_pad + c0;
-    float g[8];
-    if (any) {
-      const float off = lse[n] * L2E;
-      const int tc = tcol[n];
-      float c[8];
-      if (BF16) {
-        uint4 raw = *reinterpret_cast<const uint4*>((const __half*)cosv + base);
-        const __half2* h = reinterpret_cast<const __half2*>(&raw);
+    for (int i = 0; i < 8; ++i) off[i] = act ? s_off[i * l8 + lane + 32 * it] : INFINITY;
+    for (int64_t jb = w0; jb < k_pad; jb += U * nw) {
+      float c[U][8];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) { float2 f = __half22float2(h[i]); c[2 * i] = f.x; c[2 * i + 1] = f.y; }
-      } else {
-        float4 a = *reinterpret_cast<const float4*>((const float*)cosv + base);
-        float4 b = *reinterpret_cast<const float4*>((const float*)cosv + base + 4);
-        c[0] = a.x; c[1] = a.y; c[2] = a.z; c[3] = a.w; c[4] = b.x; c[5] = b.y; c[6] = b.z; c[7] = b.w;
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = jb + u * nw;
+        if (act && j < k) load8<BF16>(cosv, j * ldm + n0, c[u]);
       }
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const int64_t col = c0 + i;
-        if (col < k) {
-          if (col == tc) {
-            const float ctv = ct[n];
-            g[i] = gs * gt[n] * margin_dphi(mp, ctv);   // (p_t - 1) phi'(c_t), cancellation-free
-            c[i] = ctv;
-          } else {
-            g[i] = gs * exp2f(c[i] * sl - off);
+      for (int u = 0; u < U; ++u) {
+        const int64_t j = jb + u * nw;
+        if (j >= k_pad) break;
+        float g[8];
+        float d = 0.f;
+        if (act && j < k) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            // p <= 1 for every non-target entry (LSE >= z_j); the clamp only bounds the provisional value at
+            // the target column (margin not applied there), which k_softmax_grad_targets replaces exactly
+            g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -off[i]), lgs));
+            if (DOT) d = fmaf(g[i], c[u][i], d);
           }
         } else {
-          g[i] = 0.f;
+#pragma unroll
+          for (int i = 0; i < 8; ++i) g[i] = 0.f;
         }
-        if (DOT) dacc[i] += g[i] * c[i];
+        if (act) store8<BF16>(G, j * ldm + n0, g);
+        if (DOT) {
+          d = warp_sum(d);
+          if (lane == 0) {
+            if (it == 0) dotw[j] = d;
+            else dotw[j] += d;          // ldm > 256: the same warp owns class j in every row chunk
+          }
+        }
       }
-    } else {
-#pragma unroll
-      for (int i = 0; i < 8; ++i) g[i] = 0.f;
-    }
-    if (BF16) {
-      uint4 o;
-      __nv_bfloat162* ob = reinterpret_cast<__nv_bfloat162*>(&o);
-#pragma unroll
-      for (int i = 0; i < 4; ++i) ob[i] = __floats2bfloat162_rn(g[2 * i], g[2 * i + 1]);
-      *reinterpret_cast<uint4*>((__nv_bfloat16*)G + base) = o;
-    } else {
-      *reinterpret_cast<float4*>((float*)G + base) = make_float4(g[0], g[1], g[2], g[3]);
-      *reinterpret_cast<float4*>((float*)G + base + 4) = make_float4(g[4], g[5], g[6], g[7]);
     }
   }
-  if (DOT) {
-#pragma unroll
-    for (int i = 0; i < 8; ++i) red[rp][cg * 8 + i] = dacc[i];
-    __syncthreads();
-    if (threadIdx.x < 256) {
-      float v = 0.f;
-#pragma unroll
-      for (int r = 0; r < 8; ++r) v += red[r][threadIdx.x];
-      dotw[(int64_t)blockIdx.x * 256 + threadIdx.x] = v;
-    }
-  }
+}
+
+// Target entries: Gc[t_n][n] = (s/M)(p_t - 1) phi'(c_t) with the cancellation-free p_t - 1 of finalize, and the
+// radial dot corrected by (new - old) g c of that entry (several rows may share a class: atomics).
+template <bool BF16, bool DOT>
+__global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ cosv, const float* __restrict__ lse,
+                                       const float* __restrict__ gt, const int32_t* __restrict__ tcol,
+                                       const float* __restrict__ ct, MarginParams mp, void* __restrict__ G,
+                                       float* __restrict__ dotw) {
+  const int n = blockIdx.x * blockDim.x + threadIdx.x;
+  if (n >= M) return;
+  const int j = tcol[n];
+  if (j < 0) return;
+  const float L2E = 1.4426950408889634f;
+  const float gs = mp.s / (float)M;
+  const int64_t e = (int64_t)j * ldm + n;
+  const float cst = BF16 ? __half2float(((const __half*)cosv)[e]) : ((const float*)cosv)[e];
+  const float lgs = log2f(gs);
+  const float g_old = ex2_ftz(fminf(fmaf(cst, mp.s * L2E, -(lse[n] * L2E - lgs)), lgs));   // as k_softmax_grad
+  const float c_t = ct[n];
+  const float g_new = gs * gt[n] * margin_dphi(mp, c_t);
+  if (BF16) ((__nv_bfloat16*)G)[e] = __float2bfloat16_rn(g_new);
+  else ((float*)G)[e] = g_new;
+  if (DOT) atomicAdd(&dotw[j], g_new * c_t - g_old * cst);
 }
 
 // ---------------------------------------------------------------- K10
@@ -383,15 +432,36 @@ int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float*
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
                         float* dotw, cudaStream_t s) {
-  const unsigned grid = (unsigned)(sz.k_pad / 256);
-  if (bf16) {
-    if (dotw) k_softmax_grad<true, true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
-    else k_softmax_grad<true, false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
-  } else {
-    if (dotw) k_softmax_grad<false, true><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
-    else k_softmax_grad<false, false><<<grid, 256, 0, s>>>(sz.k_pad, sz.M, cosv, lse, gt, tcol, ct, st, mp, G, dotw);
+  const size_t smem = (size_t)sz.M_pad * sizeof(float);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_softmax_grad<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_softmax_grad<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_softmax_grad<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    cudaFuncSetAttribute(k_softmax_grad<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+    attr = true;
   }
-  return 1;
+  const unsigned grid = (unsigned)std::min<int64_t>(sz.k_pad / 8, 148 * 8);
+  const int ldm = sz.M_pad;
+  const unsigned tg = (unsigned)((sz.M + 255) / 256);
+  if (bf16) {
+    if (dotw) {
+      k_softmax_grad<true, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
+      k_softmax_grad_targets<true, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+    } else {
+      k_softmax_grad<true, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
+      k_softmax_grad_targets<true, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+    }
+  } else {
+    if (dotw) {
+      k_softmax_grad<false, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
+      k_softmax_grad_targets<false, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+    } else {
+      k_softmax_grad<false, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
+      k_softmax_grad_targets<false, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+    }
+  }
+  return 2;
 }
 
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm, float* grad_x,
