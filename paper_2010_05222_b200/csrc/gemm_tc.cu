@@ -88,6 +88,12 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ float ex2_ftz(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // UMMA shared-memory descriptor, 128-byte swizzle (layout type 2), version 1 (sm_100).
 //   K-major   : rows of 64 bf16 (128 B), 8-row atoms 1024 B apart (SBO), LBO unused (16 B)
 //   MN-major  : 64-element MN chunks of BK rows; SBO = 1024 (8 K-rows), LBO = chunk stride
@@ -123,7 +129,7 @@ template <int KIND>
 struct Cfg;
 template <>
 struct Cfg<LOGITS> {  // tile 256 x 128 (two M = 128 halves sharing the B tile), K = d
-  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 128, STAGES = 4, ACC = 2, EPI_WARPS = 4;
+  static constexpr int MSUB = 2, NMMA = 1, UMMA_N = 128, STAGES = 4, ACC = 2, EPI_WARPS = 8;
   static constexpr bool A_MN = false, B_MN = false;
 };
 template <>
@@ -150,11 +156,11 @@ struct Smem {
   static constexpr int B_BYTES = C::NMMA * C::UMMA_N * BK * 2;      // per stage
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = C::MSUB * C::NMMA * C::UMMA_N * C::ACC;
-  static constexpr int EPI_BYTES = KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 0;
+  static constexpr int EPI_BYTES = KIND == DWF ? 128 * 128 * 4 + 128 * 16 : KIND == LOGITS ? 2 * 2 * 128 * 8 : 0;
   static constexpr int THREADS = 64 + 32 * C::EPI_WARPS;
   static constexpr int TOTAL = C::STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BYTES;
   static_assert(TMEM_COLS <= 512, "TMEM overflow");
-  static_assert(C::STAGES * STAGE_BYTES + 1024 + 256 + (KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 0) <= 232448,
+  static_assert(C::STAGES * STAGE_BYTES + 1024 + 256 + (KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 4096) <= 232448,
                 "shared memory overflow (227 KB per CTA)");
 };
 
@@ -167,6 +173,7 @@ struct TcParams {
   // logits epilogue
   const int32_t* tcol;
   float s_log2e;         // s * log2(e)
+  float scale;           // s
   __half* cosv;          // M x k_pad
   float2* partials;      // M x n_ltiles
   int n_ltiles;
@@ -243,6 +250,8 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
   int32_t* s_rowj = reinterpret_cast<int32_t*>(s_tile + 128 * 32);
   float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
   float* s_rad = s_inv + 128;
+  // logits: per-row (max cos, sum) of the second warp set, per accumulator buffer and M-half
+  float2* s_part = reinterpret_cast<float2*>(smem + C::STAGES * S::STAGE_BYTES + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int k = p.st->k;
@@ -439,59 +448,96 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
         }
         continue;
       }
-#pragma unroll 1
-      for (int ms = 0; ms < C::MSUB; ++ms) {
-        const int row = m0 + ms * 128 + row_in;
-        if (KIND == LOGITS) {
+      if constexpr (KIND_ == LOGITS) {
+        // Two warp sets split the 128 columns (64 each). Per row and set: fp16-round the cosines (the rounded
+        // value is what K7/K8 see), store them class-major, and accumulate max c and sum 2^{(c - max) s log2 e}
+        // over the columns that are sampled (< k_i) and not the row's target (R22); set 1 hands its pair to
+        // set 0 through shared memory, set 0 writes the (row, tile) partial in natural units (max z = s max c).
+        const float sl = p.s_log2e;
+        float pm[C::MSUB], ps[C::MSUB];
+#pragma unroll
+        for (int ms = 0; ms < C::MSUB; ++ms) {
+          const int row = m0 + ms * 128 + row_in;
           const bool rv = row < p.M;
           const int tc = rv ? p.tcol[row] : -1;
           float mx = -INFINITY, sum = 0.f;
 #pragma unroll 1
-          for (int c = 0; c < C::UMMA_N / 32; ++c) {
+          for (int c = eset * 2; c < eset * 2 + 2; ++c) {
             uint32_t v[32];
             tmem_ld32(tacc + ms * C::UMMA_N + c * 32, v);
             const int col0 = n0 + c * 32;
-            __half h[32];
-            float z[32];
-            float cmx = -INFINITY;
+            __half2 h2[16];
+            float cf[32];
 #pragma unroll
-            for (int j = 0; j < 32; ++j) {
-              h[j] = __float2half_rn(__uint_as_float(v[j]));
-              const int col = col0 + j;
-              const bool ok = (col < k) && (col != tc);
-              z[j] = ok ? __half2float(h[j]) * p.s_log2e : -INFINITY;
-              cmx = fmaxf(cmx, z[j]);
+            for (int i = 0; i < 16; ++i) {
+              h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+              const float2 f = __half22float2(h2[i]);
+              cf[2 * i] = f.x;
+              cf[2 * i + 1] = f.y;
             }
+            if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {     // rare: mask columns >= k_i and the target
+#pragma unroll
+              for (int j = 0; j < 32; ++j)
+                if (col0 + j >= k || col0 + j == tc) cf[j] = -INFINITY;
+            }
+            float cmx = cf[0];
+#pragma unroll
+            for (int j = 1; j < 32; ++j) cmx = fmaxf(cmx, cf[j]);
             const float nmx = fmaxf(mx, cmx);
             if (nmx > -INFINITY) {
+              const float nb = nmx * sl;
               float cs = 0.f;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) cs += exp2f(z[j] - nmx);
-              sum = (mx > -INFINITY ? sum * exp2f(mx - nmx) : 0.f) + cs;
+              for (int j = 0; j < 32; ++j) cs += ex2_ftz(fmaf(cf[j], sl, -nb));
+              sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + cs;
               mx = nmx;
             }
-            // class-major store: lane pairs swap halves so that every 32-bit store covers rows (n, n+1)
-            // of one class; a warp instruction writes two 64-byte runs.
-            if (row < p.ldm) {
-              const bool odd = lane & 1;
-              __half* cb = p.cosv + (row & ~1);
+            // class-major store: lane pairs swap halves so that every 32-bit store covers rows (n, n+1) of one
+            // class; a warp instruction writes two 64-byte runs
+            const bool odd = lane & 1;
+            __half* cb = p.cosv + (row & ~1);
 #pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                const __half send = odd ? h[2 * i] : h[2 * i + 1];
-                const unsigned short rcv =
-                    (unsigned short)__shfl_xor_sync(0xffffffffu, (int)__half_as_ushort(send), 1);
-                const __half other = __ushort_as_half(rcv);
-                const __half2 pr = odd ? __halves2half2(other, h[2 * i + 1]) : __halves2half2(h[2 * i], other);
-                *reinterpret_cast<__half2*>(cb + (int64_t)(col0 + 2 * i + (odd ? 1 : 0)) * p.ldm) = pr;
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 16; ++i) __shfl_xor_sync(0xffffffffu, 0, 1);
+            for (int i = 0; i < 16; ++i) {
+              const __half send = odd ? __low2half(h2[i]) : __high2half(h2[i]);
+              const unsigned short rcv = (unsigned short)__shfl_xor_sync(0xffffffffu, (int)__half_as_ushort(send), 1);
+              const __half other = __ushort_as_half(rcv);
+              const __half2 pr = odd ? __halves2half2(other, __high2half(h2[i])) : __halves2half2(__low2half(h2[i]), other);
+              if (row < p.ldm) *reinterpret_cast<__half2*>(cb + (int64_t)(col0 + 2 * i + (odd ? 1 : 0)) * p.ldm) = pr;
             }
           }
-          if (rv)
-            p.partials[(int64_t)row * p.n_ltiles + n0 / 128] =
-                make_float2(mx > -INFINITY ? mx * 0.69314718055994531f : -INFINITY, sum);
+          pm[ms] = mx;
+          ps[ms] = sum;
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[acc]);             // accumulator consumed
+        float2* sp = s_part + acc * (C::MSUB * 128);
+        if (eset == 1) {
+#pragma unroll
+          for (int ms = 0; ms < C::MSUB; ++ms) sp[ms * 128 + row_in] = make_float2(pm[ms], ps[ms]);
+        }
+        asm volatile("bar.sync 4, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+        if (eset == 0) {
+#pragma unroll
+          for (int ms = 0; ms < C::MSUB; ++ms) {
+            const int row = m0 + ms * 128 + row_in;
+            const float2 o = sp[ms * 128 + row_in];
+            const float m = fmaxf(pm[ms], o.x);
+            float l = 0.f;
+            if (m > -INFINITY)
+              l = (pm[ms] > -INFINITY ? ps[ms] * ex2_ftz((pm[ms] - m) * sl) : 0.f) +
+                  (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
+            if (row < p.M)
+              p.partials[(int64_t)row * p.n_ltiles + n0 / 128] = make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
+          }
+        }
+        if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+        continue;
+      }
+#pragma unroll 1
+      for (int ms = 0; ms < C::MSUB; ++ms) {
+        const int row = m0 + ms * 128 + row_in;
+        if (false) {
         } else if (KIND == DX) {
           const int sp = u / (w.mt * w.nt);
           const bool rv = row < p.M;
@@ -622,7 +668,7 @@ int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.tcol = tcol;
-  p.s_log2e = mp.s * 1.4426950408889634f; p.cosv = cosv; p.partials = partials; p.n_ltiles = sz.n_ltiles;
+  p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials; p.n_ltiles = sz.n_ltiles;
   const int64_t units = ((sz.M + 255) / 256) * ((sz.k_pad + 127) / 128);
   launch<LOGITS>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
   return 1;
