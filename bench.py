@@ -136,18 +136,18 @@ def roofline_entry(section, ms, launches, M, k, d, peaks, traffic):
 # ------------------------------------------------------------------------------------------------ CPU baseline
 def cpu_baseline(cfgname, budget_s=25.0, steps=1, warm=0):
     """The oracle (oracle/, float64 numpy, as it stands) on the host cores, on a bounded sample of the
-    workload: B_ref = 8 samples against a contiguous C_ref-class slice of the shard (r, margin, d as the
-    workload), one full step (sampler, forward, backward, momentum SGD) per bench step. Every part of the
-    oracle step scales with the class count, so samples/s of the full workload ~ B_ref (C_ref / C) / t."""
+    workload: a contiguous C_ref-class slice of the shard (r, margin, d as the workload), one full oracle step
+    (sampler, forward, backward, momentum SGD) with 8 and with 16 samples; the per-step fixed cost and the
+    per-sample cost are fitted from the two and extrapolated to the workload's batch B, then scaled by class count
+    (every part of the oracle step is proportional to it): samples/s ~ B (C_ref / C) / (t_fix + B t_row)."""
     import torch
     import oracle
     import synth
     from oracle import OracleConfig
     C, d, B, r, mt, m, _ = CONFIGS[cfgname]
-    B_ref = 8
     MT = {"none": 0, "arcface": 1, "cosface": 2}
 
-    def one(C_ref, step):
+    def one(C_ref, B_ref, step):
         cfg = OracleConfig(num_classes=C_ref, dim=d, batch=B_ref, sample_rate=r, scale=SCALE, margin_type=MT[mt],
                            margin=m, momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, seed=0)
         ys = synth.make_labels(0, step, 1, B_ref, C_ref)
@@ -167,21 +167,26 @@ def cpu_baseline(cfgname, budget_s=25.0, steps=1, warm=0):
         return time.perf_counter() - t0
 
     probe_c = min(C, 100_000)
-    tp = one(probe_c, 0)
+    tp = one(probe_c, 8, 0)
     per_class = tp / probe_c
-    C_ref = int(min(C, max(20_000, budget_s / max(steps, 1) / per_class)))
-    times = []
+    C_ref = int(min(C, max(20_000, budget_s / (2 * max(steps, 1)) / per_class)))
+    t8, t16 = [], []
     for i in range(warm + steps):
-        t = one(C_ref, i + 1)
+        a, b = one(C_ref, 8, 2 * i + 1), one(C_ref, 16, 2 * i + 2)
         if i >= warm:
-            times.append(t)
-    t = float(np.mean(times))
-    value = B_ref * (C_ref / C) / t
+            t8.append(a)
+            t16.append(b)
+    a, b = float(np.mean(t8)), float(np.mean(t16))
+    t_row = max((b - a) / 8.0, 0.0)
+    t_fix = max(a - 8 * t_row, 0.0)
+    t_step = t_fix + B * t_row
+    value = B * (C_ref / C) / t_step
     return {"value": value, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "oracle",
-            "sample": f"{B_ref} samples x {C_ref}-class slice of the {C}-class shard per step (r={r}, d={d}), "
-                      f"full oracle step (sampler, fwd, bwd, SGD) in float64 numpy; value = {B_ref}*({C_ref}/{C})/"
-                      f"{t:.3f}s, i.e. scaled to the full workload by class count; {len(times)} step(s)",
-            "seconds_per_step": t}
+            "sample": f"oracle steps on a {C_ref}-class slice of the {C}-class shard (r={r}, d={d}) with 8 and 16 "
+                      f"samples ({a:.3f} s, {b:.3f} s per full step: sampler, fwd, bwd, SGD, float64 numpy); fitted "
+                      f"{t_fix:.3f} s/step + {t_row*1e3:.1f} ms/sample, extrapolated to B={B} and scaled by class "
+                      f"count C/C_ref; {len(t8)} step pair(s)",
+            "seconds_per_step": t_step * C / C_ref}
 
 
 # ------------------------------------------------------------------------------------------------ main

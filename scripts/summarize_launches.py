@@ -1,0 +1,36 @@
+"""Summarise an ncu launch-list CSV (gpu__time_duration + dram bytes per launch) per kernel, and write
+profiles/ncu_traffic.json for bench.py's `traffic` field.
+    python scripts/summarize_launches.py launches.csv out_summary.csv [workload] [n_gpus]"""
+import collections, csv, json, re, sys
+src, out = sys.argv[1], sys.argv[2]
+workload = sys.argv[3] if len(sys.argv) > 3 else "c4"
+ngpu = int(sys.argv[4]) if len(sys.argv) > 4 else 1
+rows = [r for r in csv.reader(open(src)) if r]
+hi = [i for i, r in enumerate(rows) if 'Kernel Name' in r][0]
+h = rows[hi]; ci = {n: i for i, n in enumerate(h)}
+data = collections.defaultdict(dict)
+for r in rows[hi + 1:]:
+    data[(r[ci['ID']], r[ci['Kernel Name']])][r[ci['Metric Name']]] = (float(r[ci['Metric Value']].replace(',', '')), r[ci['Metric Unit']])
+mult = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1e-3, 'us': 1, 'ms': 1e3}
+agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
+for (i, name), m in data.items():
+    short = re.search(r'(k_[a-z0-9_]+(<[^>]*>)?)', name).group(1)
+    a = agg[short]; a[0] += 1
+    t = m['gpu__time_duration.sum']; a[1] += t[0] * mult[t[1]]
+    for mm, idx in (('dram__bytes_read.sum', 2), ('dram__bytes_write.sum', 3)):
+        v, u = m[mm]; a[idx] += v * mult[u]
+tot = sum(a[1] for a in agg.values())
+sec = {'k_tc_gemm<5>': 'dw_gemm_sgd', 'k_tc_gemm<0>': 'logits_gemm', 'k_tc_gemm<1>': 'dx_gemm', 'k_gather_w<1>': 'gather_w',
+       'k_softmax_grad<1, 1>': 'softmax_grad'}
+lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU): cold-cache, serialised launches",
+         "# k_tc_gemm<0> = logits (K6), <1> = dx split-K (K9), <5> = dW + fused momentum SGD (K11+K12)",
+         "kernel, launches, avg_us, share_of_step, dram_read_MB_per_launch, dram_write_MB_per_launch"]
+traffic = {}
+for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+    lines.append(f"{name}, {a[0]}, {a[1]/a[0]:.1f}, {a[1]/tot:.3f}, {a[2]/a[0]/1e6:.1f}, {a[3]/a[0]/1e6:.1f}")
+    if name in sec:
+        traffic[sec[name]] = round((a[2] + a[3]) / a[0])
+open(out, 'w').write("\n".join(lines) + "\n")
+json.dump({"workload": workload, "n_gpus": ngpu, "source": src + " (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)",
+           "bytes_per_launch": traffic}, open('profiles/ncu_traffic.json', 'w'), indent=1)
+print("\n".join(lines[2:10]))
