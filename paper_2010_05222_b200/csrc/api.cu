@@ -80,6 +80,19 @@ struct pfc_ctx {
   float* x_in = nullptr;
   int64_t* y_in = nullptr;
   float* gx_out = nullptr;
+  // device-resident step counter and learning rate (the step is CUDA-graph replayable)
+  uint64_t* step_dev = nullptr;
+  float* lr_dev = nullptr;
+  bool graph_on = true;
+  int graph_warm = 0;
+  int64_t graph_launches = 0;     // kernels inside one captured step
+  struct GraphEntry {
+    const void *x, *y, *gx, *loss;
+    cudaStream_t s;
+    bool fused;
+    cudaGraphExec_t exec;
+  };
+  std::vector<GraphEntry> graphs;
   // per-kernel event timing (pfc_profile_*)
   bool prof = false;
   std::vector<std::array<cudaEvent_t, PFC_PROF_SECTIONS + 1>> prof_ev;
@@ -273,6 +286,8 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->dWh, kp * d * 4);
   ALLOC(c->dotw, kp * 4);
   ALLOC(c->err_dev, 16);
+  ALLOC(c->step_dev, 16);
+  ALLOC(c->lr_dev, 16);
   ALLOC(c->x_in, B * d * 4);
   ALLOC(c->y_in, B * 8);
   ALLOC(c->gx_out, B * d * 4);
@@ -283,6 +298,12 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   cudaMemset(c->Xb, 0, Mp * d * 2);
   cudaMemset(c->dXh, 0, Mp * d * 4);
   cudaMemset(c->err_dev, 0, 16);
+  cudaMemset(c->step_dev, 0, 16);
+  cudaMemset(c->lr_dev, 0, 16);
+  {
+    const char* g = std::getenv("PFC_GRAPH");
+    c->graph_on = !(g && g[0] == '0');
+  }
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) {
     std::string m = std::string("init memset: ") + cudaGetErrorString(e);
@@ -307,6 +328,7 @@ pfc_status pfc_destroy(pfc_ctx* c) {
   if (!c) return PFC_OK;
   cudaSetDevice(c->cfg.device);
   cudaDeviceSynchronize();
+  for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->comm) ncclCommDestroy(c->comm);
   for (auto& ev : c->prof_ev)
     for (auto& e : ev) cudaEventDestroy(e);
@@ -361,7 +383,7 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
   int n = 0;
   mark(c, 1, s);
   if (bf) n += launch_x_to_bf16(sz, c->X32, c->Xb, s);
-  n += launch_sampler(sz, c->Y, c->cfg.seed, (uint32_t)c->step, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
+  n += launch_sampler(sz, c->Y, c->cfg.seed, c->step_dev, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
                       c->tcol, c->err_dev, s);
   mark(c, 2, s);
   n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
@@ -400,13 +422,13 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
 }
 
 // after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat (+ K12 when fused)
-void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, float lr, cudaStream_t s) {
+void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
   n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
   mark(c, 8, s);
   if (c->use_tc && fused) {
-    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, lr, c->cfg.momentum, c->cfg.weight_decay};
+    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay};
     n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, s);
   } else {
     if (c->use_tc)
@@ -414,7 +436,8 @@ void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, float lr, 
     else
       n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
     if (fused)
-      n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, lr, c->cfg.momentum, c->cfg.weight_decay, s);
+      n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
+                      c->cfg.weight_decay, s);
   }
   mark(c, 9, s);
   c->launches += n;
@@ -447,6 +470,39 @@ pfc_status pfc_train_step(pfc_ctx* c, const float* x, const int64_t* labels, flo
   return run_step(c, x, labels, grad_x, loss, true, lr, stream);
 }
 
+static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss_out, bool fused,
+                         cudaStream_t s, ncclResult_t* nres) {
+  const Sizes& sz = c->sz;
+  const bool multi = sz.world > 1;
+  *nres = ncclSuccess;
+  auto nccl = [&](ncclResult_t r) { if (r != ncclSuccess && *nres == ncclSuccess) *nres = r; };
+  mark(c, 0, s);
+  phase_a(c, x, labels, s);
+  if (multi) {  // Alg.1 L2: X = allgather(x_i) (+ labels, PAPER.md:297)
+    nccl(ncclGroupStart());
+    nccl(ncclAllGather(c->X32 + (size_t)sz.rank * sz.B * sz.d, c->X32, (size_t)sz.B * sz.d, ncclFloat, c->comm, s));
+    nccl(ncclAllGather(c->Y + (size_t)sz.rank * sz.B, c->Y, (size_t)sz.B, ncclInt64, c->comm, s));
+    nccl(ncclGroupEnd());
+  }
+  phase_b(c, s);
+  const float* gmax = c->rowmax;
+  if (multi) {  // Alg.1 L7 (stabilised, R12): global row max, then global sum
+    nccl(ncclAllReduce(c->rowmax, c->gmax, sz.M, ncclFloat, ncclMax, c->comm, s));
+    gmax = c->gmax;
+  }
+  phase_c(c, gmax, s);
+  if (multi) nccl(ncclAllReduce(c->red, c->red, 2 * sz.M, ncclFloat, ncclSum, c->comm, s));
+  phase_d(c, gmax, loss_out, fused, s);
+  mark(c, 7, s);
+  const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
+  if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
+    nccl(ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
+    dxh = c->dxh_local;
+  }
+  phase_e(c, dxh, grad_x, fused, s);
+  c->launches += launch_advance_step(c->step_dev, s);
+}
+
 static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss, bool fused,
                            float lr, void* stream) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
@@ -455,35 +511,48 @@ static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, fl
   if (c->sz.world > 1 && c->cfg.comm_mode == PFC_COMM_LOOPBACK)
     return set_err(c, PFC_ERR_CONTRACT, "loopback contexts are driven by pfc_group_forward_backward");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  const Sizes& sz = c->sz;
-  const bool multi = sz.world > 1;
   float* loss_out = loss ? loss : c->loss_dev;
-
-  prof_begin_step(c);
-  mark(c, 0, s);
-  phase_a(c, x, labels, s);
-  if (multi) {  // Alg.1 L2: X = allgather(x_i) (+ labels, PAPER.md:297)
-    NCCL_TRY(c, ncclGroupStart());
-    NCCL_TRY(c, ncclAllGather(c->X32 + (size_t)sz.rank * sz.B * sz.d, c->X32, (size_t)sz.B * sz.d, ncclFloat, c->comm, s));
-    NCCL_TRY(c, ncclAllGather(c->Y + (size_t)sz.rank * sz.B, c->Y, (size_t)sz.B, ncclInt64, c->comm, s));
-    NCCL_TRY(c, ncclGroupEnd());
+  if (fused) c->launches += launch_set_scalar(c->lr_dev, lr, s);   // outside any graph: a kernel argument
+  ncclResult_t nres = ncclSuccess;
+  const bool use_graph = c->graph_on && !c->prof && s != nullptr;
+  if (!use_graph) {
+    prof_begin_step(c);
+    enqueue_step(c, x, labels, grad_x, loss_out, fused, s, &nres);
+    if (nres != ncclSuccess) return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres));
+    return finish_fb(c, fused, s);
   }
-  phase_b(c, s);
-  const float* gmax = c->rowmax;
-  if (multi) {  // Alg.1 L7 (stabilised, R12): global row max, then global sum
-    NCCL_TRY(c, ncclAllReduce(c->rowmax, c->gmax, sz.M, ncclFloat, ncclMax, c->comm, s));
-    gmax = c->gmax;
+  // CUDA graph of the whole step, cached per (pointers, stream, fused); the first call of a context runs eagerly
+  // (one-time kernel attribute setup), later calls capture once and replay.
+  for (auto& g : c->graphs) {
+    if (g.x == x && g.y == labels && g.gx == grad_x && g.loss == loss_out && g.s == s && g.fused == fused) {
+      CUDA_TRY(c, cudaGraphLaunch(g.exec, s));
+      c->launches += c->graph_launches;
+      return finish_fb(c, fused, s);
+    }
   }
-  phase_c(c, gmax, s);
-  if (multi) NCCL_TRY(c, ncclAllReduce(c->red, c->red, 2 * sz.M, ncclFloat, ncclSum, c->comm, s));
-  phase_d(c, gmax, loss_out, fused, s);
-  mark(c, 7, s);
-  const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
-  if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
-    NCCL_TRY(c, ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
-    dxh = c->dxh_local;
+  if (c->graph_warm++ == 0 || c->graphs.size() >= 8) {
+    prof_begin_step(c);
+    enqueue_step(c, x, labels, grad_x, loss_out, fused, s, &nres);
+    if (nres != ncclSuccess) return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres));
+    return finish_fb(c, fused, s);
   }
-  phase_e(c, dxh, grad_x, fused, lr, s);
+  cudaGraph_t graph = nullptr;
+  CUDA_TRY(c, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+  const int64_t l0 = c->launches;
+  c->prof_cur = nullptr;
+  enqueue_step(c, x, labels, grad_x, loss_out, fused, s, &nres);
+  cudaError_t ce = cudaStreamEndCapture(s, &graph);
+  c->graph_launches = c->launches - l0;
+  c->launches = l0;
+  if (nres != ncclSuccess) { if (graph) cudaGraphDestroy(graph); return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres)); }
+  CUDA_TRY(c, ce);
+  cudaGraphExec_t exec = nullptr;
+  ce = cudaGraphInstantiate(&exec, graph, 0);
+  cudaGraphDestroy(graph);
+  CUDA_TRY(c, ce);
+  c->graphs.push_back({x, labels, grad_x, loss_out, s, fused, exec});
+  CUDA_TRY(c, cudaGraphLaunch(exec, s));
+  c->launches += c->graph_launches;
   return finish_fb(c, fused, s);
 }
 
@@ -516,6 +585,8 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   }
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   for (int r = 0; r < n; ++r) ctxs[r]->prof_cur = nullptr;  // no event timing in loopback groups
+  if (fused)
+    for (int r = 0; r < n; ++r) ctxs[r]->launches += launch_set_scalar(ctxs[r]->lr_dev, lr, s);
   const Sizes& sz = ctxs[0]->sz;
   const size_t rowbytes = (size_t)sz.B * sz.d * 4;
   pfc_ctx* c0 = ctxs[0];
@@ -542,7 +613,10 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
     one.p[0] = ctxs[r]->dxh_local;
     c0->launches += launch_group_reduce((int64_t)sz.B * sz.d, src, (int64_t)r * sz.B * sz.d, one, n, 1, 0, s);
   }
-  for (int r = 0; r < n; ++r) phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], fused, lr, s);
+  for (int r = 0; r < n; ++r) {
+    phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], fused, s);
+    ctxs[r]->launches += launch_advance_step(ctxs[r]->step_dev, s);
+  }
   for (int r = 0; r < n; ++r) {
     pfc_status f = finish_fb(ctxs[r], fused, s);
     if (f != PFC_OK) return f;
@@ -585,7 +659,8 @@ pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
     prof_begin_step(c);
     mark(c, 9, s);
   }
-  c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, lr, c->cfg.momentum,
+  c->launches += launch_set_scalar(c->lr_dev, lr, s);
+  c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
                             c->cfg.weight_decay, s);
   if (c->prof) mark(c, 10, s);
   CUDA_TRY(c, cudaGetLastError());
@@ -679,6 +754,8 @@ pfc_status pfc_get_step(const pfc_ctx* c, uint64_t* step) {
 
 pfc_status pfc_set_step(pfc_ctx* c, uint64_t step) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  CUDA_TRY(c, cudaMemcpy(c->step_dev, &step, sizeof(step), cudaMemcpyHostToDevice));
   c->step = step;
   c->fb_done = false;
   return PFC_OK;
@@ -738,6 +815,7 @@ pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, ui
   int *hist = nullptr, *tile = nullptr, *err = nullptr;
   SamplerState* st = nullptr;
   int32_t *idx = nullptr, *tcol = nullptr;
+  uint64_t* step_dev = nullptr;
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 16)); };
   A((void**)&bits, ((sz.C_local + 31) / 32) * 4);
@@ -748,12 +826,14 @@ pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, ui
   A((void**)&st, sizeof(SamplerState));
   A((void**)&idx, sz.k_max * 4);
   A((void**)&tcol, (size_t)M * 4);
+  A((void**)&step_dev, 16);
   pfc_status res = PFC_OK;
   if (e != cudaSuccess) {
     res = set_err(nullptr, PFC_ERR_OOM, cudaGetErrorString(e));
   } else {
     cudaMemsetAsync(err, 0, 16, s);
-    launch_sampler(sz, labels, seed, (uint32_t)step, bits, keys, hist, tile, st, idx, tcol, err, s);
+    cudaMemcpyAsync(step_dev, &step, sizeof(step), cudaMemcpyHostToDevice, s);
+    launch_sampler(sz, labels, seed, step_dev, bits, keys, hist, tile, st, idx, tcol, err, s);
     launch_idx_to_global(sz.k_max, idx, st, sz.a, idx_out, s);
     SamplerState h{};
     int herr = 0;
@@ -765,7 +845,7 @@ pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, ui
     *k_out = h.k;
   }
   cudaFree(bits); cudaFree(keys); cudaFree(hist); cudaFree(tile); cudaFree(err); cudaFree(st); cudaFree(idx);
-  cudaFree(tcol);
+  cudaFree(tcol); cudaFree(step_dev);
   return res;
 }
 

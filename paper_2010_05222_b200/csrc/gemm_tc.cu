@@ -417,6 +417,7 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
         }
         const int ew = warp - 2;                                 // rows ew*16 .. ew*16+15
         const int col = n0 + lane * 4;
+        const float lr = *p.sgd.lr;                              // device scalar (CUDA-graph replayable)
 #pragma unroll 1
         for (int r0 = 0; r0 < 16; r0 += 8) {
           float4 wv[8], mv[8];
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
               m.y = p.sgd.mu * m.y + (g4.y - w.y * rad) * inv + p.sgd.lambda * w.y;
               m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * inv + p.sgd.lambda * w.z;
               m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * inv + p.sgd.lambda * w.w;
-              w.x -= p.sgd.lr * m.x; w.y -= p.sgd.lr * m.y; w.z -= p.sgd.lr * m.z; w.w -= p.sgd.lr * m.w;
+              w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
               *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
               *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
             }

@@ -109,7 +109,7 @@ constexpr int kSelTile = 8192;   // sampler compaction tile (256 threads x 32)
 constexpr int kKPad = 256;       // k_pad granularity (multiple of every GEMM tile width)
 
 // sampler.cu
-int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, uint32_t step, uint32_t* bits,
+int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint64_t* step_dev, uint32_t* bits,
                    uint32_t* keys, int* hist, int* tile_cnt, SamplerState* st, int32_t* idx, int32_t* tcol,
                    int* err, cudaStream_t s);
 
@@ -133,7 +133,9 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
                           float* grad_x, cudaStream_t s);
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
-               const SamplerState* st, float lr, float mu, float lambda, cudaStream_t s);
+               const SamplerState* st, const float* lr_dev, float mu, float lambda, cudaStream_t s);
+int launch_set_scalar(float* dst, float v, cudaStream_t s);
+int launch_advance_step(uint64_t* step_dev, cudaStream_t s);
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
                     const SamplerState* st, float* out, cudaStream_t s);
 
@@ -168,7 +170,7 @@ int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* X
 // Fused K11 + K12: dW_hat tile in TMEM -> g = (dw_hat - w_hat dot)/||w||,
 // v <- mu v + g + lambda w, w <- w - lr v, written straight into the W and V shard rows.
 struct SgdArgs {
-  float* W; float* V; const int32_t* idx; const float* inv_norm; const float* dotw; float lr, mu, lambda;
+  float* W; float* V; const int32_t* idx; const float* inv_norm; const float* dotw; const float* lr; float mu, lambda;
 };
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& a, cudaStream_t s);

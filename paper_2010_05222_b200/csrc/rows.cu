@@ -342,8 +342,9 @@ __global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, co
 template <bool UPDATE>
 __global__ void k_sgd(int64_t k_pad, int d, float* __restrict__ W, float* __restrict__ V, const float* __restrict__ dWh,
                       const int32_t* __restrict__ idx, const float* __restrict__ inv_norm, const SamplerState* st,
-                      float lr, float mu, float lambda, float* __restrict__ out) {
+                      const float* __restrict__ lr_dev, float mu, float lambda, float* __restrict__ out) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const float lr = UPDATE ? *lr_dev : 0.f;
   const int lane = threadIdx.x & 31;
   if (p >= st->k) return;
   const int64_t j = idx[p];
@@ -471,17 +472,32 @@ int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_loc
 }
 
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
-               const SamplerState* st, float lr, float mu, float lambda, cudaStream_t s) {
+               const SamplerState* st, const float* lr_dev, float mu, float lambda, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
-  k_sgd<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, dWh, idx, inv_norm, st, lr, mu, lambda, nullptr);
+  k_sgd<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, dWh, idx, inv_norm, st, lr_dev, mu, lambda, nullptr);
+  return 1;
+}
+
+namespace {
+__global__ void k_set_f32(float* dst, float v) { *dst = v; }
+__global__ void k_add_u64(uint64_t* dst, uint64_t v) { *dst += v; }
+}  // namespace
+
+int launch_set_scalar(float* dst, float v, cudaStream_t s) {
+  k_set_f32<<<1, 1, 0, s>>>(dst, v);
+  return 1;
+}
+
+int launch_advance_step(uint64_t* step_dev, cudaStream_t s) {
+  k_add_u64<<<1, 1, 0, s>>>(step_dev, 1);
   return 1;
 }
 
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
                     const SamplerState* st, float* out, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
-  k_sgd<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, const_cast<float*>(W), nullptr, dWh, idx, inv_norm, st, 0.f, 0.f,
-                                    0.f, out);
+  k_sgd<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, const_cast<float*>(W), nullptr, dWh, idx, inv_norm, st, nullptr,
+                                    0.f, 0.f, out);
   return 1;
 }
 

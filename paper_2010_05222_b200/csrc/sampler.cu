@@ -32,9 +32,11 @@ __device__ __forceinline__ bool is_pos(const uint32_t* bits, int64_t j) {
 }
 
 // Pass 1: compute and store every key, histogram of the top 11 bits over non-positive classes.
-__global__ void __launch_bounds__(kThreads) k_keys_hist(int64_t a, int64_t C_local, uint64_t seed, uint32_t step,
+__global__ void __launch_bounds__(kThreads) k_keys_hist(int64_t a, int64_t C_local, uint64_t seed,
+                                                        const uint64_t* __restrict__ step_dev,
                                                         const uint32_t* __restrict__ bits, uint32_t* __restrict__ keys,
                                                         int* __restrict__ hist) {
+  const uint32_t step = (uint32_t)*step_dev;   // device-resident step counter (CUDA-graph replayable)
   __shared__ int sh[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
   __syncthreads();
@@ -267,7 +269,7 @@ __global__ void k_tcol(const int64_t* __restrict__ Y, int M, int64_t a, int64_t 
 
 }  // namespace
 
-int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, uint32_t step, uint32_t* bits, uint32_t* keys,
+int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint64_t* step, uint32_t* bits, uint32_t* keys,
                    int* hist, int* tile_cnt, SamplerState* st, int32_t* idx, int32_t* tcol, int* err,
                    cudaStream_t s) {
   const int64_t nwords = (sz.C_local + 31) / 32;

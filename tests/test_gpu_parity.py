@@ -329,3 +329,35 @@ def test_device_errors_are_reported():
         layer.step(0.1)
     assert e.value.status == 2
     layer.close()
+
+
+def test_cuda_graph_replay_matches_eager():
+    """pfc_train_step on a capturable stream is captured once and replayed as a CUDA graph (device-side step
+    counter and learning rate); results must match the eager launches on the legacy stream."""
+    C, d, B = 30000, 512, 64
+    eager = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
+    graph = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
+    ys = [synth.make_labels(3, i, 1, B, C)[0] for i in range(4)]
+    xs = [synth.make_features(3, i, 1, B, d)[0] for i in range(4)]
+    x = torch.empty(B, d, device="cuda")
+    y = torch.empty(B, dtype=torch.int64, device="cuda")
+    gx_e, gx_g = torch.empty_like(x), torch.empty_like(x)
+    le, lg = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+    side = torch.cuda.Stream()
+    for i in range(4):
+        x.copy_(torch.from_numpy(xs[i]))
+        y.copy_(torch.from_numpy(ys[i]))
+        torch.cuda.synchronize()
+        eager.train_step(x, y, gx_e, le, lr=0.05 * (i + 1))
+        with torch.cuda.stream(side):
+            graph.train_step(x, y, gx_g, lg, lr=0.05 * (i + 1), stream=side)
+        torch.cuda.synchronize()
+        assert abs(le.item() - lg.item()) <= 1e-6 * abs(le.item())
+        assert maxrel(gx_g.cpu().numpy(), gx_e.cpu().numpy()) <= 1e-6
+        assert np.array_equal(eager.sampled(), graph.sampled())
+    We, Ve = eager.params()
+    Wg, Vg = graph.params()
+    assert maxrel(Vg.cpu().numpy(), Ve.cpu().numpy()) <= 1e-5
+    assert eager.step_count == graph.step_count == 4
+    eager.close()
+    graph.close()
