@@ -56,6 +56,15 @@ typedef enum { PFC_FP32 = 0, PFC_BF16 = 1 } pfc_precision;
  *   per-rank solo timing of the scaling study. pfc_forward_backward rejects such a context when world_size > 1. */
 typedef enum { PFC_COMM_NCCL = 0, PFC_COMM_LOOPBACK = 1 } pfc_comm_mode;
 
+/* Which classes a shard samples (R1, R23, R24).
+ * PFC_SAMPLE_PPRN       north_star rule: every positive + negatives up to k_i = max(ceil(r C_local), |P_i|).
+ * PFC_SAMPLE_PPRN_PAPER the paper's step 2: |P_i| positives + round((C_local - |P_i|) r)
+ *                       negatives (round half up); k_i differs between ranks.
+ * PFC_SAMPLE_RANDOM     fully random (the Fig.3 baseline): ceil(r C_local) classes of the whole
+ *                       shard, labels ignored; a row whose positive is not sampled keeps Eq.9's denominator over the
+ *                       sampled set and gets no positive pull. */
+typedef enum { PFC_SAMPLE_PPRN = 0, PFC_SAMPLE_PPRN_PAPER = 1, PFC_SAMPLE_RANDOM = 2 } pfc_sample_mode;
+
 typedef struct {
   int64_t num_classes;   /* C >= world_size      */
   int32_t dim;           /* d, multiple of 128 in [128, 1024] (512 in the paper)      */
@@ -75,6 +84,7 @@ typedef struct {
                                  caller (e.g. over torch.distributed); required iff world_size > 1 and
                                  comm_mode == PFC_COMM_NCCL                                               */
   int32_t comm_mode;     /* pfc_comm_mode                                                                */
+  int32_t sample_mode;   /* pfc_sample_mode                                                              */
 } pfc_config;
 
 typedef struct pfc_ctx pfc_ctx;
@@ -176,6 +186,10 @@ pfc_status pfc_get_sampled_grad(pfc_ctx* ctx, float* dW_host, int64_t capacity_r
 /* Per-row log-sum-exp over the global sampled set (M floats) of the last forward_backward. */
 pfc_status pfc_get_lse(pfc_ctx* ctx, float* lse_host, int64_t capacity);
 
+/* Loss (Eq.5) and CA_pcc (Eq.7: mean cos between each feature and its own class centre) of the
+ * last forward_backward / train_step, synchronising. Either pointer may be NULL. */
+pfc_status pfc_get_metrics(pfc_ctx* ctx, float* loss_host, float* ca_pcc_host);
+
 /* Step counter (number of forward_backward calls since init / set). */
 pfc_status pfc_get_step(const pfc_ctx* ctx, uint64_t* step);
 pfc_status pfc_set_step(pfc_ctx* ctx, uint64_t step);
@@ -183,13 +197,14 @@ pfc_status pfc_set_step(pfc_ctx* ctx, uint64_t step);
 /* Synchronises the context's last stream and returns the sticky device error (PFC_OK if none). */
 pfc_status pfc_check(pfc_ctx* ctx);
 
-/* Standalone PPRN sampler (K2-K4) of shard `rank` of `world_size` (no context): labels_dev [M] int64 global
- * labels of the global batch (device), idx_dev receives the k_i sampled global ids ascending (device, room for
- * max(ceil(r C_local), min(M, C_local)) entries), *k_out = k_i (host; synchronises `stream`).
+/* Standalone sampler (K2-K4) of shard `rank` of `world_size` (no context), rule `sample_mode` (pfc_sample_mode):
+ * labels_dev [M] int64 global labels of the global batch (device), idx_dev receives the k_i sampled global ids
+ * ascending (device, room for min(C_local, ceil(r C_local) + 1 + min(M, C_local)) entries), *k_out = k_i (host;
+ * synchronises `stream`).
  * Same arithmetic as inside pfc_forward_backward with the given `step`. */
 pfc_status pfc_sample_shard(int64_t num_classes, int32_t world_size, int32_t rank, double sample_rate, uint64_t seed,
-                            uint64_t step, const int64_t* labels_dev, int32_t M, int64_t* idx_dev, int64_t* k_out,
-                            void* stream);
+                            uint64_t step, const int64_t* labels_dev, int32_t M, int32_t sample_mode, int64_t* idx_dev,
+                            int64_t* k_out, void* stream);
 
 /* ------------------------------------------------------------------------------------------------------
  * Per-kernel timing (CUDA events recorded on the launching stream between the kernels of the step)

@@ -6,7 +6,7 @@ used only to check the CUDA path. Only tests/, __graft_entry__.smoke() and bench
 """
 from .philox import philox4x32_10, class_key  # noqa: F401
 from .pfc import (  # noqa: F401
-    OracleConfig, MARGIN_NONE, MARGIN_ARCFACE, MARGIN_COSFACE,
+    OracleConfig, MARGIN_NONE, MARGIN_ARCFACE, MARGIN_COSFACE, SAMPLE_PPRN, SAMPLE_PPRN_PAPER, SAMPLE_RANDOM, paper_budget,
     shard_range, sample_budget, positives, sample_shard, normalize_rows, margin_phi, margin_dphi,
     forward_backward, sgd_momentum_rows, spot_rows, spot_cols,
 )

@@ -32,6 +32,13 @@ import numpy as np
 from .philox import class_key
 
 MARGIN_NONE, MARGIN_ARCFACE, MARGIN_COSFACE = 0, 1, 2
+# Sampling rules (R1, R23, R24):
+#   SAMPLE_PPRN        north_star: k_i = max(ceil(r C_local), |P_i|), positives always kept
+#   SAMPLE_PPRN_PAPER  the paper's literal step 2: s_i = (|w_i| - |w_i^p|) r negatives, rounded
+#                      half up; k_i = |P_i| + s_i
+#   SAMPLE_RANDOM      fully random (the Fig.3 baseline): ceil(r C_local) classes drawn from the
+#                      whole shard ignoring the labels; positives may be missing
+SAMPLE_PPRN, SAMPLE_PPRN_PAPER, SAMPLE_RANDOM = 0, 1, 2
 NORM_EPS = 1e-12          # R8: divide by max(||v||, 1e-12)
 ARC_DERIV_EPS = 1e-6      # R10: guard of the ArcFace derivative at cos -> +-1
 
@@ -49,6 +56,7 @@ class OracleConfig:
     momentum: float = 0.9     # mu (R15)
     weight_decay: float = 0.0 # lambda (R15, explicit)
     seed: int = 0
+    sample_mode: int = SAMPLE_PPRN
 
 
 # ----------------------------------------------------------------------------------------------
@@ -76,15 +84,30 @@ def positives(Y, a, C_local):
     return np.unique(Y[(Y >= a) & (Y < a + C_local)])
 
 
-def sample_shard(Y, a, C_local, r, seed, step):
+def paper_budget(r, C_local, npos):
+    """The paper's step 2: s_i = (|w_i| - |w_i^p|) * r negatives; the product is rounded half up
+    (floor(x + 0.5) of the IEEE double product) and clamped to [0, |w_i| - |w_i^p|] (R23)."""
+    n = int(math.floor(float(C_local - npos) * float(r) + 0.5))
+    return min(max(n, 0), C_local - npos)
+
+
+def sample_shard(Y, a, C_local, r, seed, step, mode=SAMPLE_PPRN):
     """Steps 1-3 of the distributed approximation on one shard.
 
     k_i = max(ceil(r C_local), |P_i|) (R1); n_i = k_i - |P_i| negatives are "randomly sampled" from
     w_i - w_i^p (step 3). R2/R3: the n_i negatives with the smallest (h_j, j), h_j = Philox key of the
     global class id j. R4: the sampled set is returned in ascending global id order.
-    Returns (idx int64 ascending global ids, number of positives)."""
+    mode SAMPLE_PPRN_PAPER: n_i = paper_budget (R23). mode SAMPLE_RANDOM: no positives are kept; the
+    ceil(r C_local) classes with the smallest (h_j, j) over the whole shard (R24).
+    Returns (idx int64 ascending global ids, number of positives kept)."""
     P = positives(Y, a, C_local)
-    k_i = max(sample_budget(r, C_local), len(P))
+    if mode == SAMPLE_RANDOM:
+        P = P[:0]
+        k_i = sample_budget(r, C_local)
+    elif mode == SAMPLE_PPRN_PAPER:
+        k_i = len(P) + paper_budget(r, C_local, len(P))
+    else:
+        k_i = max(sample_budget(r, C_local), len(P))
     n_i = k_i - len(P)
     U = np.setdiff1d(np.arange(a, a + C_local, dtype=np.int64), P)     # w_i - w_i^p
     h = class_key(U, seed, step)
@@ -155,7 +178,7 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     idx, kk, npos = [], [], []
     for i in range(k):
         a, Cl = shard_range(C, k, i)
-        ii, npi = sample_shard(Y, a, Cl, cfg.sample_rate, cfg.seed, step)
+        ii, npi = sample_shard(Y, a, Cl, cfg.sample_rate, cfg.seed, step, cfg.sample_mode)
         idx.append(ii); kk.append(len(ii)); npos.append(npi)
     S = np.concatenate(idx)                                          # global ids of the sampled set
     Wraw = np.asarray(w_rows(S), dtype=np.float64).reshape(len(S), d)
@@ -164,27 +187,34 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     # Alg.1 L3 (sampled): cosines, then the margin at each row's positive column (R11).
     cos = Xh @ Wh.T                                                  # M x |S|
     col_of = {int(g): t for t, g in enumerate(S)}
-    tcol = np.array([col_of[int(y)] for y in Y], dtype=np.int64)     # positives always sampled (PPRN)
+    tcol = np.array([col_of.get(int(y), -1) for y in Y], dtype=np.int64)   # -1: positive not sampled (R24)
     rows = np.arange(M)
-    ct = cos[rows, tcol]
+    hit = tcol >= 0
+    # cos(theta) between each row and its own class centre (sampled or not): Eq.7's CA_pcc and z_t
+    Wy, _ = normalize_rows(np.asarray(w_rows(Y), dtype=np.float64).reshape(M, d))
+    ct = np.sum(Xh * Wy, axis=1)
+    zt = s * margin_phi(ct, mt, m)
     Z = s * cos
-    Z[rows, tcol] = s * margin_phi(ct, mt, m)
+    Z[rows[hit], tcol[hit]] = zt[hit]
 
     # Alg.1 L5-8: den_i, den = allreduce(den_i), prob = e^logits / den; R12: shift by the global row max.
     zmax = np.max(Z, axis=1)
     den = np.sum(np.exp(Z - zmax[:, None]), axis=1)
     lse = zmax + np.log(den)
     prob = np.exp(Z - lse[:, None])
-    # Eq.5 (R13: mean over the global batch M = N k).
-    loss = float(np.mean(lse - Z[rows, tcol]))
+    # Eq.5 (R13: mean over the global batch M = N k). A row whose positive is not in S (fully random, R24)
+    # keeps Eq.9's denominator over S and its own positive logit as numerator.
+    loss = float(np.mean(lse - zt))
+    ca_pcc = float(np.mean(ct))                                      # Eq.7
 
     # Alg.1 L9: grad logits = prob - onehot, times dL/dlogits scale 1/M, chained through
-    # z = s * phi(c) at the target and z = s * c elsewhere.
+    # z = s * phi(c) at the target and z = s * c elsewhere. R24: no onehot term (no positive pull) when the
+    # positive is not sampled.
     onehot = np.zeros_like(prob)
-    onehot[rows, tcol] = 1.0
+    onehot[rows[hit], tcol[hit]] = 1.0
     G = (prob - onehot) / M                                          # dL/dZ
     Gc = s * G                                                       # dL/dcos, non-target columns
-    Gc[rows, tcol] *= margin_dphi(ct, mt, m)
+    Gc[rows[hit], tcol[hit]] *= margin_dphi(ct[hit], mt, m)
 
     # Alg.1 L10: grad w = X^T grad logits ; L12: grad X = allreduce(grad logits w^T) (sum over ranks is
     # the sum over the concatenated sampled columns); R14: analytic backprop through both l2 norms.
@@ -194,7 +224,7 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     gw = (dWh - Wh * np.sum(Wh * dWh, axis=1, keepdims=True)) / np.maximum(wnorm, NORM_EPS)[:, None]
 
     out = {
-        "loss": loss,
+        "loss": loss, "ca_pcc": ca_pcc,
         "grad_x": [gx[i * B:(i + 1) * B] for i in range(k)],         # Alg.1 L13: get_submatrix(i, grad X)
         "idx": idx, "k": kk, "num_pos": npos,
         "dW": [], "lse": lse, "target_cos": ct, "tcol": tcol,

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_HERE, "_lib", "libpfc.so")
 MARGINS = {"none": 0, "arcface": 1, "cosface": 2}
 PRECISIONS = {"fp32": 0, "bf16": 1}
 COMM_MODES = {"nccl": 0, "loopback": 1}
+SAMPLE_MODES = {"pprn": 0, "pprn_paper": 1, "random": 2}
 STATUS = {0: "PFC_OK", 1: "PFC_ERR_CONFIG", 2: "PFC_ERR_CONTRACT", 3: "PFC_ERR_DATA", 4: "PFC_ERR_DEGENERATE",
           5: "PFC_ERR_NUMERIC", 6: "PFC_ERR_CUDA", 7: "PFC_ERR_NCCL", 8: "PFC_ERR_OOM"}
 
@@ -31,7 +32,7 @@ EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pf
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
            "pfc_launch_count", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
            "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section", "pfc_train_step", "pfc_train_step_host",
-           "pfc_group_train_step"]
+           "pfc_group_train_step", "pfc_get_metrics"]
 PROF_SECTIONS = 10
 
 
@@ -47,7 +48,7 @@ class _Config(ctypes.Structure):
                 ("margin", ctypes.c_float), ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("precision", ctypes.c_int32), ("seed", ctypes.c_uint64), ("rank", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("comm_mode", ctypes.c_int32)]
+                ("comm_mode", ctypes.c_int32), ("sample_mode", ctypes.c_int32)]
 
 
 _lib = None
@@ -84,6 +85,7 @@ def load_library(path=LIB_PATH):
         "pfc_launch_count": (I64, [VP]),
         "pfc_version": (ctypes.c_char_p, []),
         "pfc_train_step": (st, [VP, VP, VP, VP, VP, F, VP]),
+        "pfc_get_metrics": (st, [VP, P(F), P(F)]),
         "pfc_train_step_host": (st, [VP, VP, VP, VP, VP, F, VP]),
         "pfc_group_train_step": (st, [P(VP), ctypes.c_int32, P(VP), P(VP), P(VP), VP, F, VP]),
         "pfc_profile_enable": (st, [VP, ctypes.c_int32]),
@@ -91,7 +93,7 @@ def load_library(path=LIB_PATH):
         "pfc_profile_section": (ctypes.c_char_p, [ctypes.c_int32]),
         "pfc_group_forward_backward": (st, [P(VP), ctypes.c_int32, P(VP), P(VP), P(VP), VP, VP]),
         "pfc_sample_shard": (st, [I64, ctypes.c_int32, ctypes.c_int32, ctypes.c_double, U64, U64, VP, ctypes.c_int32,
-                                  VP, P(I64), VP]),
+                                  ctypes.c_int32, VP, P(I64), VP]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -127,7 +129,7 @@ class PartialFC:
 
     def __init__(self, num_classes, dim, batch, sample_rate=0.1, scale=64.0, margin_type="arcface", margin=0.5,
                  momentum=0.9, weight_decay=0.0, precision="bf16", seed=0, rank=0, world_size=1, device=0,
-                 nccl_unique_id=None, comm_mode="nccl"):
+                 nccl_unique_id=None, comm_mode="nccl", sample_mode="pprn"):
         self._lib = load_library()
         self.rank, self.world_size, self.device = rank, world_size, device
         self.dim, self.batch, self.num_classes = dim, batch, num_classes
@@ -137,7 +139,8 @@ class PartialFC:
                       float(momentum), float(weight_decay),
                       PRECISIONS[precision] if isinstance(precision, str) else int(precision), int(seed), rank,
                       world_size, device, ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf else None,
-                      COMM_MODES[comm_mode] if isinstance(comm_mode, str) else int(comm_mode))
+                      COMM_MODES[comm_mode] if isinstance(comm_mode, str) else int(comm_mode),
+                      SAMPLE_MODES[sample_mode] if isinstance(sample_mode, str) else int(sample_mode))
         h = ctypes.c_void_p()
         s = self._lib.pfc_init(ctypes.byref(cfg), ctypes.byref(h))
         if s:
@@ -237,6 +240,12 @@ class PartialFC:
         self._check(self._lib.pfc_get_sampled_grad(self._h, out.ctypes.data_as(ctypes.c_void_p), k.value))
         return out
 
+    def metrics(self):
+        """(loss, CA_pcc) of the last step (Eq.5, Eq.7); synchronises."""
+        L, ca = ctypes.c_float(), ctypes.c_float()
+        self._check(self._lib.pfc_get_metrics(self._h, ctypes.byref(L), ctypes.byref(ca)))
+        return L.value, ca.value
+
     def lse(self):
         import numpy as np
         out = np.empty(self.global_batch, dtype=np.float32)
@@ -295,19 +304,21 @@ def group_forward_backward(ranks, xs, labels, grad_xs, loss=None, stream=None, l
         raise PfcError(s, msg)
 
 
-def sample_shard(num_classes, world_size, rank, sample_rate, seed, step, labels, stream=None):
-    """Standalone PPRN sampler of one shard on the GPU: labels = global-batch int64 CUDA tensor.
+def sample_shard(num_classes, world_size, rank, sample_rate, seed, step, labels, stream=None, sample_mode="pprn"):
+    """Standalone sampler of one shard on the GPU: labels = global-batch int64 CUDA tensor.
     Returns the sampled global ids (ascending) as an int64 CUDA tensor."""
     import torch
     lib = load_library()
     base, extra = divmod(num_classes, world_size)
     C_local = base + (1 if rank < extra else 0)
     import math
-    k_max = max(int(math.ceil(float(sample_rate) * float(C_local))), min(labels.numel(), C_local))
+    k_max = min(C_local, int(math.ceil(float(sample_rate) * float(C_local))) + 1 + min(labels.numel(), C_local))
     out = torch.empty(max(k_max, 1), dtype=torch.int64, device=labels.device)
     k = ctypes.c_int64()
     s = lib.pfc_sample_shard(num_classes, world_size, rank, float(sample_rate), int(seed), int(step),
-                             _ptr(labels), labels.numel(), _ptr(out), ctypes.byref(k), _stream_ptr(stream))
+                             _ptr(labels), labels.numel(),
+                             SAMPLE_MODES[sample_mode] if isinstance(sample_mode, str) else int(sample_mode),
+                             _ptr(out), ctypes.byref(k), _stream_ptr(stream))
     if s:
         raise PfcError(s, lib.pfc_last_error(None).decode())
     return out[:k.value]

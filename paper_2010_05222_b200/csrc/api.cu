@@ -67,6 +67,7 @@ struct pfc_ctx {
   float* red = nullptr;        // M + 1
   float* lse = nullptr;        // M
   float* gt = nullptr;         // M, p_t - 1 per row
+  float* metrics = nullptr;    // {loss, CA_pcc} of the last step
   float* loss_dev = nullptr;   // 1 (scratch when the caller passes NULL)
   void* G = nullptr;           // M x k_pad (bf16 or fp32)
   // gradients
@@ -167,6 +168,8 @@ pfc_status validate(const pfc_config* c) {
   if (c->precision != PFC_FP32 && c->precision != PFC_BF16) return set_err(nullptr, PFC_ERR_CONFIG, "unknown precision");
   if (!(c->momentum >= 0.f && c->momentum < 1.f)) return set_err(nullptr, PFC_ERR_CONFIG, "momentum must be in [0, 1)");
   if (!(c->weight_decay >= 0.f)) return set_err(nullptr, PFC_ERR_CONFIG, "weight_decay must be >= 0");
+  if (c->sample_mode < PFC_SAMPLE_PPRN || c->sample_mode > PFC_SAMPLE_RANDOM)
+    return set_err(nullptr, PFC_ERR_CONFIG, "unknown sample_mode");
   if (c->comm_mode != PFC_COMM_NCCL && c->comm_mode != PFC_COMM_LOOPBACK)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown comm_mode");
   if (c->comm_mode == PFC_COMM_LOOPBACK && c->world_size > kMaxLoopback)
@@ -232,7 +235,14 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   sz.M = k * cfg->batch;
   sz.M_pad = (int)round_up(sz.M, 128);
   sz.budget = (int64_t)std::ceil((double)cfg->sample_rate * (double)sz.C_local);  // R1 (IEEE double)
-  sz.k_max = std::max<int64_t>(sz.budget, std::min<int64_t>(sz.M, sz.C_local));
+  sz.rate = cfg->sample_rate;
+  sz.sample_mode = cfg->sample_mode;
+  if (cfg->sample_mode == PFC_SAMPLE_PPRN_PAPER)   // |P_i| + round((C_local - |P_i|) r) <= budget + min(M, C_local)
+    sz.k_max = std::min<int64_t>(sz.C_local, sz.budget + 1 + std::min<int64_t>(sz.M, sz.C_local));
+  else if (cfg->sample_mode == PFC_SAMPLE_RANDOM)
+    sz.k_max = sz.budget;
+  else
+    sz.k_max = std::max<int64_t>(sz.budget, std::min<int64_t>(sz.M, sz.C_local));
   sz.k_pad = round_up(sz.k_max, kKPad);
   sz.ltile = c->use_tc ? 128 : 64;
   sz.n_ltiles = (int)(sz.k_pad / sz.ltile);
@@ -275,7 +285,8 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->gmax, M * 4);
   ALLOC(c->rowsum, M * 4);
   ALLOC(c->zt, M * 4);
-  ALLOC(c->red, 2 * M * 4);
+  ALLOC(c->red, (3 * M + 1) * 4);
+  ALLOC(c->metrics, 16);
   ALLOC(c->gt, M * 4);
   ALLOC(c->lse, M * 4);
   ALLOC(c->loss_dev, 16);
@@ -387,7 +398,7 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
                       c->tcol, c->err_dev, s);
   mark(c, 2, s);
   n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
-  n += launch_target_cos(sz, c->X32, c->W, c->idx, c->tcol, c->inv_norm, c->ct, s);
+  n += launch_target_cos(sz, c->X32, c->W, c->Y, c->ct, s);
   mark(c, 3, s);
   if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
@@ -396,20 +407,20 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
     n += launch_logits_simt(sz, bf, bf ? (const void*)c->Xb : (const void*)c->X32, c->Ws, c->tcol, c->ct, c->st, c->mp,
                             c->cosv, c->partials, s);
   mark(c, 4, s);
-  n += launch_row_combine(sz, c->partials, c->tcol, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, s);
+  n += launch_row_combine(sz, c->partials, c->Y, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, s);
   c->launches += n;
 }
 
 // after all-reduce MAX: red[n] = l_n e^{m_n - gm_n} (non-target columns), red[M + n] = local z_t
 void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
-  c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->red, s);
+  c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->tcol, c->Y, c->ct, c->red, s);
 }
 
 // after all-reduce SUM: LSE, loss, K8 (prob - onehot), K9 dX_hat partial
 void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
-  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->err_dev, s);
+  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, s);
   mark(c, 5, s);
   n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
                            fused && c->use_tc ? c->dotw : nullptr, s);
@@ -491,7 +502,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     gmax = c->gmax;
   }
   phase_c(c, gmax, s);
-  if (multi) nccl(ncclAllReduce(c->red, c->red, 2 * sz.M, ncclFloat, ncclSum, c->comm, s));
+  if (multi) nccl(ncclAllReduce(c->red, c->red, 3 * sz.M + 1, ncclFloat, ncclSum, c->comm, s));
   phase_d(c, gmax, loss_out, fused, s);
   mark(c, 7, s);
   const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
@@ -605,7 +616,7 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   c0->launches += launch_group_reduce(sz.M, src, 0, dst, n, n, 1, s);
   for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
   for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->red; dst.p[r] = ctxs[r]->red; }
-  c0->launches += launch_group_reduce(2 * sz.M, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
+  c0->launches += launch_group_reduce(3 * sz.M + 1, src, 0, dst, n, n, 0, s);  // in place: all reads precede writes per element
   for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, fused, s);
   for (int r = 0; r < n; ++r) src.p[r] = ctxs[r]->dXh;
   for (int r = 0; r < n; ++r) {  // reduce-scatter: owner r sums rows [rB, (r+1)B) over ranks
@@ -746,6 +757,17 @@ pfc_status pfc_get_lse(pfc_ctx* c, float* lse_host, int64_t capacity) {
   return PFC_OK;
 }
 
+pfc_status pfc_get_metrics(pfc_ctx* c, float* loss, float* ca_pcc) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  pfc_status r = sync_and_check(c);
+  if (r != PFC_OK) return r;
+  float h[2];
+  CUDA_TRY(c, cudaMemcpy(h, c->metrics, sizeof(h), cudaMemcpyDeviceToHost));
+  if (loss) *loss = h[0];
+  if (ca_pcc) *ca_pcc = h[1];
+  return PFC_OK;
+}
+
 pfc_status pfc_get_step(const pfc_ctx* c, uint64_t* step) {
   if (!c || !step) return set_err(nullptr, PFC_ERR_CONTRACT, "NULL argument");
   *step = c->step;
@@ -799,7 +821,8 @@ pfc_status pfc_profile_read(pfc_ctx* c, double* ms, int64_t* count) {
 }
 
 pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, uint64_t seed, uint64_t step,
-                            const int64_t* labels, int32_t M, int64_t* idx_out, int64_t* k_out, void* stream) {
+                            const int64_t* labels, int32_t M, int32_t sample_mode, int64_t* idx_out, int64_t* k_out,
+                            void* stream) {
   if (!labels || !idx_out || !k_out || M < 1) return set_err(nullptr, PFC_ERR_CONTRACT, "bad arguments");
   if (world < 1 || rank < 0 || rank >= world || C < world || !(r > 0.0 && r <= 1.0))
     return set_err(nullptr, PFC_ERR_CONFIG, "bad shard configuration");
@@ -809,7 +832,9 @@ pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, ui
   sz.C_local = C / world + (rank < C % world ? 1 : 0);
   sz.a = (int64_t)rank * (C / world) + std::min<int64_t>(rank, C % world);
   sz.budget = (int64_t)std::ceil(r * (double)sz.C_local);
-  sz.k_max = std::max<int64_t>(sz.budget, std::min<int64_t>(M, sz.C_local));
+  sz.rate = r;
+  sz.sample_mode = sample_mode;
+  sz.k_max = std::min<int64_t>(sz.C_local, sz.budget + 1 + std::min<int64_t>(M, sz.C_local));
   sz.ntiles_sel = (int)((sz.C_local + kSelTile - 1) / kSelTile);
   uint32_t *bits = nullptr, *keys = nullptr;
   int *hist = nullptr, *tile = nullptr, *err = nullptr;

@@ -99,6 +99,8 @@ struct Sizes {
   int d, B, M, M_pad;      // dim, per-rank batch, global batch, M rounded up to 128
   int rank, world;
   int64_t budget;          // ceil(r C_local)
+  double rate;             // r
+  int sample_mode;         // pfc_sample_mode
   int64_t k_max, k_pad;    // workspace bound and its padding to the tile width
   int ltile;               // columns per logits partial tile (64 SIMT, 128 tcgen05)
   int n_ltiles;            // number of logits column tiles (k_pad / ltile)
@@ -119,14 +121,13 @@ int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, f
 int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s);
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st,
                     void* Ws, float* inv_norm, int* err, cudaStream_t s);
-int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int32_t* idx, const int32_t* tcol,
-                      const float* inv_norm, float* ct, cudaStream_t s);
-int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* tcol, const float* ct,
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, float* ct, cudaStream_t s);
+int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
-                    float* red, cudaStream_t s);
+                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, cudaStream_t s);
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    int* err, cudaStream_t s);
+                    float* metrics, int* err, cudaStream_t s);
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
                         float* dotw /* per-class w_hat . dW_hat, or NULL */, cudaStream_t s);

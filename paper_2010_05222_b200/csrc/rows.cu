@@ -101,26 +101,29 @@ __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, co
 }
 
 // ---------------------------------------------------------------- K5b: one warp per batch row
-__global__ void k_target_cos(int M, int d, const float* __restrict__ X32, const float* __restrict__ W,
-                             const int32_t* __restrict__ idx, const int32_t* __restrict__ tcol,
-                             const float* __restrict__ inv_norm, float* __restrict__ ct) {
+// c_t[n] = x_hat_n . W[y_n] / ||W[y_n]|| in fp32 for every row whose class is on this shard (sampled or not:
+// fully random sampling may leave the positive out, R24); 0 elsewhere. Used for the target logit, CA_pcc (Eq.7)
+// and the ArcFace derivative.
+__global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const float* __restrict__ X32,
+                             const float* __restrict__ W, const int64_t* __restrict__ Y, float* __restrict__ ct) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= M) return;
-  const int p = tcol[n];
-  if (p < 0) { if (lane == 0) ct[n] = 0.f; return; }
+  const int64_t j = Y[n] - a;
+  if (j < 0 || j >= C_local) { if (lane == 0) ct[n] = 0.f; return; }
   const float* xr = X32 + (int64_t)n * d;
-  const float* wr = W + (int64_t)idx[p] * d;
-  float acc = 0.f;
-  for (int c = lane; c < d; c += 32) acc += xr[c] * wr[c];
+  const float* wr = W + j * d;
+  float acc = 0.f, ss = 0.f;
+  for (int c = lane; c < d; c += 32) { const float w = wr[c]; acc += xr[c] * w; ss += w * w; }
   acc = warp_sum(acc);
-  if (lane == 0) ct[n] = acc * inv_norm[p];
+  ss = warp_sum(ss);
+  if (lane == 0) ct[n] = acc / fmaxf(sqrtf(ss), kNormEps);
 }
 
 // ---------------------------------------------------------------- K7: one warp per batch row
-__global__ void k_row_combine(int M, int ntiles, int ltile, const float2* __restrict__ partials,
-                              const int32_t* __restrict__ tcol, const float* __restrict__ ct, const SamplerState* st,
-                              MarginParams mp, float* __restrict__ rowmax, float* __restrict__ rowsum,
-                              float* __restrict__ zt) {
+__global__ void k_row_combine(int M, int ntiles, int ltile, int64_t a, int64_t C_local,
+                              const float2* __restrict__ partials, const int64_t* __restrict__ Y,
+                              const float* __restrict__ ct, const SamplerState* st, MarginParams mp,
+                              float* __restrict__ rowmax, float* __restrict__ rowsum, float* __restrict__ zt) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= M) return;
   const float2* pr = partials + (int64_t)n * ntiles;
@@ -136,34 +139,59 @@ __global__ void k_row_combine(int M, int ntiles, int ltile, const float2* __rest
   if (lane == 0) {
     rowmax[n] = m;
     rowsum[n] = l;
-    zt[n] = tcol[n] >= 0 ? mp.s * margin_phi(mp, ct[n]) : 0.f;
+    const int64_t j = Y[n] - a;
+    zt[n] = (j >= 0 && j < C_local) ? mp.s * margin_phi(mp, ct[n]) : 0.f;   // owner rank of the positive
   }
 }
 
 // The per-tile partials exclude each row's target column (its logit z_t = s phi(c_t) is known exactly
 // from K5b), so that the loss and the target gradient can be formed without cancellation when p_t -> 1:
-//   q_n = sum_{j != t} e^{z_j - z_t},  loss_n = log1p(q_n),  p_t - 1 = -q_n / (1 + q_n).
-// red[n] = l_n e^{m_n - gm_n} (sum over non-target columns relative to the global non-target max);
-// red[M + n] = z_t of row n if its class is on this rank, else 0 (the all-reduce SUM gathers it).
-__global__ void k_prep_sum(int M, const float* __restrict__ rowmax, const float* __restrict__ gmax,
-                           const float* __restrict__ rowsum, const float* __restrict__ zt, float* __restrict__ red) {
-  const int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= M) return;
-  const float rm = rowmax[n];
-  red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
-  red[M + n] = zt[n];
+//   q_n = sum_{j != t} e^{z_j - z_t},  loss_n = log1p(q_n),  p_t - 1 = -q_n / (1 + q_n)          (R22)
+// Layout of the SUM all-reduce buffer (3M + 1 floats):
+//   red[n]      = l_n e^{m_n - gm_n}  (sum over the sampled non-target columns, relative to the global max)
+//   red[M + n]  = z_t of row n on the rank owning its class (0 elsewhere)
+//   red[2M + n] = 1 if the rank sampled row n's class (the sum is 1 iff the positive is in S; R24)
+//   red[3M]     = sum of c_t over the rows whose class is on this rank (CA_pcc numerator, Eq.7)
+__global__ void __launch_bounds__(1024) k_prep_sum(int M, int64_t a, int64_t C_local, const float* __restrict__ rowmax,
+                                                   const float* __restrict__ gmax, const float* __restrict__ rowsum,
+                                                   const float* __restrict__ zt, const int32_t* __restrict__ tcol,
+                                                   const int64_t* __restrict__ Y, const float* __restrict__ ct,
+                                                   float* __restrict__ red) {
+  __shared__ float sh[32];
+  float acc = 0.f;
+  for (int n = threadIdx.x; n < M; n += blockDim.x) {
+    const float rm = rowmax[n];
+    red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
+    red[M + n] = zt[n];
+    red[2 * M + n] = tcol[n] >= 0 ? 1.f : 0.f;
+    const int64_t j = Y[n] - a;
+    if (j >= 0 && j < C_local) acc += ct[n];
+  }
+  acc = warp_sum(acc);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    v = warp_sum(v);
+    if (threadIdx.x == 0) red[3 * M] = v;
+  }
 }
 
-// Global LSE_n, loss (Eq.5 over the global batch, R13) and g_t[n] = p_t - 1 for K8.
+// Global LSE_n, loss (Eq.5 over the global batch, R13), g_t[n] = p_t - 1 for K8, CA_pcc (Eq.7).
 __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restrict__ gmax, const float* __restrict__ red,
                                                    float* __restrict__ lse, float* __restrict__ gt,
-                                                   float* __restrict__ loss_out, int* err) {
+                                                   float* __restrict__ loss_out, float* __restrict__ metrics, int* err) {
   __shared__ float sh[32];
   float acc = 0.f;
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
     const float gm = gmax[n], S = red[n], z = red[M + n];
+    const bool sampled = red[2 * M + n] > 0.5f;
     float L, g, ls;
-    if (!(gm > -INFINITY) || S == 0.f) {          // no negative in the sampled set: p_t = 1
+    if (!sampled) {                               // positive not in S (fully random): Eq.9 over S, no pull
+      ls = (gm > -INFINITY && S > 0.f) ? gm + __logf(S) : -INFINITY;
+      L = ls - z;
+      g = 0.f;
+    } else if (!(gm > -INFINITY) || S == 0.f) {   // no negative in the sampled set: p_t = 1
       ls = z; L = 0.f; g = 0.f;
     } else if (z >= gm) {
       const float q = S * __expf(gm - z);
@@ -187,20 +215,15 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
     float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
     v = warp_sum(v);
     if (threadIdx.x == 0) {
-      float Lm = v / (float)M;
+      const float Lm = v / (float)M;
       if (loss_out) *loss_out = Lm;
+      metrics[0] = Lm;
+      metrics[1] = red[3 * M] / (float)M;
       if (!isfinite(Lm)) atomicOr(err, ERR_NUMERIC);
     }
   }
 }
 
-// ---------------------------------------------------------------- K8: softmax gradient (class-major)
-// cos and G are [k_pad][ldm] (ldm = M rounded up to 128): one warp streams one sampled class j at a time, a
-// lane owning 8 consecutive batch rows (16-byte loads/stores, 512 contiguous bytes per warp). Per-row data
-// (LSE, target column, target gradient) sits in shared memory.
-//   Gc[j][n] = (s/M) e^{z_nj - LSE_n}            j != t_n
-//            = (s/M) (p_t - 1) phi'(c_t)          j == t_n   (cancellation-free p_t - 1, rows.cu finalize)
-// With DOT: dot[j] = sum_n Gc[j][n] c[j][n] = w_hat_j . dW_hat_j (radial term of the fused SGD epilogue).
 template <bool BF16>
 __device__ __forceinline__ void load8(const void* cosv, int64_t base, float (&c)[8]) {
   if (BF16) {
@@ -405,28 +428,27 @@ int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* i
   return 1;
 }
 
-int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int32_t* idx, const int32_t* tcol,
-                      const float* inv_norm, float* ct, cudaStream_t s) {
-  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, X32, W, idx, tcol, inv_norm, ct);
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, float* ct, cudaStream_t s) {
+  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, ct);
   return 1;
 }
 
-int launch_row_combine(const Sizes& sz, const float2* partials, const int32_t* tcol, const float* ct,
+int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s) {
-  k_row_combine<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, partials, tcol, ct, st, mp, rowmax,
-                                                        rowsum, zt);
+  k_row_combine<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct,
+                                                        st, mp, rowmax, rowsum, zt);
   return 1;
 }
 
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
-                    float* red, cudaStream_t s) {
-  k_prep_sum<<<(sz.M + 255) / 256, 256, 0, s>>>(sz.M, rowmax, gmax, rowsum, zt, red);
+                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, cudaStream_t s) {
+  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, sz.a, sz.C_local, rowmax, gmax, rowsum, zt, tcol, Y, ct, red);
   return 1;
 }
 
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    int* err, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, err);
+                    float* metrics, int* err, cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err);
   return 1;
 }
 

@@ -16,9 +16,9 @@ namespace {
 constexpr int kThreads = 256;
 
 __global__ void k_mark_positives(const int64_t* __restrict__ Y, int M, int64_t a, int64_t C_local,
-                                 uint32_t* __restrict__ bits, SamplerState* st, int* err) {
+                                 uint32_t* __restrict__ bits, SamplerState* st, int mode) {
   int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= M) return;
+  if (n >= M || mode == PFC_SAMPLE_RANDOM) return;   // fully random: labels ignored (R24)
   int64_t y = Y[n] - a;
   if (y >= 0 && y < C_local) {
     uint32_t mask = 1u << (y & 31);
@@ -72,12 +72,23 @@ __global__ void __launch_bounds__(kThreads) k_hist_pass(int64_t C_local, const u
 // Single block: locate the bucket holding the `remaining`-th smallest key of this pass.
 // pass 0 also computes k_i and n_i from |P_i| (R1).
 __global__ void __launch_bounds__(1024) k_select_bucket(const int* __restrict__ hist, int nbins, int pass,
-                                                        int64_t budget, SamplerState* st) {
+                                                        int64_t budget, int64_t C_local, double rate, int mode,
+                                                        SamplerState* st) {
   __shared__ int scan[1024];
   __shared__ int found;
   if (pass == 0) {
     if (threadIdx.x == 0) {
-      int k = (int)max(budget, (int64_t)st->npos);
+      int k;
+      if (mode == PFC_SAMPLE_PPRN_PAPER) {   // R23: |P_i| + round_half_up((C_local - |P_i|) r)
+        const int64_t rest = C_local - st->npos;
+        int64_t n = (int64_t)floor((double)rest * rate + 0.5);
+        n = n < 0 ? 0 : (n > rest ? rest : n);
+        k = st->npos + (int)n;
+      } else if (mode == PFC_SAMPLE_RANDOM) {
+        k = (int)budget;
+      } else {
+        k = (int)max(budget, (int64_t)st->npos);   // R1
+      }
       st->k = k;
       st->n_neg = k - st->npos;
       st->none = (st->n_neg == 0);
@@ -276,14 +287,14 @@ int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint6
   cudaMemsetAsync(bits, 0, nwords * sizeof(uint32_t), s);
   cudaMemsetAsync(hist, 0, (2048 + 2048 + 1024) * sizeof(int), s);
   cudaMemsetAsync(st, 0, sizeof(SamplerState), s);
-  k_mark_positives<<<(sz.M + 255) / 256, 256, 0, s>>>(Y, sz.M, sz.a, sz.C_local, bits, st, err);
+  k_mark_positives<<<(sz.M + 255) / 256, 256, 0, s>>>(Y, sz.M, sz.a, sz.C_local, bits, st, sz.sample_mode);
   int grid = (int)std::min<int64_t>((sz.C_local + kThreads - 1) / kThreads, 148 * 8);
   k_keys_hist<<<grid, kThreads, 0, s>>>(sz.a, sz.C_local, seed, step, bits, keys, hist);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist, 2048, 0, sz.budget, st);
+  k_select_bucket<<<1, 1024, 0, s>>>(hist, 2048, 0, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
   k_hist_pass<<<grid, kThreads, 0, s>>>(sz.C_local, bits, keys, st, 21, 10, 0x7FFu, hist + 2048);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist + 2048, 2048, 1, sz.budget, st);
+  k_select_bucket<<<1, 1024, 0, s>>>(hist + 2048, 2048, 1, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
   k_hist_pass<<<grid, kThreads, 0, s>>>(sz.C_local, bits, keys, st, 10, 0, 0x3FFu, hist + 4096);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist + 4096, 1024, 2, sz.budget, st);
+  k_select_bucket<<<1, 1024, 0, s>>>(hist + 4096, 1024, 2, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
   k_tile_counts<<<sz.ntiles_sel, kThreads, 0, s>>>(sz.C_local, bits, keys, st, tile_cnt, sz.ntiles_sel);
   k_tile_scan<<<1, 1024, 0, s>>>(tile_cnt, sz.ntiles_sel, st, err);
   k_tile_write<<<sz.ntiles_sel, kThreads, 0, s>>>(sz.C_local, bits, keys, st, tile_cnt, sz.ntiles_sel, idx);

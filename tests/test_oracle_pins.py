@@ -457,3 +457,75 @@ def test_spot_cols_agree_with_full_forward_backward():
     full = np.concatenate(out["dW"])
     assert np.allclose(lse, out["lse"], rtol=1e-13)
     assert np.allclose(dW, full[cols], rtol=1e-10, atol=1e-16)
+
+
+# ---------------------------------------------------------------- method variants
+def test_paper_budget_spec_examples():
+    # SPEC.md:275-277 (round half up of the paper's product)
+    assert oracle.paper_budget(0.1, 1000, 100) == 90
+    assert oracle.paper_budget(0.1, 125000, 512) == 12449          # round(12448.8)
+    assert oracle.paper_budget(1.0, 500, 37) == 463                 # full complement
+    # k = 1, C = 10, labels {2, 5}, r = 0.5 -> 2 positives + round(8 * 0.5) = 4 negatives
+    idx, npos = oracle.sample_shard(np.array([2, 5]), 0, 10, 0.5, seed=0, step=0, mode=oracle.SAMPLE_PPRN_PAPER)
+    assert npos == 2 and len(idx) == 6 and {2, 5} <= set(idx.tolist())
+
+
+def test_fully_random_ignores_labels_and_misses_positives():
+    # over 1000 trials with C = 100, batch 10, r = 0.1, at least one trial misses a positive
+    missed = 0
+    counts = np.zeros(100)
+    for t in range(1000):
+        Y = np.random.default_rng(t).integers(0, 100, size=10)
+        idx, npos = oracle.sample_shard(Y, 0, 100, 0.1, seed=3, step=t, mode=oracle.SAMPLE_RANDOM)
+        assert npos == 0 and len(idx) == 10
+        counts[idx] += 1
+        missed += not set(Y.tolist()) <= set(idx.tolist())
+    assert missed > 0
+    assert np.all(np.abs(counts / 1000 - 0.1) < 0.05)                # uniform over the whole shard
+
+
+def test_ca_pcc_closed_forms():
+    # SPEC.md ca_pcc: every feature equals its centre -> 1.0; features orthogonal to their centres -> 0.0 (Eq.7)
+    C, d = 4, 8
+    W = np.zeros((C, d)); W[np.arange(C), np.arange(C)] = 1.0
+    cfg = OracleConfig(num_classes=C, dim=d, batch=C, sample_rate=1.0, margin_type=MARGIN_NONE)
+    out = oracle.forward_backward(cfg, [W.copy()], [np.arange(C)], lambda ids: W[np.asarray(ids)])
+    assert out["ca_pcc"] == pytest.approx(1.0, abs=1e-15)
+    X = np.zeros((C, d)); X[np.arange(C), np.arange(C) + 4] = 1.0
+    out = oracle.forward_backward(cfg, [X], [np.arange(C)], lambda ids: W[np.asarray(ids)])
+    assert out["ca_pcc"] == pytest.approx(0.0, abs=1e-15)
+
+
+@pytest.mark.parametrize("mode", [1, 2])
+def test_variants_equal_masked_torch_autograd(mode):
+    """PPRN with the paper's budget and fully random sampling against torch autograd of the dense problem with
+    unsampled logits masked to -inf; for fully random rows whose positive is unsampled the loss is
+    LSE_S - z_t with z_t detached (no positive pull)."""
+    C, d, B, k = 80, 12, 6, 2
+    W = w_rows_np(2, np.arange(C), d)
+    ys = make_labels(8, 0, k, B, C)
+    xs = [x.astype(np.float64) for x in make_features(8, 0, k, B, d)]
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, world_size=k, sample_rate=0.2, scale=16.0,
+                       margin_type=MARGIN_COSFACE, margin=0.4, seed=5, sample_mode=mode)
+    out = oracle.forward_backward(cfg, xs, ys, lambda i: W[np.asarray(i)], step=3)
+    S = np.concatenate(out["idx"])
+    Y = np.concatenate(ys)
+    if mode == 2:
+        assert not set(Y.tolist()) <= set(S.tolist())                 # this seed misses some positives
+    mask = np.zeros(C, dtype=bool); mask[S] = True
+    xt = torch.tensor(np.concatenate(xs), requires_grad=True)
+    Wt = torch.tensor(W, requires_grad=True)
+    cos = torch.nn.functional.normalize(xt, dim=1) @ torch.nn.functional.normalize(Wt, dim=1).T
+    yt = torch.tensor(Y)
+    ct = cos[torch.arange(len(Y)), yt]
+    zt = 16.0 * (ct - 0.4)
+    hit = torch.tensor(mask[Y])
+    logits = 16.0 * cos
+    logits = torch.where(torch.nn.functional.one_hot(yt, C).bool(), zt[:, None].expand(-1, C), logits)
+    logits = logits.masked_fill(~torch.tensor(mask)[None, :], float("-inf"))
+    lse = torch.logsumexp(logits, dim=1)
+    L = torch.mean(lse - torch.where(hit, zt, zt.detach()))
+    L.backward()
+    assert out["loss"] == pytest.approx(L.item(), rel=1e-12)
+    assert np.allclose(np.concatenate(out["grad_x"]), xt.grad.numpy(), rtol=1e-9, atol=1e-15)
+    assert np.allclose(np.concatenate(out["dW"]), Wt.grad.numpy()[S], rtol=1e-9, atol=1e-15)
