@@ -398,7 +398,7 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
                       c->tcol, c->err_dev, s);
   mark(c, 2, s);
   n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
-  n += launch_target_cos(sz, c->X32, c->W, c->Y, c->ct, s);
+  n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tcol, c->ct, s);
   mark(c, 3, s);
   if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,

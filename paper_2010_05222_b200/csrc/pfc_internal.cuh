@@ -20,16 +20,18 @@ constexpr float kArcDerivEps = 1e-6f;  // DESIGN.md R10
 
 // Device-resident state of the sampler for one step.
 struct SamplerState {
-  int npos;        // |P_i|
-  int k;           // k_i = max(ceil(r C_local), |P_i|)
-  int n_neg;       // n_i = k_i - |P_i|
-  int none;        // n_i == 0: no negative selected
-  uint32_t prefix; // radix-select prefix after each pass
-  int remaining;   // rank of the threshold inside the current prefix bucket (1-based)
-  uint32_t T;      // threshold key
-  int t;           // number of tied (key == T) negatives to take, smallest ids first
-  int total;       // number of selected rows written by the compaction (== k)
-  int pad[7];
+  int npos;          // |P_i|
+  int k;             // k_i (R1 / R23 / R24)
+  int n_neg;         // n_i = k_i - |P_i|
+  int none;          // n_i == 0: no negative selected
+  uint32_t prefix1;  // radix select: top 11 bits of the threshold key (pass 1)
+  int rem1;          //   rank of the threshold inside that bucket (1-based)
+  uint32_t prefix2;  //   top 22 bits (pass 2)
+  int rem2;
+  uint32_t T;        // threshold key
+  int t;             // number of tied (key == T) negatives to take, smallest ids first
+  int total;         // number of selected rows written by the compaction (== k)
+  int pad[5];
 };
 
 // Margin parameters used by the epilogues (R9-R11).
@@ -121,7 +123,8 @@ int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, f
 int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s);
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st,
                     void* Ws, float* inv_norm, int* err, cudaStream_t s);
-int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, float* ct, cudaStream_t s);
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
+                      const SamplerState* st, int32_t* tcol, float* ct, cudaStream_t s);
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,

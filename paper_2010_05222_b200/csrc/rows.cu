@@ -104,12 +104,28 @@ __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, co
 // c_t[n] = x_hat_n . W[y_n] / ||W[y_n]|| in fp32 for every row whose class is on this shard (sampled or not:
 // fully random sampling may leave the positive out, R24); 0 elsewhere. Used for the target logit, CA_pcc (Eq.7)
 // and the ArcFace derivative.
+// Also tcol[n] = position of y_n in the sampled set idx (binary search; -1 when not sampled on this rank).
 __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const float* __restrict__ X32,
-                             const float* __restrict__ W, const int64_t* __restrict__ Y, float* __restrict__ ct) {
+                             const float* __restrict__ W, const int64_t* __restrict__ Y,
+                             const int32_t* __restrict__ idx, const SamplerState* st, int32_t* __restrict__ tcol,
+                             float* __restrict__ ct) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= M) return;
   const int64_t j = Y[n] - a;
-  if (j < 0 || j >= C_local) { if (lane == 0) ct[n] = 0.f; return; }
+  if (j < 0 || j >= C_local) {
+    if (lane == 0) { ct[n] = 0.f; tcol[n] = -1; }
+    return;
+  }
+  if (lane == 0) {
+    int lo = 0, hi = st->k - 1, res = -1;
+    while (lo <= hi) {
+      const int mid = (lo + hi) >> 1;
+      const int v = idx[mid];
+      if (v == (int)j) { res = mid; break; }
+      if (v < (int)j) lo = mid + 1; else hi = mid - 1;
+    }
+    tcol[n] = res;
+  }
   const float* xr = X32 + (int64_t)n * d;
   const float* wr = W + j * d;
   float acc = 0.f, ss = 0.f;
@@ -428,8 +444,9 @@ int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* i
   return 1;
 }
 
-int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, float* ct, cudaStream_t s) {
-  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, ct);
+int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
+                      const SamplerState* st, int32_t* tcol, float* ct, cudaStream_t s) {
+  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, idx, st, tcol, ct);
   return 1;
 }
 

@@ -50,138 +50,181 @@ __global__ void __launch_bounds__(kThreads) k_keys_hist(int64_t a, int64_t C_loc
     if (sh[i]) atomicAdd(&hist[i], sh[i]);
 }
 
-// Passes 2 and 3: histogram of the next digit among keys whose higher digits equal the prefix.
-__global__ void __launch_bounds__(kThreads) k_hist_pass(int64_t C_local, const uint32_t* __restrict__ bits,
-                                                        const uint32_t* __restrict__ keys, const SamplerState* st,
-                                                        int hi_shift, int lo_shift, uint32_t lo_mask,
-                                                        int* __restrict__ hist) {
-  __shared__ int sh[2048];
-  if (st->none) return;
-  const uint32_t prefix = st->prefix;
-  for (int i = threadIdx.x; i <= (int)lo_mask; i += blockDim.x) sh[i] = 0;
-  __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t h = keys[j];
-    if ((h >> hi_shift) == prefix && !is_pos(bits, j)) atomicAdd(&sh[(h >> lo_shift) & lo_mask], 1);
-  }
-  __syncthreads();
-  for (int i = threadIdx.x; i <= (int)lo_mask; i += blockDim.x)
-    if (sh[i]) atomicAdd(&hist[i], sh[i]);
-}
-
-// Single block: locate the bucket holding the `remaining`-th smallest key of this pass.
-// pass 0 also computes k_i and n_i from |P_i| (R1).
-__global__ void __launch_bounds__(1024) k_select_bucket(const int* __restrict__ hist, int nbins, int pass,
-                                                        int64_t budget, int64_t C_local, double rate, int mode,
-                                                        SamplerState* st) {
-  __shared__ int scan[1024];
-  __shared__ int found;
-  if (pass == 0) {
-    if (threadIdx.x == 0) {
-      int k;
-      if (mode == PFC_SAMPLE_PPRN_PAPER) {   // R23: |P_i| + round_half_up((C_local - |P_i|) r)
-        const int64_t rest = C_local - st->npos;
-        int64_t n = (int64_t)floor((double)rest * rate + 0.5);
-        n = n < 0 ? 0 : (n > rest ? rest : n);
-        k = st->npos + (int)n;
-      } else if (mode == PFC_SAMPLE_RANDOM) {
-        k = (int)budget;
-      } else {
-        k = (int)max(budget, (int64_t)st->npos);   // R1
-      }
-      st->k = k;
-      st->n_neg = k - st->npos;
-      st->none = (st->n_neg == 0);
-      st->remaining = st->n_neg;
-      st->prefix = 0;
-    }
-    __syncthreads();
-  }
-  if (st->none) return;
-  const int need = st->remaining;
-  // each thread owns a contiguous chunk of bins
-  const int per = (nbins + blockDim.x - 1) / blockDim.x;
+// Locate, with a 256-thread block, the bucket b of `hist` (nbins) holding the `need`-th smallest key:
+// cum(b) < need <= cum(b) + hist[b]. Returns b and need - cum(b) (1-based rank inside the bucket).
+__device__ void block_select(const int* __restrict__ hist, int nbins, int need, int& bucket, int& rem) {
+  __shared__ int wsum[kThreads / 32];
+  __shared__ int res[2];
+  const int per = nbins / kThreads;            // 8 (2048 bins) or 4 (1024 bins)
   const int b0 = threadIdx.x * per;
   int local = 0;
-  for (int b = b0; b < min(nbins, b0 + per); ++b) local += hist[b];
-  scan[threadIdx.x] = local;
-  if (threadIdx.x == 0) found = 0;
-  __syncthreads();
-  for (int off = 1; off < (int)blockDim.x; off <<= 1) {  // inclusive Hillis-Steele scan
-    int v = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
-    __syncthreads();
-    scan[threadIdx.x] += v;
-    __syncthreads();
+  for (int b = 0; b < per; ++b) local += hist[b0 + b];
+  // block exclusive scan of `local`
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  int incl = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
   }
-  int before = scan[threadIdx.x] - local;
-  if (before < need && need <= scan[threadIdx.x]) {
+  if (lane == 31) wsum[w] = incl;
+  __syncthreads();
+  int before = incl - local;
+  for (int i = 0; i < w; ++i) before += wsum[i];
+  if (before < need && need <= before + local) {
     int cum = before;
-    for (int b = b0; b < min(nbins, b0 + per); ++b) {
-      int h = hist[b];
-      if (cum < need && need <= cum + h) {
-        const int bits_of_pass = (pass == 2) ? 10 : 11;
-        st->prefix = (st->prefix << bits_of_pass) | (uint32_t)b;
-        st->remaining = need - cum;
-        found = 1;
-        break;
-      }
+    for (int b = 0; b < per; ++b) {
+      const int h = hist[b0 + b];
+      if (cum < need && need <= cum + h) { res[0] = b0 + b; res[1] = need - cum; break; }
       cum += h;
     }
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (pass == 2) {
-      st->T = st->prefix;
-      st->t = st->remaining;
+  bucket = res[0];
+  rem = res[1];
+}
+
+// k_i and n_i from |P_i| (R1, R23, R24)
+__device__ __forceinline__ int budget_k(int npos, int64_t budget, int64_t C_local, double rate, int mode) {
+  if (mode == PFC_SAMPLE_PPRN_PAPER) {   // R23: |P_i| + round_half_up((C_local - |P_i|) r)
+    const int64_t rest = C_local - npos;
+    int64_t n = (int64_t)floor((double)rest * rate + 0.5);
+    n = n < 0 ? 0 : (n > rest ? rest : n);
+    return npos + (int)n;
+  }
+  if (mode == PFC_SAMPLE_RANDOM) return (int)budget;
+  return (int)max(budget, (int64_t)npos);   // R1
+}
+
+// Pass 2: every block selects the 11-bit bucket of pass 1 from hist0 (block 0 records it), then histograms the
+// next 11 bits of the keys inside it.
+__global__ void __launch_bounds__(kThreads) k_hist_pass2(int64_t C_local, int64_t budget, double rate, int mode,
+                                                         const uint32_t* __restrict__ bits,
+                                                         const uint32_t* __restrict__ keys, const int* __restrict__ hist0,
+                                                         SamplerState* st, int* __restrict__ hist1) {
+  __shared__ int sh[2048];
+  const int npos = st->npos;
+  const int k = budget_k(npos, budget, C_local, rate, mode);
+  const int n_neg = k - npos;
+  if (n_neg == 0) {
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->k = k; st->n_neg = 0; st->none = 1; }
+    return;
+  }
+  int b1, rem1;
+  block_select(hist0, 2048, n_neg, b1, rem1);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->k = k; st->n_neg = n_neg; st->none = 0; st->prefix1 = (uint32_t)b1; st->rem1 = rem1;
+  }
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = keys[j];
+    if ((h >> 21) == (uint32_t)b1 && !is_pos(bits, j)) atomicAdd(&sh[(h >> 10) & 0x7FF], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist1[i], sh[i]);
+}
+
+// Pass 3: select the second digit from hist1, histogram the last 10 bits.
+__global__ void __launch_bounds__(kThreads) k_hist_pass3(int64_t C_local, const uint32_t* __restrict__ bits,
+                                                         const uint32_t* __restrict__ keys, const int* __restrict__ hist1,
+                                                         SamplerState* st, int* __restrict__ hist2) {
+  __shared__ int sh[1024];
+  if (st->none) return;
+  int b2, rem2;
+  block_select(hist1, 2048, st->rem1, b2, rem2);
+  const uint32_t pre = (st->prefix1 << 11) | (uint32_t)b2;
+  if (blockIdx.x == 0 && threadIdx.x == 0) { st->prefix2 = pre; st->rem2 = rem2; }
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = 0;
+  __syncthreads();
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t h = keys[j];
+    if ((h >> 10) == pre && !is_pos(bits, j)) atomicAdd(&sh[h & 0x3FF], 1);
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+    if (sh[i]) atomicAdd(&hist2[i], sh[i]);
+}
+
+// Flags of 4 consecutive classes j0..j0+3 (j0 % 4 == 0): definitely selected (positive, or key < T) and tied
+// (key == T, non-positive).
+__device__ __forceinline__ void flags4(int64_t j0, int64_t C_local, const uint32_t* bits, const uint32_t* keys,
+                                       bool none, uint32_t T, bool (&def)[4], bool (&tie)[4]) {
+  if (j0 + 3 < C_local) {
+    const uint4 h = *reinterpret_cast<const uint4*>(keys + j0);
+    const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+    const uint32_t hh[4] = {h.x, h.y, h.z, h.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const bool p = (pw >> i) & 1u;
+      def[i] = p || (!none && hh[i] < T);
+      tie[i] = !p && !none && hh[i] == T;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t j = j0 + i;
+      def[i] = false; tie[i] = false;
+      if (j < C_local) {
+        const bool p = is_pos(bits, j);
+        const uint32_t h = keys[j];
+        def[i] = p || (!none && h < T);
+        tie[i] = !p && !none && h == T;
+      }
     }
   }
 }
 
-// Block-wide exclusive scan of a 0/1 flag over 256 threads (8 warps); returns the prefix and the total.
-__device__ __forceinline__ int block_flag_scan(bool f, int* warp_tot, int& total) {
+// Block-wide exclusive scan of small per-thread counts (256 threads); returns the prefix, sets the total.
+__device__ __forceinline__ int block_count_scan(int v, int* wsum, int& total) {
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t bal = __ballot_sync(0xffffffffu, f);
-  const int wpre = __popc(bal & ((1u << lane) - 1u));
-  if (lane == 0) warp_tot[w] = __popc(bal);
+  int incl = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int u = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += u;
+  }
+  if (lane == 31) wsum[w] = incl;
   __syncthreads();
-  int pre = 0, tot = 0;
+  int pre = incl - v, tot = 0;
 #pragma unroll
   for (int i = 0; i < kThreads / 32; ++i) {
-    int v = warp_tot[i];
-    pre += (i < w) ? v : 0;
-    tot += v;
+    const int x = wsum[i];
+    pre += i < w ? x : 0;
+    tot += x;
   }
   __syncthreads();
   total = tot;
-  return pre + wpre;
+  return pre;
 }
 
-__device__ __forceinline__ void flags_of(int64_t j, int64_t C_local, const uint32_t* bits, const uint32_t* keys,
-                                         const SamplerState& s, bool& def, bool& tie) {
-  def = false; tie = false;
-  if (j >= C_local) return;
-  if (is_pos(bits, j)) { def = true; return; }
-  if (s.none) return;
-  uint32_t h = keys[j];
-  def = h < s.T;
-  tie = h == s.T;
-}
-
-// K4a: per-tile counts of definitely-selected and tied classes.
+// K4a: select the threshold key T (and t, the number of tied keys to take) from hist2 (block 0 records them),
+// then count definitely-selected and tied classes per 8192-class tile.
 __global__ void __launch_bounds__(kThreads) k_tile_counts(int64_t C_local, const uint32_t* __restrict__ bits,
-                                                          const uint32_t* __restrict__ keys, const SamplerState* st,
-                                                          int* __restrict__ tile_cnt, int ntiles) {
-  const SamplerState s = *st;
+                                                          const uint32_t* __restrict__ keys, const int* __restrict__ hist2,
+                                                          SamplerState* st, int* __restrict__ tile_cnt, int ntiles) {
+  __shared__ int sdef, stie;
+  const bool none = st->none;
+  uint32_t T = 0;
+  if (!none) {
+    int b3, rem3;
+    block_select(hist2, 1024, st->rem2, b3, rem3);
+    T = (st->prefix2 << 10) | (uint32_t)b3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->T = T; st->t = rem3; }
+  }
   const int64_t base = (int64_t)blockIdx.x * kSelTile;
   int ndef = 0, ntie = 0;
-  for (int i = 0; i < kSelTile / kThreads; ++i) {
-    bool d, t;
-    flags_of(base + i * kThreads + threadIdx.x, C_local, bits, keys, s, d, t);
-    ndef += d; ntie += t;
+#pragma unroll
+  for (int it = 0; it < kSelTile / (4 * kThreads); ++it) {
+    bool d[4], t[4];
+    flags4(base + (int64_t)it * 4 * kThreads + 4 * threadIdx.x, C_local, bits, keys, none, T, d, t);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) { ndef += d[i]; ntie += t[i]; }
   }
-  __shared__ int sdef, stie;
   if (threadIdx.x == 0) { sdef = 0; stie = 0; }
   __syncthreads();
+#pragma unroll
   for (int o = 16; o; o >>= 1) {
     ndef += __shfl_xor_sync(0xffffffffu, ndef, o);
     ntie += __shfl_xor_sync(0xffffffffu, ntie, o);
@@ -235,47 +278,42 @@ __global__ void __launch_bounds__(1024) k_tile_scan(int* __restrict__ tile_cnt, 
   }
 }
 
-// K4c: order-preserving write of the selected local ids.
+// K4c: order-preserving write of the selected local ids, 4 consecutive classes per thread per iteration.
 __global__ void __launch_bounds__(kThreads) k_tile_write(int64_t C_local, const uint32_t* __restrict__ bits,
                                                          const uint32_t* __restrict__ keys, const SamplerState* st,
                                                          const int* __restrict__ tile_cnt, int ntiles,
                                                          int32_t* __restrict__ idx) {
-  __shared__ int wt[kThreads / 32];
-  const SamplerState s = *st;
+  __shared__ int wsum[kThreads / 32];
+  const bool none = st->none;
+  const uint32_t T = st->T;
+  const int tsel = st->t;
   const int64_t base = (int64_t)blockIdx.x * kSelTile;
   int tie_run = tile_cnt[2 * ntiles + blockIdx.x];
   int out_run = tile_cnt[3 * ntiles + blockIdx.x];
-  for (int i = 0; i < kSelTile / kThreads; ++i) {
-    const int64_t j = base + i * kThreads + threadIdx.x;
-    bool d, t;
-    flags_of(j, C_local, bits, keys, s, d, t);
-    int ntie;
-    int tie_rank = tie_run + block_flag_scan(t, wt, ntie);
-    bool sel = d || (t && tie_rank < s.t);
-    int nsel;
-    int pos = out_run + block_flag_scan(sel, wt, nsel);
-    if (sel) idx[pos] = (int32_t)j;
-    tie_run += ntie;
-    out_run += nsel;
-  }
-}
-
-__global__ void k_tcol(const int64_t* __restrict__ Y, int M, int64_t a, int64_t C_local,
-                       const int32_t* __restrict__ idx, const SamplerState* st, int32_t* __restrict__ tcol) {
-  int n = blockIdx.x * blockDim.x + threadIdx.x;
-  if (n >= M) return;
-  int64_t y = Y[n] - a;
-  int res = -1;
-  if (y >= 0 && y < C_local) {
-    int lo = 0, hi = st->k - 1;
-    while (lo <= hi) {
-      int mid = (lo + hi) >> 1;
-      int v = idx[mid];
-      if (v == y) { res = mid; break; }
-      if (v < y) lo = mid + 1; else hi = mid - 1;
+#pragma unroll 1
+  for (int it = 0; it < kSelTile / (4 * kThreads); ++it) {
+    const int64_t j0 = base + (int64_t)it * 4 * kThreads + 4 * threadIdx.x;
+    bool d[4], t[4];
+    flags4(j0, C_local, bits, keys, none, T, d, t);
+    const int nt = t[0] + t[1] + t[2] + t[3];
+    int ttot;
+    int trank = tie_run + block_count_scan(nt, wsum, ttot);
+    bool sel[4];
+    int ns = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      sel[i] = d[i] || (t[i] && trank < tsel);
+      trank += t[i];
+      ns += sel[i];
     }
+    int stot;
+    int pos = out_run + block_count_scan(ns, wsum, stot);
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (sel[i]) idx[pos++] = (int32_t)(j0 + i);
+    tie_run += ttot;
+    out_run += stot;
   }
-  tcol[n] = res;
 }
 
 }  // namespace
@@ -290,16 +328,14 @@ int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint6
   k_mark_positives<<<(sz.M + 255) / 256, 256, 0, s>>>(Y, sz.M, sz.a, sz.C_local, bits, st, sz.sample_mode);
   int grid = (int)std::min<int64_t>((sz.C_local + kThreads - 1) / kThreads, 148 * 8);
   k_keys_hist<<<grid, kThreads, 0, s>>>(sz.a, sz.C_local, seed, step, bits, keys, hist);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist, 2048, 0, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
-  k_hist_pass<<<grid, kThreads, 0, s>>>(sz.C_local, bits, keys, st, 21, 10, 0x7FFu, hist + 2048);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist + 2048, 2048, 1, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
-  k_hist_pass<<<grid, kThreads, 0, s>>>(sz.C_local, bits, keys, st, 10, 0, 0x3FFu, hist + 4096);
-  k_select_bucket<<<1, 1024, 0, s>>>(hist + 4096, 1024, 2, sz.budget, sz.C_local, sz.rate, sz.sample_mode, st);
-  k_tile_counts<<<sz.ntiles_sel, kThreads, 0, s>>>(sz.C_local, bits, keys, st, tile_cnt, sz.ntiles_sel);
+  k_hist_pass2<<<grid, kThreads, 0, s>>>(sz.C_local, sz.budget, sz.rate, sz.sample_mode, bits, keys, hist, st,
+                                         hist + 2048);
+  k_hist_pass3<<<grid, kThreads, 0, s>>>(sz.C_local, bits, keys, hist + 2048, st, hist + 4096);
+  k_tile_counts<<<sz.ntiles_sel, kThreads, 0, s>>>(sz.C_local, bits, keys, hist + 4096, st, tile_cnt, sz.ntiles_sel);
   k_tile_scan<<<1, 1024, 0, s>>>(tile_cnt, sz.ntiles_sel, st, err);
   k_tile_write<<<sz.ntiles_sel, kThreads, 0, s>>>(sz.C_local, bits, keys, st, tile_cnt, sz.ntiles_sel, idx);
-  k_tcol<<<(sz.M + 255) / 256, 256, 0, s>>>(Y, sz.M, sz.a, sz.C_local, idx, st, tcol);
-  return 11;
+  (void)tcol;   // tcol is filled by the target-cosine kernel (binary search in idx)
+  return 7;
 }
 
 }  // namespace pfc
