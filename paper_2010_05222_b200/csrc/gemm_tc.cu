@@ -17,6 +17,7 @@
 #include <cuda.h>
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 
 #include "pfc_internal.cuh"
@@ -120,8 +121,12 @@ __host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool 
 
 // ------------------------------------------------------------------------------------------------ kernel
 // *128: d-tile 128 (d % 256 != 0); DWF: dW with the momentum-SGD update fused into the epilogue
-enum Kind { LOGITS = 0, DX = 1, DW = 2, DX128 = 3, DW128 = 4, DWF = 5 };
-__host__ __device__ constexpr int base_kind(int k) { return k == DX128 ? DX : (k == DW128 || k == DWF) ? DW : k; }
+// DWF2: the same with 256-class tiles (two M = 128 halves share each X_hat tile: half the operand re-reads)
+enum Kind { LOGITS = 0, DX = 1, DW = 2, DX128 = 3, DW128 = 4, DWF = 5, DWF2 = 6 };
+__host__ __device__ constexpr int base_kind(int k) {
+  return k == DX128 ? DX : (k == DW128 || k == DWF || k == DWF2) ? DW : k;
+}
+__host__ __device__ constexpr bool is_fused(int k) { return k == DWF || k == DWF2; }
 
 constexpr int BK = 64;          // K elements per stage (128 B of bf16: one swizzle row)
 
@@ -148,6 +153,8 @@ template <>
 struct Cfg<DW128> : Cfg<DW> { static constexpr int UMMA_N = 128; };
 template <>
 struct Cfg<DWF> : Cfg<DW> { static constexpr int UMMA_N = 128, STAGES = 3, ACC = 2, EPI_WARPS = 8; };
+template <>
+struct Cfg<DWF2> : Cfg<DW> { static constexpr int MSUB = 2, UMMA_N = 128, STAGES = 3, ACC = 2, EPI_WARPS = 8; };
 
 template <int KIND>
 struct Smem {
@@ -156,11 +163,13 @@ struct Smem {
   static constexpr int B_BYTES = C::NMMA * C::UMMA_N * BK * 2;      // per stage
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int TMEM_COLS = C::MSUB * C::NMMA * C::UMMA_N * C::ACC;
-  static constexpr int EPI_BYTES = KIND == DWF ? 128 * 128 * 4 + 128 * 16 : KIND == LOGITS ? 2 * 2 * 128 * 8 : 0;
+  static constexpr int EPI_BYTES =
+      is_fused(KIND) ? 128 * 128 * 4 + C::MSUB * 128 * 16 : KIND == LOGITS ? 2 * 2 * 128 * 8 : 0;
   static constexpr int THREADS = 64 + 32 * C::EPI_WARPS;
   static constexpr int TOTAL = C::STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ + EPI_BYTES;
   static_assert(TMEM_COLS <= 512, "TMEM overflow");
-  static_assert(C::STAGES * STAGE_BYTES + 1024 + 256 + (KIND == DWF ? 128 * 128 * 4 + 128 * 16 : 4096) <= 232448,
+  static_assert(C::STAGES * STAGE_BYTES + 1024 + 256 + (is_fused(KIND) ? 128 * 128 * 4 + C::MSUB * 128 * 16 : 4096) <=
+                    232448,
                 "shared memory overflow (227 KB per CTA)");
 };
 
@@ -206,7 +215,7 @@ struct Work {
       n_units = mt * nt * p.nsplit;
       n_kb = (k + BK - 1) / BK;  // total k-blocks over the sampled classes
     } else {
-      mt = (k + 127) / 128;      // class tiles
+      mt = (k + 128 * C::MSUB - 1) / (128 * C::MSUB);   // class tiles
       nt = p.d / NT;
       n_units = mt * nt;
       n_kb = (p.M + BK - 1) / BK;
@@ -225,8 +234,8 @@ struct Work {
       kb0 = sp * p.kb_per_split;
       kb1 = min(n_kb, kb0 + p.kb_per_split);
     } else {
-      const int cb = u / nt, nb = u % nt;  // both d-halves of a class tile adjacent: A (G) slice hits L2
-      m0 = cb * 128; n0 = nb * NT; kb0 = 0; kb1 = n_kb;
+      const int cb = u / nt, nb = u % nt;  // the d-tiles of a class tile adjacent: A (G) slice hits L2
+      m0 = cb * 128 * Cfg<KIND_>::MSUB; n0 = nb * NT; kb0 = 0; kb1 = n_kb;
     }
   }
 };
@@ -248,8 +257,8 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
   // (row id, 1/||w||, radial factor)
   float4* s_tile = reinterpret_cast<float4*>(smem + C::STAGES * S::STAGE_BYTES + 256);
   int32_t* s_rowj = reinterpret_cast<int32_t*>(s_tile + 128 * 32);
-  float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
-  float* s_rad = s_inv + 128;
+  float* s_inv = reinterpret_cast<float*>(s_rowj + 128 * C::MSUB);
+  float* s_rad = s_inv + 128 * C::MSUB;
   // logits: per-row (max cos, sum) of the second warp set, per accumulator buffer and M-half
   float2* s_part = reinterpret_cast<float2*>(smem + C::STAGES * S::STAGE_BYTES + 256);
 
@@ -299,7 +308,9 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
             for (int c = 0; c < C::UMMA_N / 64; ++c)
               tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
           } else {
-            tma_load_2d(sa, &tmA, &full[stage], kb * BK, m0);
+#pragma unroll
+            for (int ms = 0; ms < C::MSUB; ++ms)
+              tma_load_2d(sa + ms * 128 * BK * 2, &tmA, &full[stage], kb * BK, m0 + ms * 128);
 #pragma unroll
             for (int c = 0; c < C::UMMA_N / 64; ++c)
               tma_load_2d(sb + c * BK * 128, &tmB, &full[stage], n0 + c * 64, kb * BK);
@@ -354,13 +365,18 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
     const int row_in = lg * 32 + lane;       // accumulator row (TMEM lane) of this thread
     const int eset = (warp - 2) >> 2;        // with 8 epilogue warps: two sets splitting the 32-column chunks
     constexpr int NSET = C::EPI_WARPS / 4;
-    int32_t nx_j = -1;                       // DWF: per-row scalars of the next tile (prefetched)
-    float nx_inv = 0.f, nx_rad = 0.f;
-    if (KIND_ == DWF && eset == 0 && (int)blockIdx.x < w.n_units) {
+    int32_t nx_j[C::MSUB];                   // fused SGD: per-row scalars of the next tile (prefetched)
+    float nx_inv[C::MSUB], nx_rad[C::MSUB];
+#pragma unroll
+    for (int h = 0; h < C::MSUB; ++h) { nx_j[h] = -1; nx_inv[h] = 0.f; nx_rad[h] = 0.f; }
+    if (is_fused(KIND_) && eset == 0 && (int)blockIdx.x < w.n_units) {
       int m1, n1, k0_, k1_;
       w.decode(p, blockIdx.x, m1, n1, k0_, k1_);
-      const int prow = m1 + row_in;
-      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+#pragma unroll
+      for (int h = 0; h < C::MSUB; ++h) {
+        const int prow = m1 + h * 128 + row_in;
+        if (prow < k) { nx_j[h] = p.sgd.idx[prow]; nx_inv[h] = p.sgd.inv_norm[prow]; nx_rad[h] = p.sgd.dotw[prow]; }
+      }
     }
     int acc = 0;
     uint32_t acc_phase = 0;
@@ -368,82 +384,95 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
       int m0, n0, kb0, kb1;
       w.decode(p, u, m0, n0, kb0, kb1);
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * (C::MSUB * C::NMMA * C::UMMA_N);
-      if constexpr (KIND_ != DWF) {
+      if constexpr (!is_fused(KIND_)) {
         mbar_wait(&acc_full[acc], acc_phase);
         tc_fence_after();
       }
-      if constexpr (KIND_ == DWF) {
-        // Fused lazy momentum SGD of 128 sampled classes x 128 dims (rows.cu K12 is the unfused
-        // form). (1) two warp sets copy two 32-column chunks each of the accumulator TMEM -> smem, then TMEM is
-        // released; (2) each of the 8 warps updates 16 rows, one 512-byte coalesced W and V segment per row and
-        // instruction, 16 loads per lane in flight. The per-row scalars of tile u + gridDim are prefetched into
-        // registers during tile u so that no tile starts with a dependent global load.
+      if constexpr (is_fused(KIND_)) {
+        // Fused lazy momentum SGD of 128*MSUB sampled classes x 128 dims (rows.cu K12 is the unfused
+        // form), one 128-class half at a time: (1) two warp sets copy two 32-column chunks each of the accumulator
+        // half TMEM -> XOR-swizzled smem (TMEM released after the last half); (2) each of the 8 warps updates 16
+        // rows, one 512-byte coalesced W and V segment per row and instruction, 16 loads per lane in flight. The
+        // per-row scalars of tile u + gridDim are prefetched into registers during tile u.
         asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");  // previous tile consumed
         if (eset == 0) {
-          s_rowj[row_in] = nx_j;
-          s_inv[row_in] = nx_inv;
-          s_rad[row_in] = nx_rad;
+#pragma unroll
+          for (int h = 0; h < C::MSUB; ++h) {
+            s_rowj[h * 128 + row_in] = nx_j[h];
+            s_inv[h * 128 + row_in] = nx_inv[h];
+            s_rad[h * 128 + row_in] = nx_rad[h];
+          }
         }
         mbar_wait(&acc_full[acc], acc_phase);
         tc_fence_after();
-#pragma unroll 1
-        for (int c = eset * 2; c < eset * 2 + 2; ++c) {
-          uint32_t v[32];
-          tmem_ld32(tacc + c * 32, v);
-#pragma unroll
-          for (int q = 0; q < 8; ++q)
-            s_tile[row_in * 32 + ((c * 8 + q) ^ (row_in & 31))] =
-                make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
-                            __uint_as_float(v[4 * q + 3]));
-        }
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&acc_empty[acc]);             // TMEM free: next tile's MMAs may start
-        if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
-        asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
-        if (eset == 0) {                                         // prefetch the next tile's per-row scalars
-          const int un = u + gridDim.x;
-          nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
-          if (un < w.n_units) {
-            int m1, n1, k0_, k1_;
-            w.decode(p, un, m1, n1, k0_, k1_);
-            const int prow = m1 + row_in;
-            if (prow < k) {
-              nx_j = p.sgd.idx[prow];
-              nx_inv = p.sgd.inv_norm[prow];
-              nx_rad = p.sgd.dotw[prow];
-            }
-          }
-        }
-        const int ew = warp - 2;                                 // rows ew*16 .. ew*16+15
+        const int ew = warp - 2;                                 // rows ew*16 .. ew*16+15 of each half
         const int col = n0 + lane * 4;
         const float lr = *p.sgd.lr;                              // device scalar (CUDA-graph replayable)
 #pragma unroll 1
-        for (int r0 = 0; r0 < 16; r0 += 8) {
-          float4 wv[8], mv[8];
-          int32_t jr[8];
+        for (int h = 0; h < C::MSUB; ++h) {
+          if (h > 0) asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");  // staging free
+#pragma unroll 1
+          for (int c = eset * 2; c < eset * 2 + 2; ++c) {
+            uint32_t v[32];
+            tmem_ld32(tacc + h * C::UMMA_N + c * 32, v);
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            jr[r] = s_rowj[ew * 16 + r0 + r];
-            if (jr[r] >= 0) {
-              wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
-              mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
+            for (int q = 0; q < 8; ++q)
+              s_tile[row_in * 32 + ((c * 8 + q) ^ (row_in & 31))] =
+                  make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                              __uint_as_float(v[4 * q + 3]));
+          }
+          if (h == C::MSUB - 1) {
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[acc]);         // TMEM free: next tile's MMAs may start
+            if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
+          }
+          asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
+          if (h == C::MSUB - 1 && eset == 0) {                   // prefetch the next tile's per-row scalars
+            const int un = u + gridDim.x;
+#pragma unroll
+            for (int hh = 0; hh < C::MSUB; ++hh) { nx_j[hh] = -1; nx_inv[hh] = 0.f; nx_rad[hh] = 0.f; }
+            if (un < w.n_units) {
+              int m1, n1, k0_, k1_;
+              w.decode(p, un, m1, n1, k0_, k1_);
+#pragma unroll
+              for (int hh = 0; hh < C::MSUB; ++hh) {
+                const int prow = m1 + hh * 128 + row_in;
+                if (prow < k) {
+                  nx_j[hh] = p.sgd.idx[prow];
+                  nx_inv[hh] = p.sgd.inv_norm[prow];
+                  nx_rad[hh] = p.sgd.dotw[prow];
+                }
+              }
             }
           }
+#pragma unroll 1
+          for (int r0 = 0; r0 < 16; r0 += 8) {
+            float4 wv[8], mv[8];
+            int32_t jr[8];
 #pragma unroll
-          for (int r = 0; r < 8; ++r) {
-            const int rr = ew * 16 + r0 + r;
-            if (jr[r] >= 0) {
-              const float inv = s_inv[rr], rad = s_rad[rr] * inv;  // w * rad = w_hat (w_hat . dw_hat)
-              const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
-              float4 w = wv[r], m = mv[r];
-              m.x = p.sgd.mu * m.x + (g4.x - w.x * rad) * inv + p.sgd.lambda * w.x;
-              m.y = p.sgd.mu * m.y + (g4.y - w.y * rad) * inv + p.sgd.lambda * w.y;
-              m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * inv + p.sgd.lambda * w.z;
-              m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * inv + p.sgd.lambda * w.w;
-              w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
-              *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
-              *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+            for (int r = 0; r < 8; ++r) {
+              jr[r] = s_rowj[h * 128 + ew * 16 + r0 + r];
+              if (jr[r] >= 0) {
+                wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
+                mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
+              }
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+              const int rr = ew * 16 + r0 + r;                   // row within the half
+              if (jr[r] >= 0) {
+                const float inv = s_inv[h * 128 + rr], rad = s_rad[h * 128 + rr] * inv;  // w*rad = w_hat (w_hat.dw_hat)
+                const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
+                float4 w = wv[r], m = mv[r];
+                m.x = p.sgd.mu * m.x + (g4.x - w.x * rad) * inv + p.sgd.lambda * w.x;
+                m.y = p.sgd.mu * m.y + (g4.y - w.y * rad) * inv + p.sgd.lambda * w.y;
+                m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * inv + p.sgd.lambda * w.z;
+                m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * inv + p.sgd.lambda * w.w;
+                w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
+                *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
+                *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+              }
             }
           }
         }
@@ -714,8 +743,17 @@ int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat1
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
-  const int64_t units = (sz.k_pad / 128) * (sz.d / 128);
-  launch<DWF>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  // 256-class tiles pay off when the contraction is long (K = M >= 1024: operand-bandwidth bound); at small M
+  // the update is HBM-bound and holding TMEM across the two halves only serialises it (PFC_DWF=1|2 overrides)
+  static const int forced = [] { const char* e = std::getenv("PFC_DWF"); return e ? std::atoi(e) : 0; }();
+  const int variant = forced ? forced : (sz.M >= 1024 ? 2 : 1);
+  if (variant == 1) {
+    const int64_t units = (sz.k_pad / 128) * (sz.d / 128);
+    launch<DWF>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  } else {
+    const int64_t units = ((sz.k_pad + 255) / 256) * (sz.d / 128);
+    launch<DWF2>(a, b, p, (int)std::min<int64_t>(units, num_sms()), s);
+  }
   return 1;
 }
 
