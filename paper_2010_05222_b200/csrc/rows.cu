@@ -295,12 +295,13 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
   const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   constexpr int U = 2;
   const int nit = (ldm + 255) / 256;
-  for (int it = 0; it < nit; ++it) {         // every lane runs every iteration (full-warp reductions)
-    const int n0 = it * 256 + lane * 8;
+  if (nit == 1) {
+    // one 8-row chunk per lane: its offsets stay in registers for the whole class loop, U classes in flight
+    const int n0 = lane * 8;
     const bool act = n0 < ldm;
     float off[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) off[i] = act ? s_off[i * l8 + lane + 32 * it] : INFINITY;
+    for (int i = 0; i < 8; ++i) off[i] = act ? s_off[i * l8 + lane] : INFINITY;
     for (int64_t jb = w0; jb < k_pad; jb += U * nw) {
       float c[U][8];
 #pragma unroll
@@ -329,11 +330,44 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
         if (act) store8<BF16>(G, j * ldm + n0, g);
         if (DOT) {
           d = warp_sum(d);
-          if (lane == 0) {
-            if (it == 0) dotw[j] = d;
-            else dotw[j] += d;          // ldm > 256: the same warp owns class j in every row chunk
-          }
+          if (lane == 0) dotw[j] = d;
         }
+      }
+    }
+  } else {
+    // M > 256: a warp streams one whole class row (ldm entries, contiguous) at a time, two 256-row chunks in
+    // flight; the row offsets come from the transposed (conflict-free) shared array
+    for (int64_t j = w0; j < k_pad; j += nw) {
+      const bool valid = j < k;
+      float d = 0.f;
+      for (int it = 0; it < nit; it += U) {
+        float c[U][8];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int n0 = (it + u) * 256 + lane * 8;
+          if (valid && it + u < nit && n0 < ldm) load8<BF16>(cosv, j * ldm + n0, c[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int n0 = (it + u) * 256 + lane * 8;
+          if (it + u >= nit || n0 >= ldm) break;
+          float g[8];
+          if (valid) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -s_off[i * l8 + lane + 32 * (it + u)]), lgs));
+              if (DOT) d = fmaf(g[i], c[u][i], d);
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) g[i] = 0.f;
+          }
+          store8<BF16>(G, j * ldm + n0, g);
+        }
+      }
+      if (DOT) {
+        d = warp_sum(d);
+        if (lane == 0) dotw[j] = d;
       }
     }
   }
@@ -481,7 +515,19 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
     cudaFuncSetAttribute(k_softmax_grad<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
     attr = true;
   }
-  const unsigned grid = (unsigned)std::min<int64_t>(sz.k_pad / 8, 148 * 8);
+  // persistent grid: exactly the resident blocks (a whole number of waves over the SMs)
+  static int per_sm[4] = {0, 0, 0, 0}, sms = 0;
+  const int ti = (bf16 ? 2 : 0) + (dotw ? 1 : 0);
+  if (!per_sm[ti]) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const void* f = bf16 ? (dotw ? (const void*)k_softmax_grad<true, true> : (const void*)k_softmax_grad<true, false>)
+                         : (dotw ? (const void*)k_softmax_grad<false, true> : (const void*)k_softmax_grad<false, false>);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm[ti], f, 256, 2048 * sizeof(float));
+    if (per_sm[ti] < 1) per_sm[ti] = 1;
+  }
+  const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>(sz.k_pad / 8, (int64_t)per_sm[ti] * sms));
   const int ldm = sz.M_pad;
   const unsigned tg = (unsigned)((sz.M + 255) / 256);
   if (bf16) {
