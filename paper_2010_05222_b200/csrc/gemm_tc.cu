@@ -395,12 +395,30 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
         // rows, one 512-byte coalesced W and V segment per row and instruction, 16 loads per lane in flight. The
         // per-row scalars of tile u + gridDim are prefetched into registers during tile u.
         asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");  // previous tile consumed
+        int nx_n0 = 0;                                           // d-offset of the next tile (W/V L2 prefetch)
         if (eset == 0) {
 #pragma unroll
           for (int h = 0; h < C::MSUB; ++h) {
             s_rowj[h * 128 + row_in] = nx_j[h];
             s_inv[h * 128 + row_in] = nx_inv[h];
             s_rad[h * 128 + row_in] = nx_rad[h];
+          }
+          // per-row scalars of the next tile: issued now, consumed a whole tile later
+          const int un = u + gridDim.x;
+#pragma unroll
+          for (int hh = 0; hh < C::MSUB; ++hh) { nx_j[hh] = -1; nx_inv[hh] = 0.f; nx_rad[hh] = 0.f; }
+          if (un < w.n_units) {
+            int m1, k0_, k1_;
+            w.decode(p, un, m1, nx_n0, k0_, k1_);
+#pragma unroll
+            for (int hh = 0; hh < C::MSUB; ++hh) {
+              const int prow = m1 + hh * 128 + row_in;
+              if (prow < k) {
+                nx_j[hh] = p.sgd.idx[prow];
+                nx_inv[hh] = p.sgd.inv_norm[prow];
+                nx_rad[hh] = p.sgd.dotw[prow];
+              }
+            }
           }
         }
         mbar_wait(&acc_full[acc], acc_phase);
@@ -428,24 +446,6 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
             if (++acc == C::ACC) { acc = 0; acc_phase ^= 1; }
           }
           asm volatile("bar.sync 3, %0;" ::"n"(32 * C::EPI_WARPS) : "memory");
-          if (h == C::MSUB - 1 && eset == 0) {                   // prefetch the next tile's per-row scalars
-            const int un = u + gridDim.x;
-#pragma unroll
-            for (int hh = 0; hh < C::MSUB; ++hh) { nx_j[hh] = -1; nx_inv[hh] = 0.f; nx_rad[hh] = 0.f; }
-            if (un < w.n_units) {
-              int m1, n1, k0_, k1_;
-              w.decode(p, un, m1, n1, k0_, k1_);
-#pragma unroll
-              for (int hh = 0; hh < C::MSUB; ++hh) {
-                const int prow = m1 + hh * 128 + row_in;
-                if (prow < k) {
-                  nx_j[hh] = p.sgd.idx[prow];
-                  nx_inv[hh] = p.sgd.inv_norm[prow];
-                  nx_rad[hh] = p.sgd.dotw[prow];
-                }
-              }
-            }
-          }
 #pragma unroll 1
           for (int r0 = 0; r0 < 16; r0 += 8) {
             float4 wv[8], mv[8];
@@ -472,6 +472,21 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
                 w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
                 *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
                 *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+              }
+            }
+            if (r0 == 0 && h == C::MSUB - 1 && eset == 0) {
+              // the next tile's W / V row segments into L2 while this tile's second batch is in flight
+#pragma unroll
+              for (int hh = 0; hh < C::MSUB; ++hh) {
+                if (nx_j[hh] >= 0) {
+                  const float* wp = p.sgd.W + (int64_t)nx_j[hh] * p.d + nx_n0;
+                  const float* vp = p.sgd.V + (int64_t)nx_j[hh] * p.d + nx_n0;
+#pragma unroll
+                  for (int l = 0; l < C::UMMA_N / 32; ++l) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+                  }
+                }
               }
             }
           }

@@ -135,26 +135,38 @@ __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const flo
   if (lane == 0) ct[n] = acc / fmaxf(sqrtf(ss), kNormEps);
 }
 
-// ---------------------------------------------------------------- K7: one warp per batch row
-__global__ void k_row_combine(int M, int ntiles, int ltile, int64_t a, int64_t C_local,
-                              const float2* __restrict__ partials, const int64_t* __restrict__ Y,
-                              const float* __restrict__ ct, const SamplerState* st, MarginParams mp,
-                              float* __restrict__ rowmax, float* __restrict__ rowsum, float* __restrict__ zt) {
-  const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (n >= M) return;
+// ---------------------------------------------------------------- K7: one 256-thread block per batch row
+// (the row's ~k/128 tile partials are spread over the block; two-level max then rescaled sum)
+__global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltile, int64_t a, int64_t C_local,
+                                                     const float2* __restrict__ partials,
+                                                     const int64_t* __restrict__ Y, const float* __restrict__ ct,
+                                                     const SamplerState* st, MarginParams mp,
+                                                     float* __restrict__ rowmax, float* __restrict__ rowsum,
+                                                     float* __restrict__ zt) {
+  __shared__ float sm[8], ss[8];
+  const int n = blockIdx.x;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float2* pr = partials + (int64_t)n * ntiles;
-  const int nvalid = (st->k + ltile - 1) / ltile;  // tiles past k_i are never written
-  ntiles = min(ntiles, nvalid);
-  float m = -INFINITY;
-  for (int t = lane; t < ntiles; t += 32) m = fmaxf(m, pr[t].x);
-  m = warp_max(m);
-  float l = 0.f;
-  if (m > -INFINITY)
-    for (int t = lane; t < ntiles; t += 32) { float2 v = pr[t]; l += v.y * __expf(v.x - m); }
+  const int nvalid = min(ntiles, (st->k + ltile - 1) / ltile);   // tiles past k_i are never written
+  float m = -INFINITY, l = 0.f;
+  for (int t = threadIdx.x; t < nvalid; t += blockDim.x) {       // online (max, sum) per thread
+    const float2 v = pr[t];
+    if (v.x > m) { l = l * __expf(m - v.x) + v.y; m = v.x; }
+    else if (v.x > -INFINITY) l += v.y * __expf(v.x - m);
+  }
+  const float wm = warp_max(m);
+  l = (m > -INFINITY) ? l * __expf(m - wm) : 0.f;
   l = warp_sum(l);
-  if (lane == 0) {
-    rowmax[n] = m;
-    rowsum[n] = l;
+  if (lane == 0) { sm[w] = wm; ss[w] = l; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M_ = -INFINITY;
+    for (int i = 0; i < 8; ++i) M_ = fmaxf(M_, sm[i]);
+    float L = 0.f;
+    if (M_ > -INFINITY)
+      for (int i = 0; i < 8; ++i) L += sm[i] > -INFINITY ? ss[i] * __expf(sm[i] - M_) : 0.f;
+    rowmax[n] = M_;
+    rowsum[n] = L;
     const int64_t j = Y[n] - a;
     zt[n] = (j >= 0 && j < C_local) ? mp.s * margin_phi(mp, ct[n]) : 0.f;   // owner rank of the positive
   }
@@ -486,8 +498,8 @@ int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const i
 
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s) {
-  k_row_combine<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct,
-                                                        st, mp, rowmax, rowsum, zt);
+  k_row_combine<<<sz.M, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
+                                     rowsum, zt);
   return 1;
 }
 
