@@ -525,16 +525,24 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
               for (int j = 0; j < 32; ++j)
                 if (col0 + j >= k || col0 + j == tc) cf[j] = -INFINITY;
             }
-            float cmx = cf[0];
+            // four independent accumulators: short dependency chains (the epilogue is latency-bound)
+            float q0 = cf[0], q1 = cf[1], q2 = cf[2], q3 = cf[3];
 #pragma unroll
-            for (int j = 1; j < 32; ++j) cmx = fmaxf(cmx, cf[j]);
-            const float nmx = fmaxf(mx, cmx);
+            for (int j = 4; j < 32; j += 4) {
+              q0 = fmaxf(q0, cf[j]); q1 = fmaxf(q1, cf[j + 1]); q2 = fmaxf(q2, cf[j + 2]); q3 = fmaxf(q3, cf[j + 3]);
+            }
+            const float nmx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
             if (nmx > -INFINITY) {
               const float nb = nmx * sl;
-              float cs = 0.f;
+              float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
-              for (int j = 0; j < 32; ++j) cs += ex2_ftz(fmaf(cf[j], sl, -nb));
-              sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + cs;
+              for (int j = 0; j < 32; j += 4) {
+                s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
+                s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
+                s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
+                s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+              }
+              sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
               mx = nmx;
             }
             // class-major store: lane pairs swap halves so that every 32-bit store covers rows (n, n+1) of one
