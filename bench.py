@@ -35,6 +35,9 @@ CONFIGS = {
     "c3": (360_232, 512, 128, 0.1, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=0.1, CosFace m=0.4 (BASELINE configs[2])"),
     "c3r1": (360_232, 512, 128, 1.0, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=1.0, CosFace m=0.4 (BASELINE configs[2])"),
     "c5": (100_000_000, 512, 256, 0.1, "arcface", 0.5, "100M identities, d=512, B=256/GPU, r=0.1, ArcFace (BASELINE configs[4])"),
+    # one rank's exact per-GPU work of the 8-GPU jobs, on one GPU (its C/8 shard and the global batch 8 x 256)
+    "c4rank": (1_250_000, 512, 2048, 0.1, "arcface", 0.5, "per-rank proxy of configs[3] on 8 GPUs: 1.25M-class shard, global batch 2048, r=0.1"),
+    "c5rank": (12_500_000, 512, 2048, 0.1, "arcface", 0.5, "per-rank proxy of configs[4] on 8 GPUs: 12.5M-class shard (51 GB W+V), global batch 2048, r=0.1"),
 }
 SCALE = 64.0
 MOMENTUM, WEIGHT_DECAY, LR = 0.9, 5e-4, 0.1

@@ -404,3 +404,51 @@ def test_sampling_variants_parity(smode, precision, world):
         assert maxrel(L.sampled_grad(), ref["dW"][i]) <= tg
     for L in layers:
         L.close()
+
+
+EDGE_CASES = [
+    # C, d, B, world, r, margin, m, label mode            what it exercises
+    (129, 128, 1, 1, 0.01, "arcface", 0.5, "uniform"),    # B = 1 (M = 1 << M_pad), k_i = 2
+    (3000, 1024, 16, 1, 0.1, "arcface", 0.5, "uniform"),  # d = 1024 (largest supported)
+    (2000, 128, 32, 1, 0.05, "cosface", 0.4, "same"),     # every row has the same label (dedup: |P| = 1)
+    (100, 128, 24, 1, 1.0, "none", 0.0, "uniform"),       # r = 1 with k = C_local = 100 < one tile
+    (1001, 128, 12, 3, 0.1, "arcface", 0.5, "uniform"),   # uneven shards 334/334/333
+    (2000, 128, 64, 2, 0.01, "arcface", 0.5, "stress"),   # all labels in shard 0: k_0 = |P_0| (n_0 = 0)
+]
+
+
+@pytest.mark.parametrize("case", EDGE_CASES, ids=lambda c: f"C{c[0]}-d{c[1]}-B{c[2]}-k{c[3]}-r{c[4]}-{c[7]}")
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_edge_cases(case, precision):
+    C, d, B, world, r, mt, m, mode = case
+    layers = [pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, margin_type=mt, margin=m, momentum=0.9,
+                            weight_decay=5e-4, precision=precision, seed=2, rank=i, world_size=world,
+                            comm_mode="loopback" if world > 1 else "nccl") for i in range(world)]
+    for L in layers:
+        W, V = L.params()
+        synth.fill_w_shard(W, 5, L.shard_start)
+        V.zero_()
+    if mode == "same":
+        ys = [np.full(B, 7, dtype=np.int64) for _ in range(world)]
+    else:
+        ys = synth.make_labels(31, 0, world, B, C, mode=mode, stress_range=max(2, C // world // 4))
+    xs = synth.make_features(31, 0, world, B, d)
+    xt = [torch.from_numpy(x).cuda() for x in xs]
+    yt = [torch.from_numpy(y).cuda() for y in ys]
+    gt = [torch.empty_like(x) for x in xt]
+    loss = torch.zeros(1, device="cuda")
+    if world == 1:
+        layers[0].forward_backward(xt[0], yt[0], gt[0], loss)
+    else:
+        pfc.group_forward_backward(layers, xt, yt, gt, loss)
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, world_size=world, sample_rate=r, margin_type=MT[mt], margin=m,
+                       momentum=0.9, weight_decay=5e-4, seed=2)
+    ref = oracle.forward_backward(cfg, xs, ys, lambda i: synth.w_rows_np(5, i, d), step=0)
+    tl, tg = TOL[precision]
+    assert abs(loss.item() - ref["loss"]) / abs(ref["loss"]) <= tl
+    for i, L in enumerate(layers):
+        assert np.array_equal(L.sampled(), ref["idx"][i])
+        assert maxrel(gt[i].cpu().numpy(), ref["grad_x"][i]) <= tg
+        assert maxrel(L.sampled_grad(), ref["dW"][i]) <= tg
+    for L in layers:
+        L.close()
