@@ -27,6 +27,8 @@ struct pfc_ctx {
   MarginParams mp{};
   bool bf16 = false;
   bool use_tc = false;
+  bool fused_gather = false;   // K5 + K6 in one kernel (M <= 256); G carries 1/||w|| (R25)
+  bool use_dwx = false;        // train step: K9 + K11 + K12 in one kernel (dwx.cu), no W_s copy
   bool sync_check = false;
   std::string err;
   ncclComm_t comm = nullptr;
@@ -293,7 +295,9 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->G, Mp * kp * esz);      // class-major [k_pad][M_pad]
   ALLOC(c->dXh, Mp * d * 4);
   ALLOC(c->dxh_local, B * d * 4);
-  ALLOC(c->split_ws, (size_t)(c->use_tc ? dx_split_ws_floats(sz) : 1) * 4);
+  c->fused_gather = c->use_tc && logits_gather_supported(sz);
+  c->use_dwx = c->fused_gather && dwx_supported(sz);
+  ALLOC(c->split_ws, (size_t)(c->use_tc ? std::max(dx_split_ws_floats(sz), c->use_dwx ? dwx_ws_floats(sz) : 0) : 1) * 4);
   ALLOC(c->dWh, kp * d * 4);
   ALLOC(c->dotw, kp * 4);
   ALLOC(c->err_dev, 16);
@@ -388,7 +392,7 @@ void phase_a(pfc_ctx* c, const float* x, const int64_t* labels, cudaStream_t s) 
 }
 
 // K1b, sampler K2-K4, K5, K5b, K6 logits + partial den_i, K7 local row (max, sum).
-void phase_b(pfc_ctx* c, cudaStream_t s) {
+void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   const bool bf = c->bf16;
   int n = 0;
@@ -397,10 +401,13 @@ void phase_b(pfc_ctx* c, cudaStream_t s) {
   n += launch_sampler(sz, c->Y, c->cfg.seed, c->step_dev, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
                       c->tcol, c->err_dev, s);
   mark(c, 2, s);
-  n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
+  if (!c->fused_gather) n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
   n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tcol, c->ct, s);
   mark(c, 3, s);
-  if (c->use_tc)
+  if (c->fused_gather)
+    n += launch_logits_gather_tc(sz, c->W, c->idx, c->Xb, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
+                                 c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev, s);
+  else if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);
   else
@@ -423,9 +430,12 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
   n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, s);
   mark(c, 5, s);
   n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
-                           fused && c->use_tc ? c->dotw : nullptr, s);
+                           fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr, s);
   mark(c, 6, s);
-  if (c->use_tc)
+  if (fused && c->use_dwx) {
+    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
+    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, s);
+  } else if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
   else
     n += launch_dx_simt(sz, c->bf16, c->G, c->Ws, c->st, c->dXh, s);
@@ -438,8 +448,11 @@ void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream
   int n = 0;
   n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
   mark(c, 8, s);
-  if (c->use_tc && fused) {
-    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay};
+  if (fused && c->use_dwx) {
+    // dW + SGD ran inside the dX kernel (phase_d)
+  } else if (c->use_tc && fused) {
+    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
+              c->fused_gather ? 1 : 0};
     n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, s);
   } else {
     if (c->use_tc)
@@ -448,7 +461,7 @@ void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream
       n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
     if (fused)
       n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
-                      c->cfg.weight_decay, s);
+                      c->cfg.weight_decay, c->fused_gather ? 1 : 0, s);
   }
   mark(c, 9, s);
   c->launches += n;
@@ -495,7 +508,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     nccl(ncclAllGather(c->Y + (size_t)sz.rank * sz.B, c->Y, (size_t)sz.B, ncclInt64, c->comm, s));
     nccl(ncclGroupEnd());
   }
-  phase_b(c, s);
+  phase_b(c, fused, s);
   const float* gmax = c->rowmax;
   if (multi) {  // Alg.1 L7 (stabilised, R12): global row max, then global sum
     nccl(ncclAllReduce(c->rowmax, c->gmax, sz.M, ncclFloat, ncclMax, c->comm, s));
@@ -611,7 +624,7 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
       CUDA_TRY(c0, cudaMemcpyAsync(ctxs[q]->Y + (size_t)r * sz.B, ctxs[r]->Y + (size_t)r * sz.B, (size_t)sz.B * 8,
                                    cudaMemcpyDefault, s));
     }
-  for (int r = 0; r < n; ++r) phase_b(ctxs[r], s);
+  for (int r = 0; r < n; ++r) phase_b(ctxs[r], fused, s);
   for (int r = 0; r < n; ++r) { src.p[r] = ctxs[r]->rowmax; dst.p[r] = ctxs[r]->gmax; }
   c0->launches += launch_group_reduce(sz.M, src, 0, dst, n, n, 1, s);
   for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
@@ -672,7 +685,7 @@ pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
   }
   c->launches += launch_set_scalar(c->lr_dev, lr, s);
   c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
-                            c->cfg.weight_decay, s);
+                            c->cfg.weight_decay, c->fused_gather ? 1 : 0, s);
   if (c->prof) mark(c, 10, s);
   CUDA_TRY(c, cudaGetLastError());
   c->fb_done = false;
@@ -741,7 +754,7 @@ pfc_status pfc_get_sampled_grad(pfc_ctx* c, float* dW_host, int64_t capacity_row
   float* tmp = nullptr;
   const size_t bytes = (size_t)h.k * c->sz.d * 4;
   CUDA_TRY(c, cudaMalloc(&tmp, std::max<size_t>(bytes, 16)));
-  c->launches += launch_raw_grad(c->sz, c->W, c->dWh, c->idx, c->inv_norm, c->st, tmp, 0);
+  c->launches += launch_raw_grad(c->sz, c->W, c->dWh, c->idx, c->inv_norm, c->st, tmp, c->fused_gather ? 1 : 0, 0);
   cudaError_t e = cudaMemcpy(dW_host, tmp, bytes, cudaMemcpyDeviceToHost);
   cudaFree(tmp);
   CUDA_TRY(c, e);

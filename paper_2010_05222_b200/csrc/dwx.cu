@@ -1,0 +1,358 @@
+// K9 + K11 + K12 fused (train step, bf16 tensor-core path, global batch M <= 256): one persistent kernel computes,
+// per 128-class tile of the sampled shard,
+//   dW_hat tile  D1[128 x 128] = G'^T X_hat            (Alg.1 L10, tcgen05.mma: A = G' K-major, B = X_hat MN-major)
+//   the lazy momentum-SGD update of those W / V rows  (as K12 / the DWF kernel of gemm_tc.cu)
+//   dX_hat partial D2[M x 128] += G' bf16(w_old)       (Alg.1 L12, A = G' MN-major, B = bf16(w) MN-major)
+// The old W rows the update loads anyway are converted to bf16 in shared memory and fed to the dX contraction, so
+// neither the bf16 copy W_s (written by the logits kernel otherwise) nor a separate dX GEMM pass over it is needed.
+// G' = G / ||w_j|| (R25) makes bf16(w) un-normalised the right operand: dX_hat = sum_j G'_nj w_j.
+//
+// CTA b owns the 128-column d-tile b / gper and the class tiles g, g + gper, ... (g = b % gper); its dX_hat
+// partial for that d-tile stays in TMEM for the whole kernel and is written once to the split workspace, reduced
+// over g by k_splitk_reduce (deterministic order).
+//   warp 0    TMA producer: the class tile's G' rows (all M_pad batch columns) and the X_hat chunks (64 batch rows
+//             x 128 columns, 4-stage ring, prefetched a tile ahead)
+//   warp 1    MMA issuer: dW(t) into D1[t % 2], then dX(t) into D2 once the epilogue has staged bf16 w_old(t)
+//   warps 2-9 epilogue per tile: (1) bf16 w_old tile (first read of the W rows; it does not need D1, so dX(t) and
+//             the next tile's G' load overlap the rest), (2) D1 -> smem, (3) coalesced W / V row updates
+#include <cuda_bf16.h>
+#include <algorithm>
+#include <cstdlib>
+
+#include "pfc_internal.cuh"
+#include "tc_common.cuh"
+
+namespace pfc {
+namespace {
+
+constexpr int DX_EPI = 8;
+constexpr int DX_THREADS = 64 + 32 * DX_EPI;
+constexpr int G_CHUNK = 128 * 64 * 2;       // 128 classes x 64 batch columns (bf16, 128-byte swizzle)
+constexpr int G_BUF = 4 * G_CHUNK;          // M_pad <= 256
+constexpr int X_CHUNK = 64 * 128 * 2;       // 64 batch rows x 128 columns (two 64-column swizzled halves)
+constexpr int X_STAGES = 4;
+constexpr int WB_HALF = 128 * 128;          // 128 classes x 64 columns bf16
+constexpr int OFF_G = 0;
+constexpr int OFF_X = OFF_G + G_BUF;
+constexpr int OFF_WB = OFF_X + X_STAGES * X_CHUNK;
+constexpr int OFF_ST = OFF_WB + 2 * WB_HALF;
+constexpr int OFF_AUX = OFF_ST + 128 * 128 * 4;
+constexpr int DX_SMEM = OFF_AUX + 256 + 3 * 128 * 4 + 1024;
+static_assert(DX_SMEM <= 232448, "shared memory overflow");
+
+struct DwxParams {
+  int M, d, nkb;        // nkb = M_pad / 64
+  int gper;             // CTAs per d-tile
+  const SamplerState* st;
+  SgdArgs sgd;
+  float* ws;            // [gper][M][d] dX_hat partials
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(DX_THREADS, 1)
+    k_dwx(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX, DwxParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sG = smem + OFF_G;
+  uint8_t* sX = smem + OFF_X;
+  uint8_t* sWb = smem + OFF_WB;
+  float4* s_tile = reinterpret_cast<float4*>(smem + OFF_ST);     // [128 rows][32 float4], XOR-swizzled
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_AUX);
+  uint64_t* g_full = bars;
+  uint64_t* g_empty = bars + 1;
+  uint64_t* x_full = bars + 2;        // [X_STAGES]
+  uint64_t* x_empty = bars + 6;       // [X_STAGES]
+  uint64_t* d1_full = bars + 10;      // [2]
+  uint64_t* d1_empty = bars + 12;     // [2]
+  uint64_t* wb_full = bars + 14;
+  uint64_t* wb_empty = bars + 15;
+  uint64_t* d2_full = bars + 16;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 17);
+  int32_t* s_rowj = reinterpret_cast<int32_t*>(smem + OFF_AUX + 256);
+  float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
+  float* s_rad = s_inv + 128;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = p.st->k;
+  const int nct = (k + 127) / 128;
+  const int g = blockIdx.x % p.gper;
+  const int n0 = (blockIdx.x / p.gper) * 128;               // this CTA's d-tile
+  const int ntl = g < nct ? (nct - g + p.gper - 1) / p.gper : 0;
+  const int nkb = p.nkb, nh = p.nkb / 2 > 0 ? p.nkb / 2 : 1;   // dX M-halves of 128 batch rows
+
+  if (threadIdx.x == 0) {
+    mbar_init(g_full, 1); mbar_init(g_empty, 1);
+    for (int i = 0; i < X_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d1_full[i], 1); mbar_init(&d1_empty[i], DX_EPI); }
+    mbar_init(wb_full, DX_EPI);
+    mbar_init(wb_empty, 1);
+    mbar_init(d2_full, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmG); tma_prefetch(&tmX); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;     // cols [0, 256): D1 x 2; [256, 512): D2 halves
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer
+    if (lane == 0) {
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int i = 0; i < ntl; ++i) {
+        const int ct = g + i * p.gper;
+        mbar_wait(g_empty, (uint32_t)((i & 1) ^ 1));         // dX(t - 1) has read the previous G' tile
+        mbar_expect_tx(g_full, (uint32_t)(nkb * G_CHUNK));
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sG + kb * G_CHUNK, &tmG, g_full, kb * 64, ct * 128);
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&x_empty[xs], xph ^ 1);
+          mbar_expect_tx(&x_full[xs], (uint32_t)X_CHUNK);
+          tma_load_2d(sX + xs * X_CHUNK, &tmX, &x_full[xs], n0, kb * 64);
+          tma_load_2d(sX + xs * X_CHUNK + X_CHUNK / 2, &tmX, &x_full[xs], n0 + 64, kb * 64);
+          if (++xs == X_STAGES) { xs = 0; xph ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC_DW = make_idesc(128, 128, false, true);
+    constexpr uint32_t IDESC_DX = make_idesc(128, 128, true, true);
+    int xs = 0, acc = 0;
+    uint32_t xph = 0, aph = 0;
+    auto dx = [&](int i) {      // D2 += G'(tile i) bf16(w_old(tile i)), then release both operands
+      mbar_wait(wb_full, (uint32_t)(i & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t ga = smem_u32(sG), wa = smem_u32(sWb);
+        for (int h = 0; h < nh; ++h)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma(tmem_base + 256 + h * 128, make_desc(ga + 2 * h * G_CHUNK + ks * 2048, G_CHUNK, 1024),
+                   make_desc(wa + ks * 2048, WB_HALF, 1024), IDESC_DX, (i > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(g_empty);
+        tc_commit(wb_empty);
+      }
+      __syncwarp();
+    };
+    for (int i = 0; i < ntl; ++i) {
+      mbar_wait(g_full, (uint32_t)(i & 1));
+      mbar_wait(&d1_empty[acc], aph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&x_full[xs], xph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ga = smem_u32(sG + kb * G_CHUNK), xa = smem_u32(sX + xs * X_CHUNK);
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma(tmem_base + acc * 128, make_desc(ga + kk * 32, 16, 1024), make_desc(xa + kk * 2048, X_CHUNK / 2, 1024),
+                   IDESC_DW, (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&x_empty[xs]);
+        }
+        __syncwarp();
+        if (++xs == X_STAGES) { xs = 0; xph ^= 1; }
+      }
+      if (lane == 0) tc_commit(&d1_full[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+      dx(i);          // the epilogue stages bf16 w_old(t) before it needs D1(t)
+    }
+    if (lane == 0) {
+      if (ntl > 0) tc_commit(d2_full);
+      else mbar_arrive(d2_full);
+    }
+    __syncwarp();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int ew = warp - 2;
+    const int lg = warp & 3;
+    const int row_in = lg * 32 + lane;
+    const int eset = ew >> 2;
+    const float lr = *p.sgd.lr;
+    int32_t nx_j = -1;
+    float nx_inv = 0.f, nx_rad = 0.f;
+    if (eset == 0 && ntl > 0) {
+      const int prow = g * 128 + row_in;
+      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+    }
+    int acc = 0;
+    uint32_t aph = 0;
+    const int col = n0 + lane * 4;           // row-update mapping: one 512-byte row segment per warp instruction
+    for (int i = 0; i < ntl; ++i) {
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile fully consumed
+      if (eset == 0) {
+        s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
+        nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
+        if (i + 1 < ntl) {
+          const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
+          if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+        }
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
+      // (1) bf16 w_old tile for dX(t): independent of D1, so dX(t) and the next tile's G' load overlap (3)
+      mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));                       // dX(t - 1) has read the bf16 tile
+#pragma unroll 1
+      for (int r0 = 0; r0 < 16; r0 += 8) {
+        float4 wv[8];
+        int32_t jr[8];
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          jr[it] = s_rowj[ew * 16 + r0 + it];
+          if (jr[it] >= 0) wv[it] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[it] * p.d + col);
+        }
+        const int hc = lane >> 4, cq = lane & 15;
+#pragma unroll
+        for (int it = 0; it < 8; ++it) {
+          const int rr = ew * 16 + r0 + it;
+          const uint2 wb = jr[it] >= 0 ? make_uint2(pack_bf16x2(wv[it].x, wv[it].y), pack_bf16x2(wv[it].z, wv[it].w))
+                                       : make_uint2(0u, 0u);
+          // MN-major swizzled B tile: half hc, class row rr, columns cq*4 .. +3 (8 bytes)
+          *reinterpret_cast<uint2*>(sWb + hc * WB_HALF + rr * 128 + ((((cq >> 1) ^ (rr & 7)) << 4) | ((cq & 1) << 3))) = wb;
+        }
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wb_full);
+      // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
+      mbar_wait(&d1_full[acc], aph);
+      tc_fence_after();
+      {
+        const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 128;
+#pragma unroll 1
+        for (int c = eset * 2; c < eset * 2 + 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tacc + c * 32, v);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            s_tile[row_in * 32 + ((c * 8 + q) ^ (row_in & 31))] =
+                make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
+                            __uint_as_float(v[4 * q + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d1_empty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
+      // (3) momentum-SGD row updates (w re-read hits L2), 8 rows in flight per lane
+#pragma unroll 1
+      for (int r0 = 0; r0 < 16; r0 += 8) {
+        float4 wv[8], mv[8];
+        int32_t jr[8];
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          jr[r] = s_rowj[ew * 16 + r0 + r];
+          if (jr[r] >= 0) {
+            wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
+            mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
+          }
+        }
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+          const int rr = ew * 16 + r0 + r;
+          if (jr[r] >= 0) {
+            const float inv = s_inv[rr], rad = s_rad[rr] * inv;
+            const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
+            float4 w = wv[r], m = mv[r];
+            const float oi = p.sgd.gsc ? 1.f : inv;
+            m.x = p.sgd.mu * m.x + (g4.x - w.x * rad) * oi + p.sgd.lambda * w.x;
+            m.y = p.sgd.mu * m.y + (g4.y - w.y * rad) * oi + p.sgd.lambda * w.y;
+            m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * oi + p.sgd.lambda * w.z;
+            m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * oi + p.sgd.lambda * w.w;
+            w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
+            *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
+            *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+          }
+        }
+        if (r0 == 0 && eset == 0 && nx_j >= 0) {   // the next tile's W / V row segments into L2
+          const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
+          const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          }
+        }
+      }
+    }
+    // dX_hat partial of this CTA (zeros when it had no class tile) -> split workspace
+    mbar_wait(d2_full, 0);
+    tc_fence_after();
+    if (eset < nh) {
+      const int row = eset * 128 + row_in;
+      float* dst = p.ws + ((int64_t)g * p.M + row) * p.d + n0;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(lg * 32) << 16) + 256 + eset * 128 + c * 32, v);
+        if (ntl == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
+        if (row < p.M) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<uint4*>(dst + c * 32)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+__global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, const float* __restrict__ ws, float* __restrict__ out) {
+  const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i >= n) return;
+  float4 acc = *reinterpret_cast<const float4*>(ws + i);
+  for (int s = 1; s < nsplit; ++s) {
+    const float4 v = *reinterpret_cast<const float4*>(ws + s * stride + i);
+    acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  *reinterpret_cast<float4*>(out + i) = acc;
+}
+
+int dwx_gper(const Sizes& sz) { return std::max(1, num_sms() / (sz.d / 128)); }
+
+}  // namespace
+
+bool dwx_supported(const Sizes& sz) {
+  static const int forced = [] { const char* e = std::getenv("PFC_DWX"); return e ? std::atoi(e) : 1; }();
+  return forced != 0 && sz.M <= 256 && sz.d % 128 == 0;
+}
+
+int64_t dwx_ws_floats(const Sizes& sz) { return (int64_t)dwx_gper(sz) * sz.M * sz.d; }
+
+int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                  const SgdArgs& sa, float* ws, float* dXh, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_dwx, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
+    attr = true;
+  }
+  const CUtensorMap tg = make_map(G, sz.k_pad, sz.M_pad, 64, 128);   // G' class-major: 128 classes x 64 batch
+  const CUtensorMap tx = make_map(Xb, sz.M_pad, sz.d, 64, 64);       // X_hat: 64 batch rows x 64 columns
+  DwxParams p{};
+  p.M = sz.M; p.d = sz.d; p.nkb = (int)(sz.M_pad / 64); p.gper = dwx_gper(sz); p.st = st; p.sgd = sa; p.ws = ws;
+  const int grid = p.gper * (sz.d / 128);
+  k_dwx<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+  const int64_t n = (int64_t)sz.M * sz.d;
+  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, ws, dXh);
+  return 2;
+}
+
+}  // namespace pfc

@@ -1,0 +1,395 @@
+// K5 + K6 fused (bf16 tensor-core path, global batch M <= 256): gather of the sampled fp32 W rows, their norms,
+// the bf16 operand W_s and the logits contraction in one persistent kernel (Alg.1 L3; the sampled
+// rows W_s of L3 are read once from HBM instead of gather -> W_s -> logits re-read).
+//
+// Per 128-class tile t (sampled positions n0 .. n0+127) and 64-wide K block kb:
+//   warps 0-1   producers: TMA of the two X_hat halves (bf16, 128-byte swizzle) + 16-byte cp.async of the sampled
+//               fp32 W row chunks (padded pitch) into the stage, all completing on one mbarrier
+//   warp 2      tcgen05.mma issuer: C[256 x 128] (two M = 128 halves) += X_hat . bf16(w)^T into TMEM
+//   warps 3-6   converters, one thread per class row: fp32 row chunk -> sum of squares (the row norm after the
+//               last kb) and bf16, written in place as the K-major swizzled UMMA B tile
+//   warp 7      TMA store of that bf16 tile into W_s (the K9 dX operand; rows past k_i are zero)
+//   warps 8-15  epilogue: cos = acc / ||w|| (the norm folds in per column, R25), fp16 class-major store and the
+//               per-(row, tile) max / sum partials exactly as the unfused logits kernel (gemm_tc.cu)
+// W_s holds bf16(w) un-normalised; K8 folds 1/||w_j|| into G (so dX_hat = G' W_s), and the dW / SGD consumers
+// take G' = G / ||w|| (R25).
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <algorithm>
+#include <cstdlib>
+
+#include "pfc_internal.cuh"
+#include "tc_common.cuh"
+
+namespace pfc {
+namespace {
+
+constexpr int LG_BK = 64;
+constexpr int LG_STAGES = 3;
+constexpr int LG_ACC = 2;
+constexpr int LG_PROD = 2;                              // producer warps (64 W rows each)
+constexpr int LG_MMA_WARP = LG_PROD;
+constexpr int LG_CONV0 = LG_MMA_WARP + 1;
+constexpr int LG_CONV = 4;                              // converter warps: thread = class row of the tile
+constexpr int LG_EPI = 8;                               // epilogue warps: two sets of 4 (64 columns each)
+constexpr int LG_STORE_WARP = LG_CONV0 + LG_CONV;
+constexpr int LG_EPI_WARP0 = LG_STORE_WARP + 1;
+constexpr int LG_THREADS = 32 * (LG_EPI_WARP0 + LG_EPI);
+constexpr int LG_PITCH = 272;                           // fp32 chunk pitch: 256 B + 16 (conflict-free LDS.128)
+constexpr int LG_A_BYTES = 2 * 128 * LG_BK * 2;         // X_hat, two M halves
+constexpr int LG_W_BYTES = 35 * 1024;                   // 128 x 272 B rounded up to 1 KB
+constexpr int LG_STAGE = LG_A_BYTES + LG_W_BYTES;
+constexpr int LG_AUX = 256 /*barriers*/ + LG_ACC * 128 * 4 /*s_inv*/ + LG_ACC * 2 * 128 * 8 /*s_part*/;
+constexpr int LG_SMEM = LG_STAGES * LG_STAGE + 1024 + LG_AUX;
+static_assert(LG_SMEM <= 232448, "shared memory overflow");
+static_assert(128 * LG_PITCH <= LG_W_BYTES, "W stage too small");
+
+struct LgParams {
+  int M, ldm, d;
+  const SamplerState* st;
+  const float* W;          // C_local x d fp32 shard
+  const int32_t* idx;      // sampled local rows, ascending
+  float* inv_norm;         // out: 1/||w_j|| per sampled position (0 past k_i)
+  int* err;
+  const int32_t* tcol;     // per row: sampled position of its target or -1
+  float s_log2e, scale;
+  __half* cosv;            // class-major [k_pad][ldm]
+  float2* partials;        // M x n_ltiles
+  int n_ltiles;
+  int write_ws;            // store bf16(w) into W_s (the separate dX GEMM needs it; the fused dW/dX kernel does not)
+};
+
+__device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+__global__ void __launch_bounds__(LG_THREADS, 1)
+    k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs, LgParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* aux = smem + LG_STAGES * LG_STAGE;
+  uint64_t* full = reinterpret_cast<uint64_t*>(aux);
+  uint64_t* conv = full + LG_STAGES;
+  uint64_t* empty = conv + LG_STAGES;
+  uint64_t* acc_full = empty + LG_STAGES;
+  uint64_t* acc_empty = acc_full + LG_ACC;
+  uint64_t* inv_full = acc_empty + LG_ACC;
+  uint64_t* inv_empty = inv_full + LG_ACC;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(inv_empty + LG_ACC);
+  float* s_inv = reinterpret_cast<float*>(aux + 256);                 // [ACC][128]
+  float2* s_part = reinterpret_cast<float2*>(s_inv + LG_ACC * 128);   // [ACC][2][128]
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = p.st->k;
+  const int nt = (k + 127) / 128;                 // class tiles holding sampled classes
+  const int n_kb = p.d / LG_BK;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < LG_STAGES; ++i) {
+      mbar_init(&full[i], 1 + 32 * LG_PROD);      // TMA expect_tx + one cp.async arrive per producer lane
+      mbar_init(&conv[i], LG_CONV);
+      mbar_init(&empty[i], 2);                    // MMA commit + W_s store read back
+    }
+    for (int i = 0; i < LG_ACC; ++i) {
+      mbar_init(&acc_full[i], 1);
+      mbar_init(&acc_empty[i], LG_EPI);
+      mbar_init(&inv_full[i], LG_CONV);
+      mbar_init(&inv_empty[i], LG_EPI);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmWs); }
+  if (warp == LG_MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp < LG_PROD) {
+    // ---------------------------------------------------------------- producers
+    // W rows: 16-byte cp.async (LDGSTS); a warp instruction moves two rows x 256 B (coalesced); warp pw owns
+    // rows 64 pw .. 64 pw + 63 of the tile, their ids held in registers for the whole tile; completion is
+    // tracked by the stage mbarrier (cp.async.mbarrier.arrive.noinc). X_hat by TMA. (One 256-byte
+    // cp.async.bulk per row, and a single producer warp reading row ids from smem, were measured far slower.)
+    int stage = 0;
+    uint32_t phase = 0;
+    const int half = lane >> 4, ch = lane & 15;
+    const int rbase = warp * 64 + half;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+      const int n0 = t * 128;
+      int rid[32];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int r = n0 + rbase + 2 * i;
+        rid[i] = r < k ? p.idx[r] : -1;
+      }
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = smem + stage * LG_STAGE;
+        uint8_t* sw = sa + LG_A_BYTES;
+        if (warp == 0 && lane == 0) {
+          mbar_expect_tx(&full[stage], (uint32_t)LG_A_BYTES);
+          tma_load_2d(sa, &tmA, &full[stage], kb * LG_BK, 0);
+          tma_load_2d(sa + 128 * LG_BK * 2, &tmA, &full[stage], kb * LG_BK, 128);
+        }
+        const uint32_t dst0 = smem_u32(sw) + rbase * LG_PITCH + ch * 16;
+        const float* srcc = p.W + kb * LG_BK + ch * 4;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          if (rid[i] >= 0)
+            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + 2 * i * LG_PITCH),
+                         "l"(srcc + (int64_t)rid[i] * p.d)
+                         : "memory");
+        }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&full[stage])) : "memory");
+        if (++stage == LG_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == LG_MMA_WARP) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC = make_idesc(128, 128, false, false);
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+      mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + acc * 256;
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        mbar_wait(&conv[stage], phase);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t sa = smem_u32(smem + stage * LG_STAGE);
+          const uint32_t sb = sa + LG_A_BYTES;
+#pragma unroll
+          for (int kk = 0; kk < LG_BK / 16; ++kk) {
+#pragma unroll
+            for (int ms = 0; ms < 2; ++ms)
+              tc_mma(tacc + ms * 128, make_desc(sa + ms * 128 * LG_BK * 2 + kk * 32, 16, 1024),
+                     make_desc(sb + kk * 32, 16, 1024), IDESC, (kb > 0 || kk > 0) ? 1u : 0u);
+          }
+          tc_commit(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == LG_STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (lane == 0) tc_commit(&acc_full[acc]);
+      __syncwarp();
+      if (++acc == LG_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp < LG_STORE_WARP) {
+    // ---------------------------------------------------------------- converters (thread = class row r)
+    const int r = (warp - LG_CONV0) * 32 + lane;
+    int stage = 0, acc = 0;
+    uint32_t phase = 0, acc_phase = 0;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+      const int n0 = t * 128;
+      const bool valid = n0 + r < k;
+      float ss = 0.f;
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait(&full[stage], phase);
+        uint8_t* sw = smem + stage * LG_STAGE + LG_A_BYTES;
+        uint32_t pk[32];
+        if (valid) {
+          const float4* src = reinterpret_cast<const float4*>(sw + r * LG_PITCH);
+#pragma unroll
+          for (int q = 0; q < 16; ++q) {
+            const float4 v = src[q];
+            ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
+            pk[2 * q] = pack_bf16(v.x, v.y);
+            pk[2 * q + 1] = pack_bf16(v.z, v.w);
+          }
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q) pk[q] = 0u;
+        }
+        // every row read before the bf16 tile overwrites the head of the fp32 buffer
+        asm volatile("bar.sync 5, %0;" ::"n"(32 * LG_CONV) : "memory");
+        uint4* dst = reinterpret_cast<uint4*>(sw + r * 128);   // K-major SW128: row r, 16-byte chunk c ^ (r % 8)
+#pragma unroll
+        for (int c = 0; c < 8; ++c) dst[c ^ (r & 7)] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&conv[stage]);
+        if (++stage == LG_STAGES) { stage = 0; phase ^= 1; }
+      }
+      const float nrm = sqrtf(ss);
+      const float inv = valid ? 1.f / fmaxf(nrm, kNormEps) : 0.f;
+      p.inv_norm[n0 + r] = inv;
+      if (valid && !(nrm > 0.f)) atomicOr(p.err, ERR_DEGENERATE);
+      mbar_wait(&inv_empty[acc], acc_phase ^ 1);
+      s_inv[acc * 128 + r] = inv;
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&inv_full[acc]);
+      if (++acc == LG_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  } else if (warp == LG_STORE_WARP) {
+    // ---------------------------------------------------------------- W_s store (bf16 tile -> global)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+      for (int kb = 0; kb < n_kb; ++kb) {
+        mbar_wait(&conv[stage], phase);
+        if (lane == 0) {
+          if (p.write_ws) {
+            tma_store_2d(&tmWs, smem + stage * LG_STAGE + LG_A_BYTES, kb * LG_BK, t * 128);
+            bulk_commit();
+            bulk_wait_read0();                      // smem read back: the stage may be refilled
+          }
+          mbar_arrive(&empty[stage]);
+        }
+        __syncwarp();
+        if (++stage == LG_STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    if (lane == 0) bulk_wait0();
+  } else {
+    // ---------------------------------------------------------------- epilogue
+    const int ew = warp - LG_EPI_WARP0;
+    const int lg = warp & 3;                 // TMEM lane quarter of this warp
+    const int row_in = lg * 32 + lane;
+    const int eset = ew >> 2;                // two sets of 4 warps: columns 64*eset .. +63
+    const float sl = p.s_log2e;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+      const int n0 = t * 128;
+      mbar_wait(&inv_full[acc], acc_phase);
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
+      const float* inv_t = s_inv + acc * 128;
+      float pm[2], ps[2];
+#pragma unroll
+      for (int ms = 0; ms < 2; ++ms) {
+        const int row = ms * 128 + row_in;
+        const bool rv = row < p.M;
+        const int tc = rv ? p.tcol[row] : -1;
+        float mx = -INFINITY, sum = 0.f;
+#pragma unroll 1
+        for (int c = eset * 2; c < eset * 2 + 2; ++c) {
+          uint32_t v[32];
+          tmem_ld32(tacc + ms * 128 + c * 32, v);
+          const int col0 = n0 + c * 32;
+          const float4* iv = reinterpret_cast<const float4*>(inv_t + c * 32);
+          __half2 h2[16];
+          float cf[32];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 s4 = iv[q];
+            h2[2 * q] = __floats2half2_rn(__uint_as_float(v[4 * q]) * s4.x, __uint_as_float(v[4 * q + 1]) * s4.y);
+            h2[2 * q + 1] =
+                __floats2half2_rn(__uint_as_float(v[4 * q + 2]) * s4.z, __uint_as_float(v[4 * q + 3]) * s4.w);
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float2 f = __half22float2(h2[i]);
+            cf[2 * i] = f.x;
+            cf[2 * i + 1] = f.y;
+          }
+          if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col0 + j >= k || col0 + j == tc) cf[j] = -INFINITY;
+          }
+          float q0 = cf[0], q1 = cf[1], q2 = cf[2], q3 = cf[3];
+#pragma unroll
+          for (int j = 4; j < 32; j += 4) {
+            q0 = fmaxf(q0, cf[j]); q1 = fmaxf(q1, cf[j + 1]); q2 = fmaxf(q2, cf[j + 2]); q3 = fmaxf(q3, cf[j + 3]);
+          }
+          const float nmx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
+          if (nmx > -INFINITY) {
+            const float nb = nmx * sl;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
+              s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
+              s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
+              s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+            }
+            sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
+            mx = nmx;
+          }
+          // class-major store, lane pairs exchanging halves: each 32-bit store covers rows (n, n+1) of one class
+          const bool odd = lane & 1;
+          __half* cb = p.cosv + (row & ~1);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const __half send = odd ? __low2half(h2[i]) : __high2half(h2[i]);
+            const unsigned short rcv = (unsigned short)__shfl_xor_sync(0xffffffffu, (int)__half_as_ushort(send), 1);
+            const __half other = __ushort_as_half(rcv);
+            const __half2 pr = odd ? __halves2half2(other, __high2half(h2[i])) : __halves2half2(__low2half(h2[i]), other);
+            if (row < p.ldm) *reinterpret_cast<__half2*>(cb + (int64_t)(col0 + 2 * i + (odd ? 1 : 0)) * p.ldm) = pr;
+          }
+        }
+        pm[ms] = mx;
+        ps[ms] = sum;
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) { mbar_arrive(&acc_empty[acc]); mbar_arrive(&inv_empty[acc]); }
+      float2* sp = s_part + acc * 256;
+      if (eset == 1) {
+#pragma unroll
+        for (int ms = 0; ms < 2; ++ms) sp[ms * 128 + row_in] = make_float2(pm[ms], ps[ms]);
+      }
+      asm volatile("bar.sync 4, %0;" ::"n"(32 * LG_EPI) : "memory");
+      if (eset == 0) {
+#pragma unroll
+        for (int ms = 0; ms < 2; ++ms) {
+          const int row = ms * 128 + row_in;
+          const float2 o = sp[ms * 128 + row_in];
+          const float m = fmaxf(pm[ms], o.x);
+          float l = 0.f;
+          if (m > -INFINITY)
+            l = (pm[ms] > -INFINITY ? ps[ms] * ex2_ftz((pm[ms] - m) * sl) : 0.f) +
+                (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
+          if (row < p.M)
+            p.partials[(int64_t)row * p.n_ltiles + t] = make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
+        }
+      }
+      if (++acc == LG_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  __syncthreads();
+  if (warp == LG_MMA_WARP) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+}  // namespace
+
+bool logits_gather_supported(const Sizes& sz) {
+  static const int forced = [] { const char* e = std::getenv("PFC_FUSED_GATHER"); return e ? std::atoi(e) : 1; }();
+  return forced != 0 && sz.M <= 256 && sz.d % LG_BK == 0 && sz.k_pad % 128 == 0;
+}
+
+int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
+                            __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
+                            MarginParams mp, __half* cosv, float2* partials, int* err, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_logits_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    attr = true;
+  }
+  const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  const CUtensorMap ws = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  LgParams p{};
+  p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.st = st; p.W = W; p.idx = idx; p.inv_norm = inv_norm; p.err = err;
+  p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
+  p.n_ltiles = sz.n_ltiles;
+  p.write_ws = write_ws ? 1 : 0;
+  const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
+  k_logits_gather<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
+  return 1;
+}
+
+}  // namespace pfc

@@ -133,15 +133,16 @@ int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float*
                     float* metrics, int* err, cudaStream_t s);
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
-                        float* dotw /* per-class w_hat . dW_hat, or NULL */, cudaStream_t s);
+                        float* dotw /* per-class w_hat . dW_hat, or NULL */,
+                        const float* gsc /* R25: per-class 1/||w|| folded into G, or NULL */, cudaStream_t s);
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
                           float* grad_x, cudaStream_t s);
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
-               const SamplerState* st, const float* lr_dev, float mu, float lambda, cudaStream_t s);
+               const SamplerState* st, const float* lr_dev, float mu, float lambda, int gsc, cudaStream_t s);
 int launch_set_scalar(float* dst, float v, cudaStream_t s);
 int launch_advance_step(uint64_t* step_dev, cudaStream_t s);
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
-                    const SamplerState* st, float* out, cudaStream_t s);
+                    const SamplerState* st, float* out, int gsc, cudaStream_t s);
 
 // loopback collectives: dst[r][i] = op_{q ascending} src[q][src_off + i] for r < ndst (op 0 = sum, 1 = max)
 constexpr int kMaxLoopback = 16;
@@ -167,6 +168,11 @@ int64_t dx_split_ws_floats(const Sizes& sz);
 int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
                      const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
                      cudaStream_t s);
+// logits_gather.cu — K5 + K6 fused (M <= 256): sampled fp32 W rows -> norms, bf16 W_s (un-normalised), logits
+bool logits_gather_supported(const Sizes& sz);
+int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
+                            __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
+                            MarginParams mp, __half* cosv, float2* partials, int* err, cudaStream_t s);
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,
                  float* dXh, float* split_ws, cudaStream_t s);
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
@@ -175,8 +181,14 @@ int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* X
 // v <- mu v + g + lambda w, w <- w - lr v, written straight into the W and V shard rows.
 struct SgdArgs {
   float* W; float* V; const int32_t* idx; const float* inv_norm; const float* dotw; const float* lr; float mu, lambda;
+  int gsc;   // R25: G carries 1/||w|| (dW_hat tile is already scaled)
 };
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& a, cudaStream_t s);
+// dwx.cu — K9 + K11 + K12 fused for the train step (M <= 256, R25 scaling): dW + SGD update + dX_hat partials
+bool dwx_supported(const Sizes& sz);
+int64_t dwx_ws_floats(const Sizes& sz);
+int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                  const SgdArgs& sa, float* ws, float* dXh, cudaStream_t s);
 
 }  // namespace pfc

@@ -293,7 +293,7 @@ template <bool BF16, bool DOT>
 __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int ldm, const void* __restrict__ cosv,
                                                       const float* __restrict__ lse, const SamplerState* st,
                                                       MarginParams mp, void* __restrict__ G,
-                                                      float* __restrict__ dotw) {
+                                                      float* __restrict__ dotw, const float* __restrict__ gsc) {
   extern __shared__ float s_off[];            // transposed: pos(n) = (n % 8) * (ldm / 8) + n / 8
   const float L2E = 1.4426950408889634f;
   const float lgs = log2f(mp.s / (float)M);
@@ -315,10 +315,12 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
 #pragma unroll
     for (int i = 0; i < 8; ++i) off[i] = act ? s_off[i * l8 + lane] : INFINITY;
     for (int64_t jb = w0; jb < k_pad; jb += U * nw) {
-      float c[U][8];
+      float c[U][8], sc[U];
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t j = jb + u * nw;
+        sc[u] = 1.f;                             // R25: G' = G / ||w_j|| when W_s holds un-normalised rows
+        if (gsc && j < k) sc[u] = __ldg(gsc + j);
         if (act && j < k) load8<BF16>(cosv, j * ldm + n0, c[u]);
       }
 #pragma unroll
@@ -332,7 +334,7 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
           for (int i = 0; i < 8; ++i) {
             // p <= 1 for every non-target entry (LSE >= z_j); the clamp only bounds the provisional value at
             // the target column (margin not applied there), which k_softmax_grad_targets replaces exactly
-            g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -off[i]), lgs));
+            g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -off[i]), lgs)) * sc[u];
             if (DOT) d = fmaf(g[i], c[u][i], d);
           }
         } else {
@@ -351,6 +353,7 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
     // flight; the row offsets come from the transposed (conflict-free) shared array
     for (int64_t j = w0; j < k_pad; j += nw) {
       const bool valid = j < k;
+      const float sc = gsc && valid ? gsc[j] : 1.f;
       float d = 0.f;
       for (int it = 0; it < nit; it += U) {
         float c[U][8];
@@ -367,7 +370,7 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
           if (valid) {
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
-              g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -s_off[i * l8 + lane + 32 * (it + u)]), lgs));
+              g[i] = ex2_ftz(fminf(fmaf(c[u][i], sl, -s_off[i * l8 + lane + 32 * (it + u)]), lgs)) * sc;
               if (DOT) d = fmaf(g[i], c[u][i], d);
             }
           } else {
@@ -391,7 +394,7 @@ template <bool BF16, bool DOT>
 __global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ cosv, const float* __restrict__ lse,
                                        const float* __restrict__ gt, const int32_t* __restrict__ tcol,
                                        const float* __restrict__ ct, MarginParams mp, void* __restrict__ G,
-                                       float* __restrict__ dotw) {
+                                       float* __restrict__ dotw, const float* __restrict__ gsc) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= M) return;
   const int j = tcol[n];
@@ -401,9 +404,10 @@ __global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ 
   const int64_t e = (int64_t)j * ldm + n;
   const float cst = BF16 ? __half2float(((const __half*)cosv)[e]) : ((const float*)cosv)[e];
   const float lgs = log2f(gs);
-  const float g_old = ex2_ftz(fminf(fmaf(cst, mp.s * L2E, -(lse[n] * L2E - lgs)), lgs));   // as k_softmax_grad
+  const float sc = gsc ? gsc[j] : 1.f;
+  const float g_old = ex2_ftz(fminf(fmaf(cst, mp.s * L2E, -(lse[n] * L2E - lgs)), lgs)) * sc;   // as k_softmax_grad
   const float c_t = ct[n];
-  const float g_new = gs * gt[n] * margin_dphi(mp, c_t);
+  const float g_new = gs * gt[n] * margin_dphi(mp, c_t) * sc;
   if (BF16) ((__nv_bfloat16*)G)[e] = __float2bfloat16_rn(g_new);
   else ((float*)G)[e] = g_new;
   if (DOT) atomicAdd(&dotw[j], g_new * c_t - g_old * cst);
@@ -427,7 +431,7 @@ __global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, co
 template <bool UPDATE>
 __global__ void k_sgd(int64_t k_pad, int d, float* __restrict__ W, float* __restrict__ V, const float* __restrict__ dWh,
                       const int32_t* __restrict__ idx, const float* __restrict__ inv_norm, const SamplerState* st,
-                      const float* __restrict__ lr_dev, float mu, float lambda, float* __restrict__ out) {
+                      const float* __restrict__ lr_dev, float mu, float lambda, float* __restrict__ out, int gsc) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const float lr = UPDATE ? *lr_dev : 0.f;
   const int lane = threadIdx.x & 31;
@@ -443,14 +447,15 @@ __global__ void k_sgd(int64_t k_pad, int d, float* __restrict__ W, float* __rest
     dot += (w.x * g.x + w.y * g.y + w.z * g.z + w.w * g.w);
   }
   dot = warp_sum(dot) * inv;  // w_hat . dw_hat
+  const float oi = gsc ? 1.f : inv;   // R25: dWh = G'^T X_hat already carries 1/||w||
   for (int c = lane * 4; c < d; c += 128) {
     float4 w = *reinterpret_cast<const float4*>(wr + c);
     float4 g = *reinterpret_cast<const float4*>(gr + c);
     float4 gg;
-    gg.x = (g.x - w.x * inv * dot) * inv;
-    gg.y = (g.y - w.y * inv * dot) * inv;
-    gg.z = (g.z - w.z * inv * dot) * inv;
-    gg.w = (g.w - w.w * inv * dot) * inv;
+    gg.x = (g.x - w.x * inv * dot) * oi;
+    gg.y = (g.y - w.y * inv * dot) * oi;
+    gg.z = (g.z - w.z * inv * dot) * oi;
+    gg.w = (g.w - w.w * inv * dot) * oi;
     if (UPDATE) {
       float* vr = V + j * d;
       float4 v = *reinterpret_cast<const float4*>(vr + c);
@@ -517,7 +522,7 @@ int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float*
 
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
-                        float* dotw, cudaStream_t s) {
+                        float* dotw, const float* gsc, cudaStream_t s) {
   const size_t smem = (size_t)sz.M_pad * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -544,19 +549,19 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
   const unsigned tg = (unsigned)((sz.M + 255) / 256);
   if (bf16) {
     if (dotw) {
-      k_softmax_grad<true, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
-      k_softmax_grad_targets<true, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+      k_softmax_grad<true, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
+      k_softmax_grad_targets<true, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
     } else {
-      k_softmax_grad<true, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
-      k_softmax_grad_targets<true, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+      k_softmax_grad<true, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
+      k_softmax_grad_targets<true, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
     }
   } else {
     if (dotw) {
-      k_softmax_grad<false, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
-      k_softmax_grad_targets<false, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+      k_softmax_grad<false, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
+      k_softmax_grad_targets<false, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
     } else {
-      k_softmax_grad<false, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw);
-      k_softmax_grad_targets<false, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw);
+      k_softmax_grad<false, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
+      k_softmax_grad_targets<false, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
     }
   }
   return 2;
@@ -569,9 +574,9 @@ int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_loc
 }
 
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
-               const SamplerState* st, const float* lr_dev, float mu, float lambda, cudaStream_t s) {
+               const SamplerState* st, const float* lr_dev, float mu, float lambda, int gsc, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
-  k_sgd<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, dWh, idx, inv_norm, st, lr_dev, mu, lambda, nullptr);
+  k_sgd<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, dWh, idx, inv_norm, st, lr_dev, mu, lambda, nullptr, gsc);
   return 1;
 }
 
@@ -591,10 +596,10 @@ int launch_advance_step(uint64_t* step_dev, cudaStream_t s) {
 }
 
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
-                    const SamplerState* st, float* out, cudaStream_t s) {
+                    const SamplerState* st, float* out, int gsc, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
   k_sgd<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, const_cast<float*>(W), nullptr, dWh, idx, inv_norm, st, nullptr,
-                                    0.f, 0.f, out);
+                                    0.f, 0.f, out, gsc);
   return 1;
 }
 
