@@ -223,6 +223,14 @@ const char* pfc_profile_section(int32_t i);
 /* Number of kernels this library launched since init (each launch counted once). */
 int64_t pfc_launch_count(const pfc_ctx* ctx);
 
+/* Kernel path chosen at init for this configuration (bit set = used), for reporting: */
+#define PFC_PATH_TENSOR_CORES 1u  /* tcgen05 contractions (bf16 precision on sm_100) */
+#define PFC_PATH_FUSED_GATHER 2u  /* gather + bf16 + norms + logits in one kernel (global batch M <= 256):
+                                     profile section 3 then holds it and section 2 only the target cosines */
+#define PFC_PATH_FUSED_DWX    4u  /* train step: dW + momentum SGD + dX_hat in one kernel (section 6; 8 empty) */
+/* Returns the PFC_PATH_* bits (0 for a NULL context). */
+uint32_t pfc_path_flags(const pfc_ctx* ctx);
+
 /* Library version string. */
 const char* pfc_version(void);
 

@@ -17,7 +17,8 @@ __all__ = ["PartialFC", "load_library", "unique_id", "group_forward_backward", "
            "PRECISIONS"]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libpfc.so")
+# PFC_LIB: an alternative build of the same library (A/B timing of kernel variants); default the in-tree build
+LIB_PATH = os.environ.get("PFC_LIB") or os.path.join(_HERE, "_lib", "libpfc.so")
 
 MARGINS = {"none": 0, "arcface": 1, "cosface": 2}
 PRECISIONS = {"fp32": 0, "bf16": 1}
@@ -30,7 +31,7 @@ STATUS = {0: "PFC_OK", 1: "PFC_ERR_CONFIG", 2: "PFC_ERR_CONTRACT", 3: "PFC_ERR_D
 EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pfc_forward_backward",
            "pfc_forward_backward_host", "pfc_step", "pfc_shard_range", "pfc_sizes", "pfc_param_ptrs",
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
-           "pfc_launch_count", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
+           "pfc_launch_count", "pfc_path_flags", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
            "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section", "pfc_train_step", "pfc_train_step_host",
            "pfc_group_train_step", "pfc_get_metrics"]
 PROF_SECTIONS = 10
@@ -83,6 +84,7 @@ def load_library(path=LIB_PATH):
         "pfc_set_step": (st, [VP, U64]),
         "pfc_check": (st, [VP]),
         "pfc_launch_count": (I64, [VP]),
+        "pfc_path_flags": (ctypes.c_uint32, [VP]),
         "pfc_version": (ctypes.c_char_p, []),
         "pfc_train_step": (st, [VP, VP, VP, VP, VP, F, VP]),
         "pfc_get_metrics": (st, [VP, P(F), P(F)]),
@@ -278,6 +280,12 @@ class PartialFC:
 
     def launch_count(self):
         return int(self._lib.pfc_launch_count(self._h))
+
+    PATH_TENSOR_CORES, PATH_FUSED_GATHER, PATH_FUSED_DWX = 1, 2, 4
+
+    def path_flags(self):
+        """PFC_PATH_* bits of the kernel path chosen at init (include/pfc.h)."""
+        return int(self._lib.pfc_path_flags(self._h))
 
 
 def _stream_ptr(stream):

@@ -798,6 +798,12 @@ pfc_status pfc_set_step(pfc_ctx* c, uint64_t step) {
 
 int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
 
+uint32_t pfc_path_flags(const pfc_ctx* c) {
+  if (!c) return 0u;
+  return (c->use_tc ? PFC_PATH_TENSOR_CORES : 0u) | (c->fused_gather ? PFC_PATH_FUSED_GATHER : 0u) |
+         (c->use_dwx ? PFC_PATH_FUSED_DWX : 0u);
+}
+
 static const char* kSectionNames[PFC_PROF_SECTIONS] = {
     "normalize_x", "sampler", "gather_w", "logits_gemm", "row_lse", "softmax_grad", "dx_gemm", "xnorm_backward",
     "dw_gemm", "sgd"};

@@ -209,7 +209,11 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
 #pragma unroll
         for (int it = 0; it < 8; ++it) {
           jr[it] = s_rowj[ew * 16 + r0 + it];
-          if (jr[it] >= 0) wv[it] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[it] * p.d + col);
+          if (jr[it] >= 0) {
+            wv[it] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[it] * p.d + col);
+            // the V row segment into L2 now: the update (3) then reads both W and V from L2
+            if ((lane & 7) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.sgd.V + (int64_t)jr[it] * p.d + col));
+          }
         }
         const int hc = lane >> 4, cq = lane & 15;
 #pragma unroll
