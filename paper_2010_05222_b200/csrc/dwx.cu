@@ -10,11 +10,11 @@
 // CTA b owns the 128-column d-tile b / gper and the class tiles g, g + gper, ... (g = b % gper); its dX_hat
 // partial for that d-tile stays in TMEM for the whole kernel and is written once to the split workspace, reduced
 // over g by k_splitk_reduce (deterministic order).
-//   warp 0    TMA producer: the class tile's G' rows (all M_pad batch columns) and the X_hat chunks (64 batch rows
-//             x 128 columns, 4-stage ring, prefetched a tile ahead)
-//   warp 1    MMA issuer: dW(t) into D1[t % 2], then dX(t) into D2 once the epilogue has staged bf16 w_old(t)
-//   warps 2-9 epilogue per tile: (1) bf16 w_old tile (first read of the W rows; it does not need D1, so dX(t) and
-//             the next tile's G' load overlap the rest), (2) D1 -> smem, (3) coalesced W / V row updates
+//   warp 0    TMA producer: the dW operands (G' and X_hat 64-batch chunks, 2-stage ring) and, a tile behind, a
+//             second copy of the whole G' tile (an L2 hit) for the dX contraction
+//   warp 1    MMA issuer: dW(t) into D1[t % 2], then dX(t - 1) into D2 once the epilogue has staged bf16 w_old(t - 1)
+//   warps 2-9 epilogue per tile: D1 -> smem, coalesced W / V row updates (rows L2-prefetched a tile ahead) that
+//             also stage the old w as the bf16 dX operand
 #include <cuda_bf16.h>
 #include <algorithm>
 #include <cstdlib>
@@ -30,11 +30,12 @@ constexpr int DX_THREADS = 64 + 32 * DX_EPI;
 constexpr int G_CHUNK = 128 * 64 * 2;       // 128 classes x 64 batch columns (bf16, 128-byte swizzle)
 constexpr int G_BUF = 4 * G_CHUNK;          // M_pad <= 256
 constexpr int X_CHUNK = 64 * 128 * 2;       // 64 batch rows x 128 columns (two 64-column swizzled halves)
-constexpr int X_STAGES = 4;
+constexpr int R_STAGES = 2;                 // dW operand ring: (G' chunk, X_hat chunk) per stage
+constexpr int R_STAGE = G_CHUNK + X_CHUNK;
 constexpr int WB_HALF = 128 * 128;          // 128 classes x 64 columns bf16
-constexpr int OFF_G = 0;
-constexpr int OFF_X = OFF_G + G_BUF;
-constexpr int OFF_WB = OFF_X + X_STAGES * X_CHUNK;
+constexpr int OFF_R = 0;
+constexpr int OFF_G = OFF_R + R_STAGES * R_STAGE;   // the dX operand: the whole G' tile, loaded a second time
+constexpr int OFF_WB = OFF_G + G_BUF;
 constexpr int OFF_ST = OFF_WB + 2 * WB_HALF;
 constexpr int OFF_AUX = OFF_ST + 128 * 128 * 4;
 constexpr int DX_SMEM = OFF_AUX + 256 + 3 * 128 * 4 + 1024;
@@ -57,15 +58,15 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
     k_dwx(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX, DwxParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sR = smem + OFF_R;
   uint8_t* sG = smem + OFF_G;
-  uint8_t* sX = smem + OFF_X;
   uint8_t* sWb = smem + OFF_WB;
   float4* s_tile = reinterpret_cast<float4*>(smem + OFF_ST);     // [128 rows][32 float4], XOR-swizzled
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + OFF_AUX);
-  uint64_t* g_full = bars;
+  uint64_t* g_full = bars;            // dX copy of the G' tile
   uint64_t* g_empty = bars + 1;
-  uint64_t* x_full = bars + 2;        // [X_STAGES]
-  uint64_t* x_empty = bars + 6;       // [X_STAGES]
+  uint64_t* x_full = bars + 2;        // [R_STAGES] dW operand ring
+  uint64_t* x_empty = bars + 6;       // [R_STAGES]
   uint64_t* d1_full = bars + 10;      // [2]
   uint64_t* d1_empty = bars + 12;     // [2]
   uint64_t* wb_full = bars + 14;
@@ -86,7 +87,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(g_full, 1); mbar_init(g_empty, 1);
-    for (int i = 0; i < X_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < R_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d1_full[i], 1); mbar_init(&d1_empty[i], DX_EPI); }
     mbar_init(wb_full, DX_EPI);
     mbar_init(wb_empty, 1);
@@ -110,19 +111,25 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
     if (lane == 0) {
       int xs = 0;
       uint32_t xph = 0;
+      auto load_gdx = [&](int i) {     // the dX operand copy of tile i's G' (an L2 hit: read for dW(i) before)
+        mbar_wait(g_empty, (uint32_t)((i & 1) ^ 1));       // dX(i - 1) has read the previous copy
+        mbar_expect_tx(g_full, (uint32_t)(nkb * G_CHUNK));
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sG + kb * G_CHUNK, &tmG, g_full, kb * 64, (g + i * p.gper) * 128);
+      };
       for (int i = 0; i < ntl; ++i) {
         const int ct = g + i * p.gper;
-        mbar_wait(g_empty, (uint32_t)((i & 1) ^ 1));         // dX(t - 1) has read the previous G' tile
-        mbar_expect_tx(g_full, (uint32_t)(nkb * G_CHUNK));
-        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sG + kb * G_CHUNK, &tmG, g_full, kb * 64, ct * 128);
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&x_empty[xs], xph ^ 1);
-          mbar_expect_tx(&x_full[xs], (uint32_t)X_CHUNK);
-          tma_load_2d(sX + xs * X_CHUNK, &tmX, &x_full[xs], n0, kb * 64);
-          tma_load_2d(sX + xs * X_CHUNK + X_CHUNK / 2, &tmX, &x_full[xs], n0 + 64, kb * 64);
-          if (++xs == X_STAGES) { xs = 0; xph ^= 1; }
+          mbar_expect_tx(&x_full[xs], (uint32_t)R_STAGE);
+          uint8_t* st = sR + xs * R_STAGE;
+          tma_load_2d(st, &tmG, &x_full[xs], kb * 64, ct * 128);
+          tma_load_2d(st + G_CHUNK, &tmX, &x_full[xs], n0, kb * 64);
+          tma_load_2d(st + G_CHUNK + X_CHUNK / 2, &tmX, &x_full[xs], n0 + 64, kb * 64);
+          if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
         }
+        if (i > 0) load_gdx(i - 1);
       }
+      if (ntl > 0) load_gdx(ntl - 1);
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer
@@ -132,6 +139,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
     uint32_t xph = 0, aph = 0;
     auto dx = [&](int i) {      // D2 += G'(tile i) bf16(w_old(tile i)), then release both operands
       mbar_wait(wb_full, (uint32_t)(i & 1));
+      mbar_wait(g_full, (uint32_t)(i & 1));
       tc_fence_after();
       if (lane == 0) {
         const uint32_t ga = smem_u32(sG), wa = smem_u32(sWb);
@@ -146,14 +154,13 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       __syncwarp();
     };
     for (int i = 0; i < ntl; ++i) {
-      mbar_wait(g_full, (uint32_t)(i & 1));
       mbar_wait(&d1_empty[acc], aph ^ 1);
       tc_fence_after();
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&x_full[xs], xph);
         tc_fence_after();
         if (lane == 0) {
-          const uint32_t ga = smem_u32(sG + kb * G_CHUNK), xa = smem_u32(sX + xs * X_CHUNK);
+          const uint32_t ga = smem_u32(sR + xs * R_STAGE), xa = ga + G_CHUNK;
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
             tc_mma(tmem_base + acc * 128, make_desc(ga + kk * 32, 16, 1024), make_desc(xa + kk * 2048, X_CHUNK / 2, 1024),
@@ -161,13 +168,14 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
           tc_commit(&x_empty[xs]);
         }
         __syncwarp();
-        if (++xs == X_STAGES) { xs = 0; xph ^= 1; }
+        if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
       }
       if (lane == 0) tc_commit(&d1_full[acc]);
       __syncwarp();
       if (++acc == 2) { acc = 0; aph ^= 1; }
-      dx(i);          // the epilogue stages bf16 w_old(t) before it needs D1(t)
+      if (i > 0) dx(i - 1);     // bf16 w_old(t - 1) is staged by the epilogue's update of tile t - 1
     }
+    if (ntl > 0) dx(ntl - 1);
     if (lane == 0) {
       if (ntl > 0) tc_commit(d2_full);
       else mbar_arrive(d2_full);
@@ -199,35 +207,6 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
           if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
         }
       }
-      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
-      // (1) bf16 w_old tile for dX(t): independent of D1, so dX(t) and the next tile's G' load overlap (3)
-      mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));                       // dX(t - 1) has read the bf16 tile
-#pragma unroll 1
-      for (int r0 = 0; r0 < 16; r0 += 8) {
-        float4 wv[8];
-        int32_t jr[8];
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          jr[it] = s_rowj[ew * 16 + r0 + it];
-          if (jr[it] >= 0) {
-            wv[it] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[it] * p.d + col);
-            // the V row segment into L2 now: the update (3) then reads both W and V from L2
-            if ((lane & 7) == 0) asm volatile("prefetch.global.L2 [%0];" ::"l"(p.sgd.V + (int64_t)jr[it] * p.d + col));
-          }
-        }
-        const int hc = lane >> 4, cq = lane & 15;
-#pragma unroll
-        for (int it = 0; it < 8; ++it) {
-          const int rr = ew * 16 + r0 + it;
-          const uint2 wb = jr[it] >= 0 ? make_uint2(pack_bf16x2(wv[it].x, wv[it].y), pack_bf16x2(wv[it].z, wv[it].w))
-                                       : make_uint2(0u, 0u);
-          // MN-major swizzled B tile: half hc, class row rr, columns cq*4 .. +3 (8 bytes)
-          *reinterpret_cast<uint2*>(sWb + hc * WB_HALF + rr * 128 + ((((cq >> 1) ^ (rr & 7)) << 4) | ((cq & 1) << 3))) = wb;
-        }
-      }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(wb_full);
       // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
       mbar_wait(&d1_full[acc], aph);
       tc_fence_after();
@@ -249,7 +228,9 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       if (lane == 0) mbar_arrive(&d1_empty[acc]);
       if (++acc == 2) { acc = 0; aph ^= 1; }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
-      // (3) momentum-SGD row updates (w re-read hits L2), 8 rows in flight per lane
+      // (3) momentum-SGD row updates (rows L2-prefetched a tile ahead), 8 rows in flight per lane; the old w
+      // also goes to the bf16 dX operand tile, once dX(t - 1) has read the previous one
+      mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));
 #pragma unroll 1
       for (int r0 = 0; r0 < 16; r0 += 8) {
         float4 wv[8], mv[8];
@@ -265,6 +246,12 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           const int rr = ew * 16 + r0 + r;
+          {
+            const uint2 wb = jr[r] >= 0 ? make_uint2(pack_bf16x2(wv[r].x, wv[r].y), pack_bf16x2(wv[r].z, wv[r].w))
+                                        : make_uint2(0u, 0u);
+            const int hc = lane >> 4, cq = lane & 15;   // MN-major swizzled B tile: half hc, row rr, 8 bytes
+            *reinterpret_cast<uint2*>(sWb + hc * WB_HALF + rr * 128 + ((((cq >> 1) ^ (rr & 7)) << 4) | ((cq & 1) << 3))) = wb;
+          }
           if (jr[r] >= 0) {
             const float inv = s_inv[rr], rad = s_rad[rr] * inv;
             const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
@@ -289,6 +276,9 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
           }
         }
       }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wb_full);
     }
     // dX_hat partial of this CTA (zeros when it had no class tile) -> split workspace
     mbar_wait(d2_full, 0);
