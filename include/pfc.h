@@ -194,6 +194,13 @@ pfc_status pfc_get_metrics(pfc_ctx* ctx, float* loss_host, float* ca_pcc_host);
 pfc_status pfc_get_step(const pfc_ctx* ctx, uint64_t* step);
 pfc_status pfc_set_step(pfc_ctx* ctx, uint64_t step);
 
+/* Checkpoint / resume: copy the whole shard state to or from host memory, synchronising the
+ * device first. W_host, V_host: [C_local][d] float32 (row-major, C_local from pfc_shard_range), either may be NULL
+ * to skip that tensor; step: the step counter (keys the sampler), NULL to skip. set_state also clears a pending
+ * pfc_step. A resumed context continues bit-identically to the one the state was taken from. */
+pfc_status pfc_get_state(pfc_ctx* ctx, float* W_host, float* V_host, uint64_t* step);
+pfc_status pfc_set_state(pfc_ctx* ctx, const float* W_host, const float* V_host, const uint64_t* step);
+
 /* Synchronises the context's last stream and returns the sticky device error (PFC_OK if none). */
 pfc_status pfc_check(pfc_ctx* ctx);
 

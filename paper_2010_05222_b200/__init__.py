@@ -31,7 +31,7 @@ STATUS = {0: "PFC_OK", 1: "PFC_ERR_CONFIG", 2: "PFC_ERR_CONTRACT", 3: "PFC_ERR_D
 EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pfc_forward_backward",
            "pfc_forward_backward_host", "pfc_step", "pfc_shard_range", "pfc_sizes", "pfc_param_ptrs",
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
-           "pfc_launch_count", "pfc_path_flags", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
+           "pfc_launch_count", "pfc_path_flags", "pfc_get_state", "pfc_set_state", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
            "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section", "pfc_train_step", "pfc_train_step_host",
            "pfc_group_train_step", "pfc_get_metrics"]
 PROF_SECTIONS = 10
@@ -85,6 +85,8 @@ def load_library(path=LIB_PATH):
         "pfc_check": (st, [VP]),
         "pfc_launch_count": (I64, [VP]),
         "pfc_path_flags": (ctypes.c_uint32, [VP]),
+        "pfc_get_state": (ctypes.c_int, [VP, VP, VP, VP]),
+        "pfc_set_state": (ctypes.c_int, [VP, VP, VP, VP]),
         "pfc_version": (ctypes.c_char_p, []),
         "pfc_train_step": (st, [VP, VP, VP, VP, VP, F, VP]),
         "pfc_get_metrics": (st, [VP, P(F), P(F)]),
@@ -266,6 +268,32 @@ class PartialFC:
 
     def check(self):
         self._check(self._lib.pfc_check(self._h))
+
+    def get_state(self):
+        """Checkpoint: (W, V, step) of this shard as host numpy arrays ([C_local, d] float32) and an int."""
+        import numpy as np
+        W = np.empty((self.shard_size, self.dim), dtype=np.float32)
+        V = np.empty_like(W)
+        st = ctypes.c_uint64()
+        self._check(self._lib.pfc_get_state(self._h, W.ctypes.data, V.ctypes.data, ctypes.byref(st)))
+        return W, V, st.value
+
+    def set_state(self, W=None, V=None, step=None):
+        """Resume: load any of W, V ([C_local, d] float32 host arrays) and the step counter."""
+        import numpy as np
+        ptr = []
+        for a in (W, V):
+            if a is None:
+                ptr.append(None)
+            else:
+                a = np.ascontiguousarray(a, dtype=np.float32)
+                if a.shape != (self.shard_size, self.dim):
+                    raise ValueError(f"state array must be {(self.shard_size, self.dim)}, got {a.shape}")
+                ptr.append(a)
+        st = ctypes.c_uint64(int(step)) if step is not None else None
+        self._check(self._lib.pfc_set_state(self._h, ptr[0].ctypes.data if ptr[0] is not None else None,
+                                            ptr[1].ctypes.data if ptr[1] is not None else None,
+                                            ctypes.byref(st) if st is not None else None))
 
     def profile(self, enable=True):
         """Record CUDA events between the kernels of every following step (pfc_profile_enable)."""

@@ -796,6 +796,30 @@ pfc_status pfc_set_step(pfc_ctx* c, uint64_t step) {
   return PFC_OK;
 }
 
+pfc_status pfc_get_state(pfc_ctx* c, float* W_host, float* V_host, uint64_t* step) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  const size_t bytes = (size_t)c->sz.C_local * c->sz.d * sizeof(float);
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  if (W_host) CUDA_TRY(c, cudaMemcpy(W_host, c->W, bytes, cudaMemcpyDeviceToHost));
+  if (V_host) CUDA_TRY(c, cudaMemcpy(V_host, c->V, bytes, cudaMemcpyDeviceToHost));
+  if (step) *step = c->step;
+  return device_error(c);
+}
+
+pfc_status pfc_set_state(pfc_ctx* c, const float* W_host, const float* V_host, const uint64_t* step) {
+  if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
+  const size_t bytes = (size_t)c->sz.C_local * c->sz.d * sizeof(float);
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  if (W_host) CUDA_TRY(c, cudaMemcpy(c->W, W_host, bytes, cudaMemcpyHostToDevice));
+  if (V_host) CUDA_TRY(c, cudaMemcpy(c->V, V_host, bytes, cudaMemcpyHostToDevice));
+  if (step) {
+    CUDA_TRY(c, cudaMemcpy(c->step_dev, step, sizeof(*step), cudaMemcpyHostToDevice));
+    c->step = *step;
+  }
+  c->fb_done = false;
+  return PFC_OK;
+}
+
 int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
 
 uint32_t pfc_path_flags(const pfc_ctx* c) {

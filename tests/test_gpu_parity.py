@@ -334,6 +334,41 @@ def test_device_errors_are_reported():
     layer.close()
 
 
+def test_checkpoint_resume_continues_identically():
+    """pfc_get_state / pfc_set_state: a context resumed from a checkpoint of another one
+    (W, V, step counter) samples the same classes and produces the same losses, gradients and parameters."""
+    C, d, B = 20000, 256, 64
+    a = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=9)
+    b = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=9, wseed=5)   # different init: all from the state
+    ys = [synth.make_labels(8, i, 1, B, C)[0] for i in range(4)]
+    xs = [synth.make_features(8, i, 1, B, d)[0] for i in range(4)]
+    gx = torch.empty(B, d, device="cuda")
+    loss = torch.zeros(1, device="cuda")
+
+    def run(layer, i):
+        layer.train_step(torch.from_numpy(xs[i]).cuda(), torch.from_numpy(ys[i]).cuda(), gx, loss, lr=0.1)
+        torch.cuda.synchronize()
+        return loss.item(), gx.cpu().numpy().copy(), layer.sampled()
+
+    for i in range(2):
+        run(a, i)
+    W, V, step = a.get_state()
+    assert step == 2 and np.abs(V).max() > 0
+    ref = [run(a, i) for i in (2, 3)]
+    b.set_state(W, V, step)
+    got = [run(b, i) for i in (2, 3)]
+    for (la, ga, ia), (lb, gb, ib) in zip(ref, got):
+        assert np.array_equal(ia, ib)
+        assert abs(la - lb) <= 1e-6 * abs(la)
+        assert maxrel(gb, ga) <= 1e-5
+    Wa, Va, sa = a.get_state()
+    Wb, Vb, sb = b.get_state()
+    assert sa == sb == 4
+    assert maxrel(Wb, Wa) <= 1e-6 and maxrel(Vb, Va) <= 1e-5
+    a.close()
+    b.close()
+
+
 def test_cuda_graph_replay_matches_eager():
     """pfc_train_step on a capturable stream is captured once and replayed as a CUDA graph (device-side step
     counter and learning rate); results must match the eager launches on the legacy stream."""
