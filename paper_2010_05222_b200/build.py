@@ -35,6 +35,7 @@ def _compile(src, inc, verbose):
         return obj
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c", src, "-o", obj,
            "-I", inc, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
+    cmd += os.environ.get("PFC_NVCC_EXTRA", "").split()   # variant builds (A/B timing); empty by default
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

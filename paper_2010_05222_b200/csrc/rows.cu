@@ -289,6 +289,9 @@ __device__ __forceinline__ float ex2_ftz(float x) {
 // Every element as a non-target: Gc[j][n] = 2^min(c sl - off'_n, log2(s/M)) with off'_n = LSE_n log2 e -
 // log2(s/M) (the s/M factor folded into the exponent); padding rows have off' = +inf (their stored cosine is 0).
 // The target entries (one per row) are then rewritten by k_softmax_grad_targets.
+#ifndef PFC_K8_U
+#define PFC_K8_U 2
+#endif
 template <bool BF16, bool DOT>
 __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int ldm, const void* __restrict__ cosv,
                                                       const float* __restrict__ lse, const SamplerState* st,
@@ -305,7 +308,7 @@ __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int 
   const int lane = threadIdx.x & 31;
   const int64_t nw = (int64_t)gridDim.x * (blockDim.x >> 5);
   const int64_t w0 = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  constexpr int U = 2;
+  constexpr int U = PFC_K8_U;
   const int nit = (ldm + 255) / 256;
   if (nit == 1) {
     // one 8-row chunk per lane: its offsets stay in registers for the whole class loop, U classes in flight
