@@ -225,6 +225,41 @@ def test_fused_train_step_parity(case, precision):
         assert maxrel(Wn, Wnr) <= bound
 
 
+FUSED_SHAPES = [
+    # the fused train-step kernels (logits_gather.cu, dwx.cu) at the shapes their tiling distinguishes
+    (20000, 512, 200, 0.05, "arcface", 0.5, "init", 0.0),     # M = 200: ragged second M-half (M_pad = 256)
+    (12000, 256, 256, 0.1, "cosface", 0.4, "init", 0.0),      # M = 256 exactly, two 128-column d-tiles
+    (5000, 1024, 130, 0.2, "arcface", 0.5, "init", 0.0),      # d = 1024 (16 K-blocks, 8 d-tiles), M = 130
+    (7000, 128, 256, 0.3, "arcface", 0.5, "init", 0.0),       # d = 128: one d-tile, 148 class-tile groups
+]
+
+
+@pytest.mark.parametrize("case", FUSED_SHAPES, ids=_case_id)
+def test_fused_kernels_shapes(case):
+    """bf16 train step at M <= 256 runs the fused gather+logits and dW+SGD+dX kernels (path flags 7); two steps
+    against the oracle (loss, grad_x, updated W and V rows)."""
+    C, d, B = case[0], case[1], case[2]
+    probe = make_layer(C, d, B, case[3], case[4], case[5], "bf16")
+    assert probe.path_flags() == 7
+    probe.close()
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
+        assert abs(L - Lr) / abs(Lr) <= 1e-3
+        assert maxrel(gx, gxr) <= 2e-2
+        assert maxrel(Vn, Vnr) <= 2e-2
+        # W moves by lr * V: its error is lr times V's (the same derived bound as test_fused_train_step_parity)
+        assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
+def test_path_flags():
+    """PFC_PATH_* bits: fused kernels only for bf16 at M <= 256; fp32 runs the SIMT contractions."""
+    a = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "bf16")
+    b = make_layer(5000, 256, 257, 0.1, "arcface", 0.5, "bf16")
+    c = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "fp32")
+    assert (a.path_flags(), b.path_flags(), c.path_flags()) == (7, 1, 0)
+    for L in (a, b, c):
+        L.close()
+
+
 @pytest.mark.parametrize("case", TINY_CASES, ids=_case_id)
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_tiny_loss_regime(case, precision):
