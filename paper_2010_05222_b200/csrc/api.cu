@@ -272,7 +272,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->Y, M * 8);
   ALLOC(c->Xb, Mp * d * 2);
   ALLOC(c->bits, ((sz.C_local + 31) / 32) * 4);
-  ALLOC(c->keys, (size_t)sz.C_local * 4);
+  ALLOC(c->keys, (size_t)sz.ntiles_sel * kSelTile * 4);   // padded to whole compaction tiles (vector loads)
   ALLOC(c->hist, 5120 * 4);
   ALLOC(c->tile_cnt, (size_t)sz.ntiles_sel * 4 * 4);
   ALLOC(c->st, sizeof(SamplerState));
@@ -887,7 +887,7 @@ pfc_status pfc_sample_shard(int64_t C, int32_t world, int32_t rank, double r, ui
   cudaError_t e = cudaSuccess;
   auto A = [&](void** p, size_t b) { if (e == cudaSuccess) e = cudaMalloc(p, std::max<size_t>(b, 16)); };
   A((void**)&bits, ((sz.C_local + 31) / 32) * 4);
-  A((void**)&keys, sz.C_local * 4);
+  A((void**)&keys, (size_t)sz.ntiles_sel * kSelTile * 4);
   A((void**)&hist, 5120 * 4);
   A((void**)&tile, (size_t)sz.ntiles_sel * 16);
   A((void**)&err, 16);

@@ -117,9 +117,16 @@ __global__ void __launch_bounds__(kThreads) k_hist_pass2(int64_t C_local, int64_
   }
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t h = keys[j];
-    if ((h >> 21) == (uint32_t)b1 && !is_pos(bits, j)) atomicAdd(&sh[(h >> 10) & 0x7FF], 1);
+  // 4 consecutive keys per thread and iteration (the key array is padded to whole tiles), two in flight
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+#pragma unroll 2
+  for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; j0 < C_local; j0 += stride) {
+    const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
+    const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+    const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if ((hh[i] >> 21) == (uint32_t)b1 && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[(hh[i] >> 10) & 0x7FF], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 2048; i += blockDim.x)
@@ -138,42 +145,42 @@ __global__ void __launch_bounds__(kThreads) k_hist_pass3(int64_t C_local, const 
   if (blockIdx.x == 0 && threadIdx.x == 0) { st->prefix2 = pre; st->rem2 = rem2; }
   for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
-    const uint32_t h = keys[j];
-    if ((h >> 10) == pre && !is_pos(bits, j)) atomicAdd(&sh[h & 0x3FF], 1);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+#pragma unroll 2
+  for (int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4; j0 < C_local; j0 += stride) {
+    const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
+    const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+    const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if ((hh[i] >> 10) == pre && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[hh[i] & 0x3FF], 1);
   }
   __syncthreads();
   for (int i = threadIdx.x; i < 1024; i += blockDim.x)
     if (sh[i]) atomicAdd(&hist2[i], sh[i]);
 }
 
-// Flags of 4 consecutive classes j0..j0+3 (j0 % 4 == 0): definitely selected (positive, or key < T) and tied
-// (key == T, non-positive).
-__device__ __forceinline__ void flags4(int64_t j0, int64_t C_local, const uint32_t* bits, const uint32_t* keys,
-                                       bool none, uint32_t T, bool (&def)[4], bool (&tie)[4]) {
-  if (j0 + 3 < C_local) {
-    const uint4 h = *reinterpret_cast<const uint4*>(keys + j0);
-    const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
-    const uint32_t hh[4] = {h.x, h.y, h.z, h.w};
+// Flags of the 32 consecutive classes j0 .. j0+31 (j0 % 32 == 0) of one thread as bit masks: definitely selected
+// (positive, or key < T) and tied (key == T, non-positive); classes >= C_local have neither.
+__device__ __forceinline__ void flags32(int64_t j0, int64_t C_local, const uint32_t* bits, const uint32_t* keys,
+                                        bool none, uint32_t T, uint32_t& def, uint32_t& tie) {
+  def = 0u; tie = 0u;
+  if (j0 >= C_local) return;
+  const uint32_t pw = __ldg(&bits[j0 >> 5]);
+  const uint32_t valid = C_local - j0 >= 32 ? 0xFFFFFFFFu : ((1u << (C_local - j0)) - 1u);
+  uint32_t lt = 0u, eq = 0u;
+  if (!none) {
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const bool p = (pw >> i) & 1u;
-      def[i] = p || (!none && hh[i] < T);
-      tie[i] = !p && !none && hh[i] == T;
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t j = j0 + i;
-      def[i] = false; tie[i] = false;
-      if (j < C_local) {
-        const bool p = is_pos(bits, j);
-        const uint32_t h = keys[j];
-        def[i] = p || (!none && h < T);
-        tie[i] = !p && !none && h == T;
-      }
+    for (int q = 0; q < 8; ++q) {
+      const uint4 h = *reinterpret_cast<const uint4*>(keys + j0 + 4 * q);
+      lt |= (uint32_t)(h.x < T) << (4 * q) | (uint32_t)(h.y < T) << (4 * q + 1) | (uint32_t)(h.z < T) << (4 * q + 2) |
+            (uint32_t)(h.w < T) << (4 * q + 3);
+      eq |= (uint32_t)(h.x == T) << (4 * q) | (uint32_t)(h.y == T) << (4 * q + 1) | (uint32_t)(h.z == T) << (4 * q + 2) |
+            (uint32_t)(h.w == T) << (4 * q + 3);
     }
   }
+  def = (pw | lt) & valid;
+  tie = eq & ~pw & valid;
 }
 
 // Block-wide exclusive scan of small per-thread counts (256 threads); returns the prefix, sets the total.
@@ -214,14 +221,9 @@ __global__ void __launch_bounds__(kThreads) k_tile_counts(int64_t C_local, const
     if (blockIdx.x == 0 && threadIdx.x == 0) { st->T = T; st->t = rem3; }
   }
   const int64_t base = (int64_t)blockIdx.x * kSelTile;
-  int ndef = 0, ntie = 0;
-#pragma unroll
-  for (int it = 0; it < kSelTile / (4 * kThreads); ++it) {
-    bool d[4], t[4];
-    flags4(base + (int64_t)it * 4 * kThreads + 4 * threadIdx.x, C_local, bits, keys, none, T, d, t);
-#pragma unroll
-    for (int i = 0; i < 4; ++i) { ndef += d[i]; ntie += t[i]; }
-  }
+  uint32_t dm, tm;
+  flags32(base + 32 * threadIdx.x, C_local, bits, keys, none, T, dm, tm);
+  int ndef = __popc(dm), ntie = __popc(tm);
   if (threadIdx.x == 0) { sdef = 0; stie = 0; }
   __syncthreads();
 #pragma unroll
@@ -237,44 +239,52 @@ __global__ void __launch_bounds__(kThreads) k_tile_counts(int64_t C_local, const
   }
 }
 
-// K4b: single block. Exclusive scans: tie offsets, then selected counts (definite + ties ranked < t).
+// K4b: single block. Exclusive scans: tie offsets, then selected counts (definite + ties ranked < t); warp-shuffle
+// block scans over 1024 tiles at a time.
 __global__ void __launch_bounds__(1024) k_tile_scan(int* __restrict__ tile_cnt, int ntiles, SamplerState* st,
                                                     int* err) {
-  __shared__ int scan[1024];
-  __shared__ int carry;
+  __shared__ int wsum[32];
   const SamplerState s = *st;
   int* def = tile_cnt;
   int* tie = tile_cnt + ntiles;
   int* tie_off = tile_cnt + 2 * ntiles;
   int* sel_off = tile_cnt + 3 * ntiles;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   for (int pass = 0; pass < 2; ++pass) {
-    if (threadIdx.x == 0) carry = 0;
-    __syncthreads();
-    for (int base = 0; base < ntiles; base += blockDim.x) {
-      int i = base + threadIdx.x;
+    int carry = 0;
+    for (int base = 0; base < ntiles; base += 1024) {
+      const int i = base + threadIdx.x;
       int v = 0;
       if (i < ntiles) {
         if (pass == 0) v = tie[i];
         else v = def[i] + (s.none ? 0 : max(0, min(s.t - tie_off[i], tie[i])));
       }
-      scan[threadIdx.x] = v;
-      __syncthreads();
-      for (int off = 1; off < (int)blockDim.x; off <<= 1) {
-        int u = threadIdx.x >= off ? scan[threadIdx.x - off] : 0;
-        __syncthreads();
-        scan[threadIdx.x] += u;
-        __syncthreads();
+      int incl = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += u;
       }
-      if (i < ntiles) (pass == 0 ? tie_off : sel_off)[i] = carry + scan[threadIdx.x] - v;
+      if (lane == 31) wsum[w] = incl;
       __syncthreads();
-      if (threadIdx.x == blockDim.x - 1) carry += scan[threadIdx.x];
+      if (w == 0) {
+        int x = wsum[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int u = __shfl_up_sync(0xffffffffu, x, o);
+          if (lane >= o) x += u;
+        }
+        wsum[lane] = x;
+      }
+      __syncthreads();
+      if (i < ntiles) (pass == 0 ? tie_off : sel_off)[i] = carry + (w ? wsum[w - 1] : 0) + incl - v;
+      carry += wsum[31];
       __syncthreads();
     }
     if (pass == 1 && threadIdx.x == 0) {
       st->total = carry;
       if (carry != s.k) atomicOr(err, ERR_INTERNAL);
     }
-    __syncthreads();
   }
 }
 
@@ -288,31 +298,24 @@ __global__ void __launch_bounds__(kThreads) k_tile_write(int64_t C_local, const 
   const uint32_t T = st->T;
   const int tsel = st->t;
   const int64_t base = (int64_t)blockIdx.x * kSelTile;
-  int tie_run = tile_cnt[2 * ntiles + blockIdx.x];
-  int out_run = tile_cnt[3 * ntiles + blockIdx.x];
-#pragma unroll 1
-  for (int it = 0; it < kSelTile / (4 * kThreads); ++it) {
-    const int64_t j0 = base + (int64_t)it * 4 * kThreads + 4 * threadIdx.x;
-    bool d[4], t[4];
-    flags4(j0, C_local, bits, keys, none, T, d, t);
-    const int nt = t[0] + t[1] + t[2] + t[3];
-    int ttot;
-    int trank = tie_run + block_count_scan(nt, wsum, ttot);
-    bool sel[4];
-    int ns = 0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      sel[i] = d[i] || (t[i] && trank < tsel);
-      trank += t[i];
-      ns += sel[i];
-    }
-    int stot;
-    int pos = out_run + block_count_scan(ns, wsum, stot);
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (sel[i]) idx[pos++] = (int32_t)(j0 + i);
-    tie_run += ttot;
-    out_run += stot;
+  const int64_t j0 = base + 32 * threadIdx.x;     // this thread's 32 consecutive classes, in id order
+  uint32_t dm, tm;
+  flags32(j0, C_local, bits, keys, none, T, dm, tm);
+  int ttot;
+  int trank = tile_cnt[2 * ntiles + blockIdx.x] + block_count_scan(__popc(tm), wsum, ttot);
+  uint32_t sel = dm;
+  while (tm) {                                    // ties are taken smallest id first (R3): rank < t
+    const int i = __ffs(tm) - 1;
+    tm &= tm - 1;
+    if (trank < tsel) sel |= 1u << i;
+    ++trank;
+  }
+  int stot;
+  int pos = tile_cnt[3 * ntiles + blockIdx.x] + block_count_scan(__popc(sel), wsum, stot);
+  while (sel) {
+    const int i = __ffs(sel) - 1;
+    sel &= sel - 1;
+    idx[pos++] = (int32_t)(j0 + i);
   }
 }
 
