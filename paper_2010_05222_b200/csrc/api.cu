@@ -402,7 +402,7 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
                       c->tcol, c->err_dev, s);
   mark(c, 2, s);
   if (!c->fused_gather) n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
-  n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tcol, c->ct, s);
+  n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tile_cnt, c->tcol, c->ct, s);
   mark(c, 3, s);
   if (c->fused_gather)
     n += launch_logits_gather_tc(sz, c->W, c->idx, c->Xb, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,

@@ -313,6 +313,7 @@ __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, const float* 
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
+#pragma unroll 4
   for (int s = 1; s < nsplit; ++s) {
     const float4 v = *reinterpret_cast<const float4*>(ws + s * stride + i);
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;

@@ -124,7 +124,8 @@ int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaS
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st,
                     void* Ws, float* inv_norm, int* err, cudaStream_t s);
 int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
-                      const SamplerState* st, int32_t* tcol, float* ct, cudaStream_t s);
+                      const SamplerState* st, const int* tile_cnt /* sampler K4 tile offsets */, int32_t* tcol,
+                      float* ct, cudaStream_t s);
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
 int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,

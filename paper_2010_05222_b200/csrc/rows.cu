@@ -107,7 +107,8 @@ __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, co
 // Also tcol[n] = position of y_n in the sampled set idx (binary search; -1 when not sampled on this rank).
 __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const float* __restrict__ X32,
                              const float* __restrict__ W, const int64_t* __restrict__ Y,
-                             const int32_t* __restrict__ idx, const SamplerState* st, int32_t* __restrict__ tcol,
+                             const int32_t* __restrict__ idx, const SamplerState* st,
+                             const int* __restrict__ sel_off, int ntiles, int32_t* __restrict__ tcol,
                              float* __restrict__ ct) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= M) return;
@@ -117,7 +118,9 @@ __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const flo
     return;
   }
   if (lane == 0) {
-    int lo = 0, hi = st->k - 1, res = -1;
+    // search only the positions of j's compaction tile: [sel_off[t], sel_off[t + 1]) (K4b exclusive scan)
+    const int t = (int)(j / kSelTile);
+    int lo = sel_off[t], hi = (t + 1 < ntiles ? sel_off[t + 1] : st->k) - 1, res = -1;
     while (lo <= hi) {
       const int mid = (lo + hi) >> 1;
       const int v = idx[mid];
@@ -148,12 +151,21 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float2* pr = partials + (int64_t)n * ntiles;
   const int nvalid = min(ntiles, (st->k + ltile - 1) / ltile);   // tiles past k_i are never written
-  float m = -INFINITY, l = 0.f;
-  for (int t = threadIdx.x; t < nvalid; t += blockDim.x) {       // online (max, sum) per thread
-    const float2 v = pr[t];
-    if (v.x > m) { l = l * __expf(m - v.x) + v.y; m = v.x; }
-    else if (v.x > -INFINITY) l += v.y * __expf(v.x - m);
+  // online (max, sum) per thread, four independent accumulators (loads in flight together)
+  float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, lq[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int t0 = threadIdx.x; t0 < nvalid; t0 += 4 * blockDim.x) {
+    float2 v[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) v[q] = t0 + q * (int)blockDim.x < nvalid ? pr[t0 + q * blockDim.x] : make_float2(-INFINITY, 0.f);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (v[q].x > mq[q]) { lq[q] = lq[q] * __expf(mq[q] - v[q].x) + v[q].y; mq[q] = v[q].x; }
+      else if (v[q].x > -INFINITY) lq[q] += v[q].y * __expf(v[q].x - mq[q]);
+    }
   }
+  float m = fmaxf(fmaxf(mq[0], mq[1]), fmaxf(mq[2], mq[3])), l = 0.f;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) l += mq[q] > -INFINITY ? lq[q] * __expf(mq[q] - m) : 0.f;
   const float wm = warp_max(m);
   l = (m > -INFINITY) ? l * __expf(m - wm) : 0.f;
   l = warp_sum(l);
@@ -499,8 +511,9 @@ int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* i
 }
 
 int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
-                      const SamplerState* st, int32_t* tcol, float* ct, cudaStream_t s) {
-  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, idx, st, tcol, ct);
+                      const SamplerState* st, const int* tile_cnt, int32_t* tcol, float* ct, cudaStream_t s) {
+  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, idx, st,
+                                                       tile_cnt + 3 * sz.ntiles_sel, sz.ntiles_sel, tcol, ct);
   return 1;
 }
 
