@@ -231,6 +231,8 @@ FUSED_SHAPES = [
     (12000, 256, 256, 0.1, "cosface", 0.4, "init", 0.0),      # M = 256 exactly, two 128-column d-tiles
     (5000, 1024, 130, 0.2, "arcface", 0.5, "init", 0.0),      # d = 1024 (16 K-blocks, 8 d-tiles), M = 130
     (7000, 128, 256, 0.3, "arcface", 0.5, "init", 0.0),       # d = 128: one d-tile, 148 class-tile groups
+    (129, 128, 1, 0.02, "arcface", 0.5, "init", 0.0),         # B = 1: k_i = 3, a single partial class tile
+    (3000, 384, 3, 1.0, "cosface", 0.4, "init", 0.0),         # r = 1 (k = C), d = 384 (three d-tiles), M = 3
 ]
 
 
