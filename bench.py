@@ -31,6 +31,7 @@ METRIC = "PFC fwd+bwd samples/s, 10M ids r=0.1, 1/8×B200; tensor-pipe % of peak
 CONFIGS = {
     # name: (C, d, B per GPU, r, margin, m, description)
     "c4": (10_000_000, 512, 256, 0.1, "arcface", 0.5, "10M identities, d=512, B=256/GPU, r=0.1, ArcFace m=0.5 (BASELINE configs[3])"),
+    "c1": (1_000, 128, 64, 0.1, "arcface", 0.5, "toy: C=1000, d=128, B=64, r=0.1, ArcFace m=0.5 (BASELINE configs[0]; contract tests)"),
     "c2": (85_742, 512, 128, 0.1, "arcface", 0.5, "MS1MV2-shaped: C=85,742, d=512, B=128/GPU, r=0.1, ArcFace (BASELINE configs[1])"),
     "c3": (360_232, 512, 128, 0.1, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=0.1, CosFace m=0.4 (BASELINE configs[2])"),
     "c3r1": (360_232, 512, 128, 1.0, "cosface", 0.4, "Glint360K-shaped: C=360,232, d=512, B=128/GPU, r=1.0, CosFace m=0.4 (BASELINE configs[2])"),
