@@ -32,6 +32,7 @@ struct pfc_ctx {
   bool sync_check = false;
   std::string err;
   ncclComm_t comm = nullptr;
+  bool nccl_solo = false;      // PFC_NCCL_SOLO=1 at world size 1: run the NCCL collectives on a 1-rank communicator
   uint64_t step = 0;
   bool fb_done = false;      // a forward_backward happened and its gradient was not yet applied
   cudaStream_t last_stream = nullptr;
@@ -325,6 +326,19 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
     pfc_destroy(c);
     return set_err(nullptr, PFC_ERR_CUDA, m);
   }
+  const char* solo = std::getenv("PFC_NCCL_SOLO");
+  if (k == 1 && cfg->comm_mode == PFC_COMM_NCCL && solo && solo[0] == '1') {
+    // validation mode: the multi-rank code path (every collective call, graph-captured) on one GPU, where each
+    // collective is the identity; results must equal the world-size-1 path
+    int dev = cfg->device;
+    ncclResult_t r = ncclCommInitAll(&c->comm, 1, &dev);
+    if (r != ncclSuccess) {
+      std::string m = std::string("ncclCommInitAll: ") + ncclGetErrorString(r);
+      pfc_destroy(c);
+      return set_err(nullptr, PFC_ERR_NCCL, m);
+    }
+    c->nccl_solo = true;
+  }
   if (k > 1 && cfg->comm_mode == PFC_COMM_NCCL) {
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -497,7 +511,7 @@ pfc_status pfc_train_step(pfc_ctx* c, const float* x, const int64_t* labels, flo
 static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss_out, bool fused,
                          cudaStream_t s, ncclResult_t* nres) {
   const Sizes& sz = c->sz;
-  const bool multi = sz.world > 1;
+  const bool multi = sz.world > 1 || c->nccl_solo;
   *nres = ncclSuccess;
   auto nccl = [&](ncclResult_t r) { if (r != ncclSuccess && *nres == ncclSuccess) *nres = r; };
   mark(c, 0, s);

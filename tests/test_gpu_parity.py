@@ -406,6 +406,37 @@ def test_checkpoint_resume_continues_identically():
     b.close()
 
 
+@pytest.mark.parametrize("B", [64, 300], ids=["fused-kernels", "tcgen05-gemms"])
+def test_nccl_collectives_single_rank(monkeypatch, B):
+    """The NCCL code path (all-gather, two all-reduces, reduce-scatter, graph-captured) on a 1-rank communicator
+    (PFC_NCCL_SOLO=1), where every collective is the identity: losses, gradients and parameters equal the
+    world-size-1 path that skips them."""
+    C, d = 9000, 256
+    plain = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=6)
+    monkeypatch.setenv("PFC_NCCL_SOLO", "1")
+    solo = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=6)
+    monkeypatch.delenv("PFC_NCCL_SOLO")
+    side = torch.cuda.Stream()
+    gx_a, gx_b = torch.empty(B, d, device="cuda"), torch.empty(B, d, device="cuda")
+    la, lb = torch.zeros(1, device="cuda"), torch.zeros(1, device="cuda")
+    for i in range(4):   # eager, capture, replays
+        x = torch.from_numpy(synth.make_features(4, i, 1, B, d)[0]).cuda()
+        y = torch.from_numpy(synth.make_labels(4, i, 1, B, C)[0]).cuda()
+        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            plain.train_step(x, y, gx_a, la, lr=0.1, stream=side)
+            solo.train_step(x, y, gx_b, lb, lr=0.1, stream=side)
+        torch.cuda.synchronize()
+        assert abs(la.item() - lb.item()) <= 1e-6 * abs(la.item())
+        assert maxrel(gx_b.cpu().numpy(), gx_a.cpu().numpy()) <= 1e-5
+        assert np.array_equal(plain.sampled(), solo.sampled())
+    Wa, Va = plain.params()
+    Wb, Vb = solo.params()
+    assert maxrel(Wb.cpu().numpy(), Wa.cpu().numpy()) <= 1e-6 and maxrel(Vb.cpu().numpy(), Va.cpu().numpy()) <= 1e-5
+    plain.close()
+    solo.close()
+
+
 def test_cuda_graph_replay_matches_eager():
     """pfc_train_step on a capturable stream is captured once and replayed as a CUDA graph (device-side step
     counter and learning rate); results must match the eager launches on the legacy stream."""
