@@ -32,6 +32,8 @@ struct pfc_ctx {
   bool sync_check = false;
   std::string err;
   ncclComm_t comm = nullptr;
+  cudaStream_t side = nullptr;                    // multi-rank: dX exchange overlapping the dW kernel
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool nccl_solo = false;      // PFC_NCCL_SOLO=1 at world size 1: run the NCCL collectives on a 1-rank communicator
   uint64_t step = 0;
   bool fb_done = false;      // a forward_backward happened and its gradient was not yet applied
@@ -349,6 +351,14 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
       return set_err(nullptr, PFC_ERR_NCCL, m);
     }
   }
+  if (c->comm) {   // side stream + fork/join events of the overlapped dX exchange
+    if (cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      pfc_destroy(c);
+      return set_err(nullptr, PFC_ERR_CUDA, "side stream / event creation failed");
+    }
+  }
   *out = c;
   return PFC_OK;
 }
@@ -359,6 +369,9 @@ pfc_status pfc_destroy(pfc_ctx* c) {
   cudaDeviceSynchronize();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->side) cudaStreamDestroy(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   for (auto& ev : c->prof_ev)
     for (auto& e : ev) cudaEventDestroy(e);
   for (void* p : c->allocs) cudaFree(p);
@@ -456,12 +469,10 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
   c->launches += n;
 }
 
-// after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat (+ K12 when fused)
-void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream_t s) {
+// K11 dW_hat (+ K12 when fused); independent of the dX exchange
+void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
-  n += launch_xnorm_backward(sz, dxh, c->xh_local, c->xnorm, grad_x, s);
-  mark(c, 8, s);
   if (fused && c->use_dwx) {
     // dW + SGD ran inside the dX kernel (phase_d)
   } else if (c->use_tc && fused) {
@@ -477,8 +488,15 @@ void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream
       n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
                       c->cfg.weight_decay, c->fused_gather ? 1 : 0, s);
   }
-  mark(c, 9, s);
   c->launches += n;
+}
+
+// after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat (+ K12 when fused)
+void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream_t s) {
+  c->launches += launch_xnorm_backward(c->sz, dxh, c->xh_local, c->xnorm, grad_x, s);
+  mark(c, 8, s);
+  phase_e_dw(c, fused, s);
+  mark(c, 9, s);
 }
 
 pfc_status finish_fb(pfc_ctx* c, bool fused, cudaStream_t s) {
@@ -533,11 +551,23 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
   phase_d(c, gmax, loss_out, fused, s);
   mark(c, 7, s);
   const float* dxh = c->dXh + (size_t)sz.rank * sz.B * sz.d;
-  if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
-    nccl(ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
-    dxh = c->dxh_local;
+  if (multi && !(fused && c->use_dwx) && !c->prof_cur && c->side) {
+    // the dX exchange and the x-norm backward on a side stream, overlapping the dW (+ SGD) kernel, which does
+    // not depend on them (fork / join by events: also inside graph capture)
+    cudaEventRecord(c->ev_fork, s);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    nccl(ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, c->side));
+    c->launches += launch_xnorm_backward(sz, c->dxh_local, c->xh_local, c->xnorm, grad_x, c->side);
+    phase_e_dw(c, fused, s);
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(s, c->ev_join, 0);
+  } else {
+    if (multi) {  // Alg.1 L12-13: allreduce(grad logits w^T) then get_submatrix(i) == reduce-scatter (R16)
+      nccl(ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, s));
+      dxh = c->dxh_local;
+    }
+    phase_e(c, dxh, grad_x, fused, s);
   }
-  phase_e(c, dxh, grad_x, fused, s);
   c->launches += launch_advance_step(c->step_dev, s);
 }
 
