@@ -434,6 +434,9 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
   if (c->fused_gather)
     n += launch_logits_gather_tc(sz, c->W, c->idx, c->Xb, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
                                  c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev, s);
+  else if (c->use_tc && logits_pair_enabled(sz))
+    n += launch_logits_pair_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->st, c->mp, (__half*)c->cosv,
+                               c->partials, s);
   else if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);

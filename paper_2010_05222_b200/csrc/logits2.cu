@@ -1,0 +1,298 @@
+// K6 logits for global batches M > 256 on CTA pairs (tcgen05 cta_group::2): C[M x k] = X_hat . W_s^T with the same
+// fused epilogue as the single-CTA kernel of gemm_tc.cu (Alg.1 L3-5; fp16 class-major cosines,
+// per-(row, 128-column tile) max / sum partials with the target column excluded, R22).
+//
+// A cluster of two CTAs computes a 256 (batch rows) x 256 (classes) tile: CTA r stages batch rows 128 r .. +127
+// of X_hat and class rows 128 r .. +127 of W_s per 64-wide K block (TMA, 128-byte swizzle, both landing on the
+// leader CTA's mbarrier), and the leader's single MMA thread issues tcgen05.mma.cta_group::2 (M = 256, N = 256),
+// which reads A from both CTAs' shared memory along M and B along N and accumulates into each CTA's TMEM its own
+// 128 rows x 256 columns. Per K block and SM that is 32 KB of operands for 4.2 MFLOP instead of 48 KB for the
+// single-CTA 256 x 128 tile: the contraction is less bound by the L2 -> SM operand stream at large M.
+//   warp 0     TMA producer (each CTA its halves)
+//   warp 1     TMEM allocation (both CTAs, cta_group::2); MMA issue (leader CTA only); commits multicast to both
+//   warps 2-17 epilogue (each CTA its 128 rows): four sets of 4 warps, 64 columns each; the two sets of a
+//              128-column logits tile combine their (max, sum) through shared memory; TMEM release is signalled
+//              to the leader's barrier (remote arrive for the peer CTA)
+#include <cuda_fp16.h>
+#include <algorithm>
+#include <cstdlib>
+
+#include "pfc_internal.cuh"
+#include "tc_common.cuh"
+
+namespace pfc {
+namespace {
+
+constexpr int L2_BK = 64;
+constexpr int L2_STAGES = 6;
+constexpr int L2_ACC = 2;
+constexpr int L2_EPI = 16;
+constexpr int L2_THREADS = 32 * (2 + L2_EPI);
+constexpr int L2_HALF = 128 * L2_BK * 2;                // 16 KB: 128 rows x 64 K (bf16)
+constexpr int L2_STAGE = 2 * L2_HALF;                   // A half + B half
+constexpr int L2_PART = L2_ACC * 2 * 128 * 8;           // s_part: [acc][ltile pair][row] float2
+constexpr int L2_SMEM = L2_STAGES * L2_STAGE + 1024 + 256 + L2_PART;
+static_assert(L2_SMEM <= 232448, "shared memory overflow");
+constexpr uint32_t kPeerMask = 0xFEFFFFFFu;             // leader CTA's copy of a shared::cluster address
+
+struct L2Params {
+  int M, ldm, d;
+  const SamplerState* st;
+  const int32_t* tcol;
+  float s_log2e, scale;
+  __half* cosv;
+  float2* partials;
+  int n_ltiles;
+};
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// the leader CTA's (rank 0) copy of a local shared-memory address
+__device__ __forceinline__ uint32_t leader_addr(const void* p) {
+  uint32_t a;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(p)));
+  return a;
+}
+// default semantics (release, CTA scope) as CUTLASS's ClusterBarrier::arrive(cta_id): a release.cluster arrive
+// costs a cluster-scope fence behind every cosine store of the tile (measured 8% slower)
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// TMA tile load into this CTA's shared memory, completing on the pair leader's mbarrier
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
+      "[%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
+      : "memory");
+}
+// arrive on the barrier at this shared-memory offset in both CTAs of the pair once the issued MMAs complete
+__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
+  asm volatile(
+      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
+    k_logits_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, L2Params p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L2_STAGES * L2_STAGE);   // leader: both CTAs' bytes
+  uint64_t* empty = full + L2_STAGES;                                           // each CTA: MMA done with stage
+  uint64_t* acc_full = empty + L2_STAGES;                                       // each CTA
+  uint64_t* acc_empty = acc_full + L2_ACC;                                      // leader: both CTAs' epilogues
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + L2_ACC);
+  float2* s_part = reinterpret_cast<float2*>(smem + L2_STAGES * L2_STAGE + 256);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int k = p.st->k;
+  const int mt = (p.M + 255) / 256, nt = (k + 255) / 256;
+  const int n_units = mt * nt, n_kb = p.d / L2_BK;
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < L2_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < L2_ACC; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 2 * L2_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmB); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  cluster_sync();            // barriers initialised and TMEM allocated in both CTAs before any remote traffic
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer (this CTA's halves)
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int u = pair; u < n_units; u += npairs) {
+        const int m0 = (u % mt) * 256, n0 = (u / mt) * 256;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * L2_HALF));
+          uint8_t* sa = smem + stage * L2_STAGE;
+          tma_load_2d_pair(sa, &tmA, &full[stage], kb * L2_BK, m0 + 128 * (int)rank);
+          tma_load_2d_pair(sa + L2_HALF, &tmB, &full[stage], kb * L2_BK, n0 + 128 * (int)rank);
+          if (++stage == L2_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer (leader CTA)
+    if (leader) {
+      constexpr uint32_t IDESC = make_idesc(256, 256, false, false);
+      int stage = 0, acc = 0;
+      uint32_t phase = 0, acc_phase = 0;
+      for (int u = pair; u < n_units; u += npairs) {
+        mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tacc = tmem_base + acc * 256;
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t sa = smem_u32(smem + stage * L2_STAGE), sb = sa + L2_HALF;
+#pragma unroll
+            for (int kk = 0; kk < L2_BK / 16; ++kk)
+              tc_mma_pair(tacc, make_desc(sa + kk * 32, 16, 1024), make_desc(sb + kk * 32, 16, 1024), IDESC,
+                          (kb > 0 || kk > 0) ? 1u : 0u);
+            tc_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == L2_STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) tc_commit_pair(&acc_full[acc]);
+        __syncwarp();
+        if (++acc == L2_ACC) { acc = 0; acc_phase ^= 1; }
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- epilogue (this CTA's 128 rows)
+    const int ew = warp - 2;
+    const int lg = warp & 3;
+    const int row_in = lg * 32 + lane;
+    const int eset = ew >> 2;                 // 64 columns each; sets (0, 1) and (2, 3) form 128-column tiles
+    const float sl = p.s_log2e;
+    const uint32_t acc_empty_leader = leader_addr(&acc_empty[0]);
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int u = pair; u < n_units; u += npairs) {
+      const int m0 = (u % mt) * 256, n0 = (u / mt) * 256;
+      const int row = m0 + 128 * (int)rank + row_in;
+      const bool rv = row < p.M;
+      const int tc = rv ? p.tcol[row] : -1;
+      mbar_wait(&acc_full[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
+      float mx = -INFINITY, sum = 0.f;
+#pragma unroll 1
+      for (int c = eset * 2; c < eset * 2 + 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tacc + c * 32, v);
+        const int col0 = n0 + c * 32;
+        __half2 h2[16];
+        float cf[32];
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+          const float2 f = __half22float2(h2[i]);
+          cf[2 * i] = f.x;
+          cf[2 * i + 1] = f.y;
+        }
+        if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col0 + j >= k || col0 + j == tc) cf[j] = -INFINITY;
+        }
+        float q0 = cf[0], q1 = cf[1], q2 = cf[2], q3 = cf[3];
+#pragma unroll
+        for (int j = 4; j < 32; j += 4) {
+          q0 = fmaxf(q0, cf[j]); q1 = fmaxf(q1, cf[j + 1]); q2 = fmaxf(q2, cf[j + 2]); q3 = fmaxf(q3, cf[j + 3]);
+        }
+        const float nmx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
+        if (nmx > -INFINITY) {
+          const float nb = nmx * sl;
+          float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
+            s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
+            s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
+            s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+          }
+          sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
+          mx = nmx;
+        }
+        const bool odd = lane & 1;
+        __half* cb = p.cosv + (row & ~1);
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const __half send = odd ? __low2half(h2[i]) : __high2half(h2[i]);
+          const unsigned short rcv = (unsigned short)__shfl_xor_sync(0xffffffffu, (int)__half_as_ushort(send), 1);
+          const __half other = __ushort_as_half(rcv);
+          const __half2 pr = odd ? __halves2half2(other, __high2half(h2[i])) : __halves2half2(__low2half(h2[i]), other);
+          if (row < p.ldm) *reinterpret_cast<__half2*>(cb + (int64_t)(col0 + 2 * i + (odd ? 1 : 0)) * p.ldm) = pr;
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {                              // TMEM buffer consumed (the leader's barrier counts both CTAs)
+        if (leader) mbar_arrive(&acc_empty[acc]);
+        else mbar_arrive_cluster(acc_empty_leader + acc * 8);
+      }
+      float2* sp = s_part + acc * 256;
+      if (eset & 1) sp[(eset >> 1) * 128 + row_in] = make_float2(mx, sum);
+      asm volatile("bar.sync 4, %0;" ::"n"(32 * L2_EPI) : "memory");
+      if (!(eset & 1)) {
+        const float2 o = sp[(eset >> 1) * 128 + row_in];
+        const float m = fmaxf(mx, o.x);
+        float l = 0.f;
+        if (m > -INFINITY)
+          l = (mx > -INFINITY ? sum * ex2_ftz((mx - m) * sl) : 0.f) + (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
+        if (rv)
+          p.partials[(int64_t)row * p.n_ltiles + n0 / 128 + (eset >> 1)] =
+              make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
+      }
+      if (++acc == L2_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+  }
+  tc_fence_before();
+  cluster_sync();            // no CTA leaves while its pair may still read its shared memory or signal it
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
+}  // namespace
+
+bool logits_pair_enabled(const Sizes& sz) {
+  static const int forced = [] { const char* e = std::getenv("PFC_LOGITS_PAIR"); return e ? std::atoi(e) : 1; }();
+  return forced != 0 && sz.M > 256 && sz.k_pad % 256 == 0;
+}
+
+int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_logits_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    attr = true;
+  }
+  const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  const CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  L2Params p{};
+  p.M = sz.M; p.ldm = (int)sz.M_pad; p.d = sz.d; p.st = st; p.tcol = tcol;
+  p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
+  p.n_ltiles = sz.n_ltiles;
+  const int64_t units = ((sz.M + 255) / 256) * (sz.k_pad / 256);
+  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));
+  k_logits_pair<<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+  return 1;
+}
+
+}  // namespace pfc

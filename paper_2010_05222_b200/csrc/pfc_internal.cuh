@@ -174,6 +174,10 @@ bool logits_gather_supported(const Sizes& sz);
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
                             MarginParams mp, __half* cosv, float2* partials, int* err, cudaStream_t s);
+// logits2.cu — K6 on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) for M > 256
+bool logits_pair_enabled(const Sizes& sz);
+int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, cudaStream_t s);
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,
                  float* dXh, float* split_ws, cudaStream_t s);
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
