@@ -33,8 +33,6 @@ constexpr int L2_STAGE = 2 * L2_HALF;                   // A half + B half
 constexpr int L2_PART = L2_ACC * 2 * 128 * 8;           // s_part: [acc][ltile pair][row] float2
 constexpr int L2_SMEM = L2_STAGES * L2_STAGE + 1024 + 256 + L2_PART;
 static_assert(L2_SMEM <= 232448, "shared memory overflow");
-constexpr uint32_t kPeerMask = 0xFEFFFFFFu;             // leader CTA's copy of a shared::cluster address
-
 struct L2Params {
   int M, ldm, d;
   const SamplerState* st;
@@ -44,50 +42,6 @@ struct L2Params {
   float2* partials;
   int n_ltiles;
 };
-
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// the leader CTA's (rank 0) copy of a local shared-memory address
-__device__ __forceinline__ uint32_t leader_addr(const void* p) {
-  uint32_t a;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(a) : "r"(smem_u32(p)));
-  return a;
-}
-// default semantics (release, CTA scope) as CUTLASS's ClusterBarrier::arrive(cta_id): a release.cluster arrive
-// costs a cluster-scope fence behind every cosine store of the tile (measured 8% slower)
-__device__ __forceinline__ void mbar_arrive_cluster(uint32_t cluster_addr) {
-  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
-}
-// TMA tile load into this CTA's shared memory, completing on the pair leader's mbarrier
-__device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], "
-      "[%2];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar) & kPeerMask), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void tc_mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                            uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, {%5, %5, %5, %5, %5, %5, %5, %5}, p;\n\t}" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(acc), "r"(0u)
-      : "memory");
-}
-// arrive on the barrier at this shared-memory offset in both CTAs of the pair once the issued MMAs complete
-__device__ __forceinline__ void tc_commit_pair(uint64_t* bar) {
-  asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          smem_u32(bar))
-      : "memory");
-}
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     k_logits_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, L2Params p) {
