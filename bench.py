@@ -15,9 +15,7 @@ Prints ONE JSON line on rank 0 (see DESIGN.md §Measurement for every key).
 """
 import argparse
 import json
-import math
 import os
-import subprocess
 import sys
 import threading
 import time

@@ -1,6 +1,5 @@
 """Print bf16/fp32 parity errors per case (development diagnostic)."""
 import sys
-import numpy as np
 sys.path.insert(0, ".")
 sys.path.insert(0, "tests")
 import test_gpu_parity as T

@@ -1,6 +1,6 @@
 """Top SASS lines by warp-stall samples for one kernel (by launch index in the report) of an ncu report.
     python scripts/ncu_stalls.py report.ncu-rep <launch-index> [n]"""
-import csv, io, re, subprocess, sys
+import csv, io, subprocess, sys
 rep, pat = sys.argv[1], sys.argv[2]
 n = int(sys.argv[3]) if len(sys.argv) > 3 else 25
 out = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass", "--launch-skip", pat,

@@ -9,7 +9,6 @@
    PartialFC.from_process_group does before pfc_init).
 3. bench.py's max-over-ranks timing reduction.
 """
-import math
 import os
 import socket
 
