@@ -36,6 +36,8 @@ CONFIGS = {
     "c5": (100_000_000, 512, 256, 0.1, "arcface", 0.5, "100M identities, d=512, B=256/GPU, r=0.1, ArcFace (BASELINE configs[4])"),
     # one rank's exact per-GPU work of the 8-GPU jobs, on one GPU (its C/8 shard and the global batch 8 x 256)
     "c4rank": (1_250_000, 512, 2048, 0.1, "arcface", 0.5, "per-rank proxy of configs[3] on 8 GPUs: 1.25M-class shard, global batch 2048, r=0.1"),
+    "c4rank2": (5_000_000, 512, 512, 0.1, "arcface", 0.5, "per-rank proxy of configs[3] on 2 GPUs: 5M-class shard, global batch 512, r=0.1"),
+    "c4rank4": (2_500_000, 512, 1024, 0.1, "arcface", 0.5, "per-rank proxy of configs[3] on 4 GPUs: 2.5M-class shard, global batch 1024, r=0.1"),
     "c5rank": (12_500_000, 512, 2048, 0.1, "arcface", 0.5, "per-rank proxy of configs[4] on 8 GPUs: 12.5M-class shard (51 GB W+V), global batch 2048, r=0.1"),
 }
 SCALE = 64.0

@@ -1,4 +1,4 @@
-// K11 + K12 fused on CTA pairs (train step, bf16 tensor-core path, M >= 1024, d % 256 == 0): the dW_hat tile of
+// K11 + K12 fused on CTA pairs (train step, bf16 tensor-core path, M >= 2048, d % 256 == 0): the dW_hat tile of
 // 256 sampled classes x 256 columns = G^T X_hat (Alg.1 L10) with tcgen05.mma.cta_group::2 (M = 256 classes split
 // across the pair, N = 256 columns split across the pair), and the lazy momentum-SGD update of those W / V rows
 // in each CTA's epilogue. CTA r stages per 64-batch K block its 128 classes of G (K-major A) and its
@@ -35,6 +35,7 @@ struct DpParams {
   SgdArgs sgd;
 };
 
+template <bool HINT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
     k_dw_sgd_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, DpParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -51,11 +52,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
-  const bool leader = rank == 0;
+  const int pr = (int)rank;
+  const bool leader = pr == 0;
   const int k = p.st->k;
-  const int nd = p.d / 256, nct = (k + 255) / 256;
-  const int n_units = nct * nd, n_kb = (p.M + DP_BK - 1) / DP_BK;
+  const int ndq = p.d / 256, nct = (k + 255) / 256;    // units: (class tile, 256-column d tile)
+  const int n_units = nct * ndq, n_kb = (p.M + DP_BK - 1) / DP_BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  auto dtile = [&](int u) { return (u % ndq) * 256; };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < DP_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -80,7 +83,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int u = pair; u < n_units; u += npairs) {
-        const int c0 = (u / nd) * 256 + 128 * (int)rank, d0 = (u % nd) * 256 + 128 * (int)rank;
+        const int c0 = (u / ndq) * 256 + 128 * pr, d0 = dtile(u) + 128 * pr;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * DP_HALF));
@@ -128,11 +131,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
     const int row_in = lg * 32 + lane;
     const int eset = ew >> 2;
     const float lr = *p.sgd.lr;
+    const uint64_t pol = HINT ? policy_evict_first() : 0;
     const uint32_t acce_leader = leader_addr(&acc_empty[0]);
     int32_t nx_j = -1;
     float nx_inv = 0.f, nx_rad = 0.f;
     auto scalars = [&](int u) {
-      const int prow = (u / nd) * 256 + 128 * (int)rank + row_in;
+      const int prow = (u / ndq) * 256 + 128 * pr + row_in;
       nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
       if (u < n_units && prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
     };
@@ -140,7 +144,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = pair; u < n_units; u += npairs) {
-      const int dcol0 = (u % nd) * 256;
+      const int dcol0 = dtile(u);
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DP_EPI) : "memory");   // previous tile consumed
       int32_t pf_j = -1;
       if (eset == 0) {
@@ -159,8 +163,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
         for (int r = 0; r < 4; ++r) {
           jr[r] = s_rowj[ew16 + 4 * b + r];
           if (jr[r] >= 0) {
-            wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
-            mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
+            if (HINT) {
+              wv[r] = ld_hint4(p.sgd.W + (int64_t)jr[r] * p.d + col, pol);
+              mv[r] = ld_hint4(p.sgd.V + (int64_t)jr[r] * p.d + col, pol);
+            } else {
+              wv[r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col);
+              mv[r] = *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col);
+            }
           }
         }
       };
@@ -179,8 +188,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
             m.z = p.sgd.mu * m.z + (g4.z - w.z * rad) * oi + p.sgd.lambda * w.z;
             m.w = p.sgd.mu * m.w + (g4.w - w.w * rad) * oi + p.sgd.lambda * w.w;
             w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
-            *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
-            *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+            if (HINT) {
+              st_hint4(p.sgd.V + (int64_t)jr[r] * p.d + col, m, pol);
+              st_hint4(p.sgd.W + (int64_t)jr[r] * p.d + col, w, pol);
+            } else {
+              *reinterpret_cast<float4*>(p.sgd.V + (int64_t)jr[r] * p.d + col) = m;
+              *reinterpret_cast<float4*>(p.sgd.W + (int64_t)jr[r] * p.d + col) = w;
+            }
           }
         }
       };
@@ -206,7 +220,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       load(0, 1, wb, mb, jb);
       update(0, 0, wa, ma, ja);
       if (pf_j >= 0) {   // the next tile's W / V row segments (256 columns) into L2
-        const int ndc = ((u + npairs) % nd) * 256;
+        const int ndc = dtile(u + npairs);
         const float* wp = p.sgd.W + (int64_t)pf_j * p.d + ndc;
         const float* vp = p.sgd.V + (int64_t)pf_j * p.d + ndc;
 #pragma unroll
@@ -252,14 +266,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
 
 bool dw_sgd_pair_enabled(const Sizes& sz) {
   static const int forced = [] { const char* e = std::getenv("PFC_DW_PAIR"); return e ? std::atoi(e) : 1; }();
-  return forced != 0 && sz.M >= 1024 && sz.d % 256 == 0 && sz.k_pad % 256 == 0;
+  return forced != 0 && sz.M >= 2048 && sz.d % 256 == 0 && sz.k_pad % 256 == 0;   // M = 1024: DWF2 is as fast
 }
 
 int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                           const SgdArgs& sa, cudaStream_t s) {
+  // W / V streamed with an L2 evict-first policy (the G tile shared by the pairs of both d-halves stays resident);
+  // PFC_DW_HINT=0 disables
+  static const bool hint = [] { const char* e = std::getenv("PFC_DW_HINT"); return !e || std::atoi(e) != 0; }();
+  auto kern = hint ? k_dw_sgd_pair<true> : k_dw_sgd_pair<false>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dw_sgd_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, DP_SMEM);
+    cudaFuncSetAttribute(k_dw_sgd_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DP_SMEM);
+    cudaFuncSetAttribute(k_dw_sgd_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DP_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);    // G class-major: 128 classes x 64 batch
@@ -267,8 +286,8 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
   DpParams p{};
   p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa;
   const int64_t units = (sz.k_pad / 256) * (sz.d / 256);
-  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));
-  k_dw_sgd_pair<<<2 * pairs, DP_THREADS, DP_SMEM, s>>>(a, b, p);
+  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));   // 74 co-resident
+  kern<<<2 * pairs, DP_THREADS, DP_SMEM, s>>>(a, b, p);
   return 1;
 }
 

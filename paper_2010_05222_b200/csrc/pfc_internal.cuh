@@ -190,7 +190,7 @@ struct SgdArgs {
 };
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& a, cudaStream_t s);
-// dwpair.cu — K11 + K12 on CTA pairs (M >= 1024, d % 256 == 0; PFC_DW_PAIR=0 disables)
+// dwpair.cu — K11 + K12 on CTA pairs (M >= 2048, d % 256 == 0; PFC_DW_PAIR=0 disables)
 bool dw_sgd_pair_enabled(const Sizes& sz);
 int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                           const SgdArgs& sa, cudaStream_t s);

@@ -22,9 +22,10 @@ for (i, name), m in data.items():
 tot = sum(a[1] for a in agg.values())
 sec = {'k_tc_gemm<5>': 'dw_gemm_sgd', 'k_tc_gemm<6>': 'dw_gemm_sgd', 'k_tc_gemm<0>': 'logits_gemm',
        'k_tc_gemm<1>': 'dx_gemm', 'k_gather_w<1>': 'gather_w', 'k_softmax_grad<1, 1>': 'softmax_grad',
-       'k_logits_gather': 'gather_logits', 'k_dwx': 'dwx_sgd'}
+       'k_logits_gather': 'gather_logits', 'k_dwx_t<true>': 'dwx_sgd', 'k_dwx_t<false>': 'dwx_sgd',
+       'k_dw_sgd_pair<true>': 'dw_gemm_sgd', 'k_dw_sgd_pair<false>': 'dw_gemm_sgd', 'k_logits_pair': 'logits_gemm'}
 lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU): cold-cache, serialised launches",
-         "# k_logits_gather = K5+K6 (gather, norms, bf16, logits), k_dwx = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
+         "# k_logits_gather = K5+K6 (gather, norms, bf16, logits), k_dwx_t = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
          "# k_tc_gemm<0> = logits (K6), <1> = dx split-K (K9), <5>/<6> = dW + fused momentum SGD (K11+K12) otherwise",
          "kernel, launches, avg_us, share_of_step, dram_read_MB_per_launch, dram_write_MB_per_launch"]
 traffic = {}

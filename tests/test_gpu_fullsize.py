@@ -36,6 +36,7 @@ def maxrel(a, b):
 
 @pytest.mark.parametrize("C,world,B,r,mt,m", [
     (85_742, 8, 128, 0.1, "arcface", 0.5),     # BASELINE configs[1]
+    (85_742, 8, 256, 0.1, "arcface", 0.5),     # configs[1] shape at M = 2048: logits and dW + SGD on CTA pairs
     (360_232, 8, 128, 0.1, "cosface", 0.4),    # configs[2], r = 0.1
     (360_232, 1, 128, 1.0, "cosface", 0.4),    # configs[2], r = 1.0 (full softmax over 360k classes)
 ])
