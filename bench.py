@@ -351,9 +351,8 @@ def main():
         traffic = {}
         tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tp):
-            tj = json.load(open(tp))
-            if tj.get("workload") == args.config and tj.get("n_gpus", 1) == world:
-                traffic = tj.get("bytes_per_launch", {})
+            tj = json.load(open(tp)).get("workloads", {}).get(f"{args.config}/{world}", {})
+            traffic = tj.get("bytes_per_launch", {})
         entries = [e for e in (roofline_entry(s, ms, n, M, k, d, peaks, traffic) for s, (ms, n) in prof.items()) if e]
         gemm = [prof[s_] for s_ in ("logits_gemm", "gather_logits", "dx_gemm", "dwx_sgd", "dw_gemm_sgd")
                 if s_ in prof and prof[s_][1]]

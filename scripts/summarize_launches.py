@@ -22,8 +22,8 @@ for (i, name), m in data.items():
 tot = sum(a[1] for a in agg.values())
 sec = {'k_tc_gemm<5>': 'dw_gemm_sgd', 'k_tc_gemm<6>': 'dw_gemm_sgd', 'k_tc_gemm<0>': 'logits_gemm',
        'k_tc_gemm<1>': 'dx_gemm', 'k_gather_w<1>': 'gather_w', 'k_softmax_grad<1, 1>': 'softmax_grad',
-       'k_logits_gather': 'gather_logits', 'k_dwx_t<true>': 'dwx_sgd', 'k_dwx_t<false>': 'dwx_sgd',
-       'k_dw_sgd_pair<true>': 'dw_gemm_sgd', 'k_dw_sgd_pair<false>': 'dw_gemm_sgd', 'k_logits_pair': 'logits_gemm'}
+       'k_logits_gather': 'gather_logits', 'k_dwx_t<1>': 'dwx_sgd', 'k_dwx_t<0>': 'dwx_sgd',
+       'k_dw_sgd_pair<1>': 'dw_gemm_sgd', 'k_dw_sgd_pair<0>': 'dw_gemm_sgd', 'k_logits_pair': 'logits_gemm'}
 lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU): cold-cache, serialised launches",
          "# k_logits_gather = K5+K6 (gather, norms, bf16, logits), k_dwx_t = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
          "# k_tc_gemm<0> = logits (K6), <1> = dx split-K (K9), <5>/<6> = dW + fused momentum SGD (K11+K12) otherwise",
@@ -34,6 +34,14 @@ for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     if name in sec:
         traffic[sec[name]] = round((a[2] + a[3]) / a[0])
 open(out, 'w').write("\n".join(lines) + "\n")
-json.dump({"workload": workload, "n_gpus": ngpu, "source": src + " (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)",
-           "bytes_per_launch": traffic}, open('profiles/ncu_traffic.json', 'w'), indent=1)
+tp = 'profiles/ncu_traffic.json'
+try:
+    tj = json.load(open(tp))
+except (OSError, ValueError):
+    tj = {}
+wl = tj.get("workloads", {})
+wl[f"{workload}/{ngpu}"] = {"workload": workload, "n_gpus": ngpu,
+                            "source": src + " (ncu dram__bytes_read.sum + dram__bytes_write.sum per launch)",
+                            "bytes_per_launch": traffic}
+json.dump({"workloads": wl}, open(tp, 'w'), indent=1)
 print("\n".join(lines[2:10]))
