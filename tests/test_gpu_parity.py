@@ -555,3 +555,39 @@ def test_edge_cases(case, precision):
         assert maxrel(L.sampled_grad(), ref["dW"][i]) <= tg
     for L in layers:
         L.close()
+
+
+@pytest.mark.parametrize("C,d,B,precision,fused", [
+    (60_000, 512, 256, "bf16", True),      # k_logits_gather + k_dwx
+    (60_000, 512, 512, "bf16", True),      # k_logits_pair + DWF
+    (60_000, 512, 1024, "bf16", True),     # k_logits_pair + DWF2
+    (60_000, 512, 2048, "bf16", True),     # k_logits_pair + k_dw_sgd_pair
+    (20_000, 256, 300, "fp32", True),      # SIMT contractions
+    (60_000, 512, 256, "bf16", False),     # forward_backward, then K12 k_sgd
+], ids=lambda v: str(v))
+def test_update_touches_exactly_the_sampled_rows(C, d, B, precision, fused):
+    """PAPER.md:146 lazy update: after a step every unsampled row of W and of the momentum V is bit-identical
+    (no stray writes anywhere in the shard), every sampled row is finite and its momentum was written."""
+    L = make_layer(C, d, B, 0.1, "arcface", 0.5, precision, seed=5)
+    W, V = L.params()
+    g = torch.Generator().manual_seed(11)
+    V.copy_(torch.randn(V.shape, generator=g).mul_(1e-3).to(V.device))
+    W0, V0 = W.clone(), V.clone()
+    xs = synth.make_features(4, 0, 1, B, d)
+    ys = synth.make_labels(4, 0, 1, B, C)
+    x, y = torch.from_numpy(xs[0]).cuda(), torch.from_numpy(ys[0]).cuda()
+    gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+    if fused:
+        L.train_step(x, y, gx, loss, lr=0.1)
+    else:
+        L.forward_backward(x, y, gx, loss)
+        L.step(0.1)
+    torch.cuda.synchronize()
+    L.check()
+    idx = torch.from_numpy(L.sampled() - L.shard_start).cuda()
+    mask = torch.ones(W.shape[0], dtype=torch.bool, device="cuda")
+    mask[idx] = False
+    assert torch.equal(W[mask], W0[mask]) and torch.equal(V[mask], V0[mask])
+    assert torch.isfinite(W[idx]).all() and torch.isfinite(V[idx]).all()
+    assert (V[idx] != V0[idx]).any(dim=1).all()
+    L.close()
