@@ -321,6 +321,8 @@ def main():
         rename |= {"logits_gemm": "gather_logits", "gather_w": "target_cos"}
     if flags & layer.PATH_FUSED_DWX:
         rename |= {"dx_gemm": "dwx_sgd"}
+    if flags & layer.PATH_EFORM:                 # E-form: no softmax-gradient pass, section 5 = per-row preparation
+        rename |= {"softmax_grad": "eform_prep"}
     prof = {rename.get(s, s): v for s, v in prof.items()}
     if flags & layer.PATH_FUSED_DWX:
         prof.pop("dw_gemm_sgd", None)        # empty: dW + SGD ran inside dwx_sgd

@@ -235,6 +235,9 @@ int64_t pfc_launch_count(const pfc_ctx* ctx);
 #define PFC_PATH_FUSED_GATHER 2u  /* gather + bf16 + norms + logits in one kernel (global batch M <= 256):
                                      profile section 3 then holds it and section 2 only the target cosines */
 #define PFC_PATH_FUSED_DWX    4u  /* train step: dW + momentum SGD + dX_hat in one kernel (section 6; 8 empty) */
+#define PFC_PATH_EFORM        8u  /* train step with FUSED_DWX: the logits kernel stores E = exp(s c) (bf16) and the
+                                     dW/dX kernel consumes it directly (no softmax-gradient pass; section 5 then
+                                     holds the small per-row preparation). PFC_EFORM=0 at init disables. */
 /* Returns the PFC_PATH_* bits (0 for a NULL context). */
 uint32_t pfc_path_flags(const pfc_ctx* ctx);
 

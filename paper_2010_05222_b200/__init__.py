@@ -309,7 +309,7 @@ class PartialFC:
     def launch_count(self):
         return int(self._lib.pfc_launch_count(self._h))
 
-    PATH_TENSOR_CORES, PATH_FUSED_GATHER, PATH_FUSED_DWX = 1, 2, 4
+    PATH_TENSOR_CORES, PATH_FUSED_GATHER, PATH_FUSED_DWX, PATH_EFORM = 1, 2, 4, 8
 
     def path_flags(self):
         """PFC_PATH_* bits of the kernel path chosen at init (include/pfc.h)."""

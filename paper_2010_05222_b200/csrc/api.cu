@@ -81,6 +81,13 @@ struct pfc_ctx {
   float* split_ws = nullptr;   // split-K partials of the dx GEMM
   float* dWh = nullptr;        // k_pad x d
   float* dotw = nullptr;       // k_pad: w_hat . dW_hat per sampled class (fused SGD)
+  // E-form train step (DESIGN.md f1; use_dwx): cosv holds E = e^{s c} (bf16), no softmax-gradient pass
+  bool eform = false;
+  float* ef_f = nullptr;             // M_pad: f_n = (s/M) e^{-LSE_n}
+  __nv_bfloat16* Xt = nullptr;       // M_pad x d: bf16(f_n x_hat_n)
+  float* dcorr = nullptr;            // k_pad: sum of G_t c_t over each class's target entries
+  float* xch = nullptr;              // k_pad x (d/128): radial-dot partials
+  int* cnt = nullptr;                // k_pad/128
   int* err_dev = nullptr;
   // host-buffer entry point
   float* x_in = nullptr;
@@ -150,7 +157,7 @@ pfc_status device_error(pfc_ctx* c) {
   if (h & ERR_DATA) return set_err(c, PFC_ERR_DATA, "a label is outside [0, num_classes)");
   if (h & ERR_DEGENERATE) return set_err(c, PFC_ERR_DEGENERATE, "a feature or class-centre row has zero norm");
   if (h & ERR_NUMERIC) return set_err(c, PFC_ERR_NUMERIC, "non-finite loss");
-  return set_err(c, PFC_ERR_CUDA, "internal sampler consistency check failed (selected count != k_i)");
+  return set_err(c, PFC_ERR_CUDA, "internal consistency check failed (sampler count != k_i, or a radial-dot exchange timed out)");
 }
 
 pfc_status validate(const pfc_config* c) {
@@ -301,6 +308,17 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   c->fused_gather = c->use_tc && logits_gather_supported(sz);
   c->use_dwx = c->fused_gather && dwx_supported(sz);
   ALLOC(c->split_ws, (size_t)(c->use_tc ? std::max(dx_split_ws_floats(sz), c->use_dwx ? dwx_ws_floats(sz) : 0) : 1) * 4);
+  {
+    const char* e = std::getenv("PFC_EFORM");
+    c->eform = c->use_dwx && sz.d <= 1024 && !(e && e[0] == '0');   // dwx.cu sums <= 8 d-tile partials
+  }
+  if (c->eform) {
+    ALLOC(c->ef_f, Mp * 4);
+    ALLOC(c->Xt, Mp * d * 2);
+    ALLOC(c->dcorr, kp * 4);
+    ALLOC(c->xch, kp * (size_t)(d / 128) * 4);
+    ALLOC(c->cnt, (kp / 128) * 4);
+  }
   ALLOC(c->dWh, kp * d * 4);
   ALLOC(c->dotw, kp * 4);
   ALLOC(c->err_dev, 16);
@@ -314,6 +332,10 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   cudaMemset(c->V, 0, (size_t)sz.C_local * d * 4);
   cudaMemset(c->X32, 0, Mp * d * 4);
   cudaMemset(c->Xb, 0, Mp * d * 2);
+  if (c->eform) {
+    cudaMemset(c->ef_f, 0, Mp * 4);
+    cudaMemset(c->Xt, 0, Mp * d * 2);
+  }
   cudaMemset(c->dXh, 0, Mp * d * 4);
   cudaMemset(c->err_dev, 0, 16);
   cudaMemset(c->step_dev, 0, 16);
@@ -433,7 +455,8 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
   mark(c, 3, s);
   if (c->fused_gather)
     n += launch_logits_gather_tc(sz, c->W, c->idx, c->Xb, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
-                                 c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev, s);
+                                 c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev,
+                                 fused && c->eform, s);
   else if (c->use_tc && logits_pair_enabled(sz))
     n += launch_logits_pair_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->st, c->mp, (__half*)c->cosv,
                                c->partials, s);
@@ -459,12 +482,23 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
   int n = 0;
   n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, s);
   mark(c, 5, s);
+  if (fused && c->eform) {
+    // E-form: no softmax-gradient pass; f, X~ and the target entries, then dW + SGD + dX on E directly
+    n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
+                           (__nv_bfloat16*)c->cosv, c->dcorr, s);
+    mark(c, 6, s);
+    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 0};
+    EformArgs ef{c->ef_f, c->tcol, c->dcorr, c->xch, c->cnt, c->err_dev, c->mp.s};
+    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, c->split_ws, c->dXh, &ef, s);
+    c->launches += n;
+    return;
+  }
   n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
                            fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr, s);
   mark(c, 6, s);
   if (fused && c->use_dwx) {
     SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
-    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, s);
+    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, nullptr, s);
   } else if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
   else
@@ -872,7 +906,7 @@ int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
 uint32_t pfc_path_flags(const pfc_ctx* c) {
   if (!c) return 0u;
   return (c->use_tc ? PFC_PATH_TENSOR_CORES : 0u) | (c->fused_gather ? PFC_PATH_FUSED_GATHER : 0u) |
-         (c->use_dwx ? PFC_PATH_FUSED_DWX : 0u);
+         (c->use_dwx ? PFC_PATH_FUSED_DWX : 0u) | (c->eform ? PFC_PATH_EFORM : 0u);
 }
 
 static const char* kSectionNames[PFC_PROF_SECTIONS] = {

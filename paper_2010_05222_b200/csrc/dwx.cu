@@ -26,7 +26,9 @@ namespace pfc {
 namespace {
 
 constexpr int DX_EPI = 8;
+constexpr int DX_DOTW = 2;                  // E-form: warps forming the radial dot from the E chunks
 constexpr int DX_THREADS = 64 + 32 * DX_EPI;
+constexpr int DX_THREADS_EF = DX_THREADS + 32 * DX_DOTW;
 constexpr int G_CHUNK = 128 * 64 * 2;       // 128 classes x 64 batch columns (bf16, 128-byte swizzle)
 constexpr int G_BUF = 4 * G_CHUNK;          // M_pad <= 256
 constexpr int X_CHUNK = 64 * 128 * 2;       // 64 batch rows x 128 columns (two 64-column swizzled halves)
@@ -47,6 +49,14 @@ struct DwxParams {
   const SamplerState* st;
   SgdArgs sgd;
   float* ws;            // [gper][M][d] dX_hat partials
+  // E-form (DESIGN.md f1): the G operand is E (bf16 e^{s c}, target entries G_t / f_n), the dW operand X~ = f X_hat
+  const float* f;       // [M] f_n = (s/M) e^{-LSE_n}
+  const int32_t* tcol;  // [M] sampled position of row n's target or -1
+  const float* dcorr;   // [k_pad] sum of G_t c_t over the target entries of each sampled class
+  float* xch;           // [nct][n_dt][128] per-d-tile partial radial dots
+  int* cnt;             // [nct] partials published per class tile (zeroed each step)
+  int* err;
+  float s;              // logit scale
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -54,8 +64,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
-template <bool HINT>
-__global__ void __launch_bounds__(DX_THREADS, 1)
+template <bool HINT, bool EF>
+__global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
     k_dwx_t(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX, DwxParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -88,7 +98,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
 
   if (threadIdx.x == 0) {
     mbar_init(g_full, 1); mbar_init(g_empty, 1);
-    for (int i = 0; i < R_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], 1); }
+    for (int i = 0; i < R_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], EF ? 1 + DX_DOTW : 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(&d1_full[i], 1); mbar_init(&d1_empty[i], DX_EPI); }
     mbar_init(wb_full, DX_EPI);
     mbar_init(wb_empty, 1);
@@ -182,6 +192,66 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       else mbar_arrive(d2_full);
     }
     __syncwarp();
+  } else if (warp >= 2 + DX_EPI) {
+    // ---------------------------------------------------------------- E-form radial dot (2 warps)
+    // dotw_j = sum_n G_nj c_nj (the w-normalisation backprop, Eq.6): off the target entries G = f_n E and
+    // c = ln(E)/s, so each E chunk of the dW ring contributes (ln2/s) sum_n f_n E lg2(E); the target entries
+    // (E' = G_t/f_n < 0, clamped away) contribute G_t c_t through dcorr (k_eform_prep). This CTA covers the batch
+    // chunks kb = dt mod n_dt of its class tiles and publishes its partial per class row; the epilogues of the
+    // n_dt d-tile CTAs sum them.
+    if (EF) {
+      const int t = threadIdx.x - 32 * (2 + DX_EPI);    // rows t and t + 64 of the tile
+      const int n_dt = p.d / 128, dt = blockIdx.x / p.gper;
+      const float kc = 0.69314718f / p.s;
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int i = 0; i < ntl; ++i) {
+        const int ct = g + i * p.gper;
+        float B0 = 0.f, B1 = 0.f;   // sum_n f_n E lg2(E) over this CTA's chunks
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&x_full[xs], xph);
+          if (kb % n_dt == dt) {
+            const uint8_t* ga = sR + xs * R_STAGE;
+            const float4* f4 = reinterpret_cast<const float4*>(p.f + kb * 64);
+#pragma unroll 2
+            for (int u = 0; u < 8; ++u) {
+              const uint4 q0 = *reinterpret_cast<const uint4*>(ga + t * 128 + ((u ^ (t & 7)) << 4));
+              const uint4 q1 = *reinterpret_cast<const uint4*>(ga + (t + 64) * 128 + ((u ^ (t & 7)) << 4));
+              const float4 fa = __ldg(f4 + 2 * u), fb = __ldg(f4 + 2 * u + 1);
+              const float fv[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
+              const uint32_t r0[4] = {q0.x, q0.y, q0.z, q0.w}, r1[4] = {q1.x, q1.y, q1.z, q1.w};
+#pragma unroll
+              for (int e2 = 0; e2 < 4; ++e2) {
+                const float e0l = fmaxf(__uint_as_float(r0[e2] << 16), 1e-37f);
+                const float e0h = fmaxf(__uint_as_float(r0[e2] & 0xFFFF0000u), 1e-37f);
+                const float e1l = fmaxf(__uint_as_float(r1[e2] << 16), 1e-37f);
+                const float e1h = fmaxf(__uint_as_float(r1[e2] & 0xFFFF0000u), 1e-37f);
+                float l0l, l0h, l1l, l1h;
+                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0l) : "f"(e0l));
+                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0h) : "f"(e0h));
+                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1l) : "f"(e1l));
+                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1h) : "f"(e1h));
+                const float w0l = e0l * fv[2 * e2], w0h = e0h * fv[2 * e2 + 1];
+                const float w1l = e1l * fv[2 * e2], w1h = e1h * fv[2 * e2 + 1];
+                B0 = fmaf(w0l, l0l, fmaf(w0h, l0h, B0));
+                B1 = fmaf(w1l, l1l, fmaf(w1h, l1h, B1));
+              }
+            }
+          }
+          __syncwarp();
+          if ((t & 31) == 0) mbar_arrive(&x_empty[xs]);
+          if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
+        }
+        float* dst = p.xch + ((int64_t)ct * n_dt + dt) * 128;
+        dst[t] = kc * B0;
+        dst[t + 64] = kc * B1;
+        asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
+        if (t == 0) {
+          __threadfence();
+          atomicAdd(p.cnt + ct, 1);
+        }
+      }
+    }
   } else {
     // ---------------------------------------------------------------- epilogue
     const int ew = warp - 2;
@@ -194,7 +264,7 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
     float nx_inv = 0.f, nx_rad = 0.f;
     if (eset == 0 && ntl > 0) {
       const int prow = g * 128 + row_in;
-      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
     }
     int acc = 0;
     uint32_t aph = 0;
@@ -206,12 +276,35 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
         nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
         if (i + 1 < ntl) {
           const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
-          if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
+          if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
         }
       }
       // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
       mbar_wait(&d1_full[acc], aph);
       tc_fence_after();
+      float rad16 = 0.f;   // E-form: lane l < 16 holds the radial dot of row ew * 16 + l
+      float radp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (EF) {
+        // the radial dots of this warp's 16 rows: the n_dt d-tile CTAs' partials (all CTAs are resident: one per
+        // SM; their dotw warps finish this tile with its dW operands), loads in flight during the staging
+        const int ct = g + i * p.gper, n_dt = p.d / 128;
+        if (lane == 0) {
+          const int* c = p.cnt + ct;
+          int v, spins = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+          } while (v < n_dt && ++spins < (1 << 26));
+          if (v < n_dt) atomicOr(p.err, ERR_INTERNAL);   // never expected: bounded instead of a hang
+        }
+        __syncwarp();
+        if (lane < 16) {   // loads only: summed after the staging
+          const int row = ew * 16 + lane;
+          rad16 = __ldcg(p.dcorr + ct * 128 + row);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < n_dt) radp[q] = __ldcg(p.xch + ((int64_t)ct * n_dt + q) * 128 + row);
+        }
+      }
       {
         const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 128;
 #pragma unroll 1
@@ -233,6 +326,10 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
       // (3) momentum-SGD row updates (rows L2-prefetched a tile ahead), 8 rows in flight per lane; the old w
       // also goes to the bf16 dX operand tile, once dX(t - 1) has read the previous one
       mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));
+      if (EF) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rad16 += radp[q];
+      }
 #pragma unroll 1
       for (int r0 = 0; r0 < 16; r0 += 8) {
         float4 wv[8], mv[8];
@@ -254,13 +351,16 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
         for (int r = 0; r < 8; ++r) {
           const int rr = ew * 16 + r0 + r;
           {
-            const uint2 wb = jr[r] >= 0 ? make_uint2(pack_bf16x2(wv[r].x, wv[r].y), pack_bf16x2(wv[r].z, wv[r].w))
+            const float ws = EF ? s_inv[rr] : 1.f;    // E-form: the dX operand is w_hat (G' carries no 1/||w||)
+            const uint2 wb = jr[r] >= 0 ? make_uint2(pack_bf16x2(wv[r].x * ws, wv[r].y * ws),
+                                                     pack_bf16x2(wv[r].z * ws, wv[r].w * ws))
                                         : make_uint2(0u, 0u);
             const int hc = lane >> 4, cq = lane & 15;   // MN-major swizzled B tile: half hc, row rr, 8 bytes
             *reinterpret_cast<uint2*>(sWb + hc * WB_HALF + rr * 128 + ((((cq >> 1) ^ (rr & 7)) << 4) | ((cq & 1) << 3))) = wb;
           }
           if (jr[r] >= 0) {
-            const float inv = s_inv[rr], rad = s_rad[rr] * inv;
+            const float inv = s_inv[rr];
+            const float rad = (EF ? __shfl_sync(0xffffffffu, rad16, r0 + r) : s_rad[rr]) * inv;
             const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
             float4 w = wv[r], m = mv[r];
             const float oi = p.sgd.gsc ? 1.f : inv;
@@ -321,7 +421,9 @@ __global__ void __launch_bounds__(DX_THREADS, 1)
   }
 }
 
-__global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, const float* __restrict__ ws, float* __restrict__ out) {
+// dX_hat = sum of the split partials (fixed order); E-form: times f_n per batch row (dX_hat_n = f_n sum_j E'_nj w_hat_j)
+__global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
+                            const float* __restrict__ f, float* __restrict__ out) {
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
@@ -330,7 +432,39 @@ __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, const float* 
     const float4 v = *reinterpret_cast<const float4*>(ws + s * stride + i);
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
   }
+  if (f) {
+    const float fn = f[i / d];
+    acc.x *= fn; acc.y *= fn; acc.z *= fn; acc.w *= fn;
+  }
   *reinterpret_cast<float4*>(out + i) = acc;
+}
+
+// E-form preparation, after the global LSE (Alg.1 L8-9 in this representation): f_n = (s/M) e^{-LSE_n};
+// X~ = bf16(f_n x_hat_n) (the dW operand); the target entry E'[t_n][n] = G_t / f_n with
+// G_t = (s/M)(p_t - 1) phi'(c_t) (the cancellation-free p_t - 1 of finalize), and dcorr[t_n] += G_t c_t for the
+// radial dot (several rows may share a class; dcorr zeroed before).
+__global__ void k_eform_prep(int M, int ldm, int d, const float* __restrict__ X32, const float* __restrict__ lse,
+                             const float* __restrict__ gt, const int32_t* __restrict__ tcol,
+                             const float* __restrict__ ct, MarginParams mp, float* __restrict__ f,
+                             __nv_bfloat16* __restrict__ Xt, __nv_bfloat16* __restrict__ E, float* __restrict__ dcorr) {
+  const int n = blockIdx.x;
+  if (n >= M) return;
+  const float gs = mp.s / (float)M;
+  const float fn = gs * expf(-lse[n]);
+  for (int c = threadIdx.x * 2; c < d; c += blockDim.x * 2) {
+    const float2 v = *reinterpret_cast<const float2*>(X32 + (int64_t)n * d + c);
+    *reinterpret_cast<__nv_bfloat162*>(Xt + (int64_t)n * d + c) = __floats2bfloat162_rn(fn * v.x, fn * v.y);
+  }
+  if (threadIdx.x == 0) {
+    f[n] = fn;
+    const int j = tcol[n];
+    if (j >= 0) {
+      const float c_t = ct[n];
+      const float g_t = gs * gt[n] * margin_dphi(mp, c_t);
+      E[(int64_t)j * ldm + n] = __float2bfloat16_rn(g_t / fn);
+      atomicAdd(dcorr + j, g_t * c_t);
+    }
+  }
 }
 
 int dwx_gper(const Sizes& sz) { return std::max(1, num_sms() / (sz.d / 128)); }
@@ -345,26 +479,42 @@ bool dwx_supported(const Sizes& sz) {
 int64_t dwx_ws_floats(const Sizes& sz) { return (int64_t)dwx_gper(sz) * sz.M * sz.d; }
 
 int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
-                  const SgdArgs& sa, float* ws, float* dXh, cudaStream_t s) {
+                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, cudaStream_t s) {
   // W / V streamed with an L2 evict-first policy so that the G' tile re-read for dX stays resident (-0.1 to -0.2 GB
   // of DRAM reads per step at C4); PFC_DWX_HINT=0 disables
   static const bool hint = [] { const char* e = std::getenv("PFC_DWX_HINT"); return !e || std::atoi(e) != 0; }();
-  auto kern = hint ? k_dwx_t<true> : k_dwx_t<false>;
+  auto kern = ef ? (hint ? k_dwx_t<true, true> : k_dwx_t<false, true>)
+                 : (hint ? k_dwx_t<true, false> : k_dwx_t<false, false>);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_dwx_t<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
-    cudaFuncSetAttribute(k_dwx_t<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
+    cudaFuncSetAttribute(k_dwx_t<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
+    cudaFuncSetAttribute(k_dwx_t<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
+    cudaFuncSetAttribute(k_dwx_t<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
+    cudaFuncSetAttribute(k_dwx_t<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
     attr = true;
   }
-  const CUtensorMap tg = make_map(G, sz.k_pad, sz.M_pad, 64, 128);   // G' class-major: 128 classes x 64 batch
-  const CUtensorMap tx = make_map(Xb, sz.M_pad, sz.d, 64, 64);       // X_hat: 64 batch rows x 64 columns
+  const CUtensorMap tg = make_map(G, sz.k_pad, sz.M_pad, 64, 128);   // G' (or E') class-major: 128 classes x 64 batch
+  const CUtensorMap tx = make_map(Xb, sz.M_pad, sz.d, 64, 64);       // X_hat (or X~): 64 batch rows x 64 columns
   DwxParams p{};
   p.M = sz.M; p.d = sz.d; p.nkb = (int)(sz.M_pad / 64); p.gper = dwx_gper(sz); p.st = st; p.sgd = sa; p.ws = ws;
+  if (ef) {
+    p.f = ef->f; p.tcol = ef->tcol; p.dcorr = ef->dcorr; p.xch = ef->xch; p.cnt = ef->cnt; p.err = ef->err;
+    p.s = ef->s;
+    cudaMemsetAsync(ef->cnt, 0, (size_t)(sz.k_pad / 128) * sizeof(int), s);
+  }
   const int grid = p.gper * (sz.d / 128);
-  kern<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+  kern<<<grid, ef ? DX_THREADS_EF : DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
   const int64_t n = (int64_t)sz.M * sz.d;
-  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, ws, dXh);
+  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh);
   return 2;
+}
+
+int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
+                      const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
+                      cudaStream_t s) {
+  cudaMemsetAsync(dcorr, 0, (size_t)sz.k_pad * sizeof(float), s);
+  k_eform_prep<<<sz.M, 128, 0, s>>>(sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr);
+  return 1;
 }
 
 }  // namespace pfc

@@ -64,6 +64,10 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 
+// EF (E-form, DESIGN.md f1): store E = bf16(e^{s c}) (c the fp16-rounded cosine the partials use) instead of the
+// fp16 cosine: the fused dW/dX kernel then consumes E directly (G = (s/M) e^{-LSE_n} E off the target entries), so
+// the softmax-gradient pass over the cosines disappears.
+template <bool EF>
 __global__ void __launch_bounds__(LG_THREADS, 1)
     k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs, LgParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -307,15 +311,31 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
           if (nmx > -INFINITY) {
             const float nb = nmx * sl;
             float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+            if (EF) {   // the terms are kept: E_j = 2^{c sl - nb} 2^{nb} (0 at the target / padding columns)
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) {
-              s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
-              s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
-              s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
-              s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+              for (int j = 0; j < 32; ++j) cf[j] = ex2_ftz(fmaf(cf[j], sl, -nb));
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) { s0 += cf[j]; s1 += cf[j + 1]; s2 += cf[j + 2]; s3 += cf[j + 3]; }
+              const float eb = exp2f(nb);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                const __nv_bfloat162 b = __floats2bfloat162_rn(cf[2 * i] * eb, cf[2 * i + 1] * eb);
+                h2[i] = *reinterpret_cast<const __half2*>(&b);   // bit pattern carried through the store below
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 32; j += 4) {
+                s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
+                s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
+                s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
+                s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+              }
             }
             sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
             mx = nmx;
+          } else if (EF) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) h2[i] = __half2(__ushort_as_half(0), __ushort_as_half(0));
           }
           // class-major store, lane pairs exchanging halves: each 32-bit store covers rows (n, n+1) of one class
           const bool odd = lane & 1;
@@ -374,10 +394,11 @@ bool logits_gather_supported(const Sizes& sz) {
 
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
-                            MarginParams mp, __half* cosv, float2* partials, int* err, cudaStream_t s) {
+                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_logits_gather, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
@@ -388,7 +409,8 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   p.n_ltiles = sz.n_ltiles;
   p.write_ws = write_ws ? 1 : 0;
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
-  k_logits_gather<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
+  if (eform) k_logits_gather<true><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
+  else k_logits_gather<false><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
   return 1;
 }
 

@@ -173,7 +173,7 @@ int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat
 bool logits_gather_supported(const Sizes& sz);
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
-                            MarginParams mp, __half* cosv, float2* partials, int* err, cudaStream_t s);
+                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s);
 // logits2.cu — K6 on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) for M > 256
 bool logits_pair_enabled(const Sizes& sz);
 int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
@@ -197,7 +197,14 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
 // dwx.cu — K9 + K11 + K12 fused for the train step (M <= 256, R25 scaling): dW + SGD update + dX_hat partials
 bool dwx_supported(const Sizes& sz);
 int64_t dwx_ws_floats(const Sizes& sz);
+// E-form (DESIGN.md f1): the logits kernel stored E = e^{s c}; no softmax-gradient pass
+struct EformArgs {
+  const float* f; const int32_t* tcol; const float* dcorr; float* xch; int* cnt; int* err; float s;
+};
 int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
-                  const SgdArgs& sa, float* ws, float* dXh, cudaStream_t s);
+                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, cudaStream_t s);
+int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
+                      const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
+                      cudaStream_t s);
 
 }  // namespace pfc

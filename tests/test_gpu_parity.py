@@ -236,13 +236,17 @@ FUSED_SHAPES = [
 ]
 
 
+@pytest.mark.parametrize("eform", [True, False], ids=["eform", "softmax-grad"])
 @pytest.mark.parametrize("case", FUSED_SHAPES, ids=_case_id)
-def test_fused_kernels_shapes(case):
-    """bf16 train step at M <= 256 runs the fused gather+logits and dW+SGD+dX kernels (path flags 7); two steps
-    against the oracle (loss, grad_x, updated W and V rows)."""
+def test_fused_kernels_shapes(case, eform, monkeypatch):
+    """bf16 train step at M <= 256 runs the fused gather+logits and dW+SGD+dX kernels (path flags 7), by default
+    in E-form (flag 8: no softmax-gradient pass, DESIGN.md f1); two steps against the oracle (loss, grad_x,
+    updated W and V rows)."""
+    if not eform:
+        monkeypatch.setenv("PFC_EFORM", "0")
     C, d, B = case[0], case[1], case[2]
     probe = make_layer(C, d, B, case[3], case[4], case[5], "bf16")
-    assert probe.path_flags() == 7
+    assert probe.path_flags() == (15 if eform else 7)
     probe.close()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
         assert abs(L - Lr) / abs(Lr) <= 1e-3
@@ -253,11 +257,12 @@ def test_fused_kernels_shapes(case):
 
 
 def test_path_flags():
-    """PFC_PATH_* bits: fused kernels only for bf16 at M <= 256; fp32 runs the SIMT contractions."""
+    """PFC_PATH_* bits: fused kernels (and the E-form train step) only for bf16 at M <= 256; fp32 runs the SIMT
+    contractions."""
     a = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "bf16")
     b = make_layer(5000, 256, 257, 0.1, "arcface", 0.5, "bf16")
     c = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "fp32")
-    assert (a.path_flags(), b.path_flags(), c.path_flags()) == (7, 1, 0)
+    assert (a.path_flags(), b.path_flags(), c.path_flags()) == (15, 1, 0)
     for L in (a, b, c):
         L.close()
 
