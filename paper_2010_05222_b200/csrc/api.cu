@@ -82,7 +82,8 @@ struct pfc_ctx {
   float* dWh = nullptr;        // k_pad x d
   float* dotw = nullptr;       // k_pad: w_hat . dW_hat per sampled class (fused SGD)
   // E-form train step (DESIGN.md f1; use_dwx): cosv holds E = e^{s c} (bf16), no softmax-gradient pass
-  bool eform = false;
+  bool eform = false;                // M <= 256: inside the fused dW + SGD + dX kernel
+  bool eform_pair = false;           // M > 256: CTA-pair logits store E, radial dots by k_eform_dotw, dX / dW on E
   float* ef_f = nullptr;             // M_pad: f_n = (s/M) e^{-LSE_n}
   __nv_bfloat16* Xt = nullptr;       // M_pad x d: bf16(f_n x_hat_n)
   float* dcorr = nullptr;            // k_pad: sum of G_t c_t over each class's target entries
@@ -310,12 +311,19 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->split_ws, (size_t)(c->use_tc ? std::max(dx_split_ws_floats(sz), c->use_dwx ? dwx_ws_floats(sz) : 0) : 1) * 4);
   {
     const char* e = std::getenv("PFC_EFORM");
-    c->eform = c->use_dwx && sz.d <= 1024 && !(e && e[0] == '0');   // dwx.cu sums <= 8 d-tile partials
+    // E = e^{s c} must stay finite in bf16/fp32 (s < 88) and f_n = (s/M) e^{-LSE_n}, LSE_n <= s + ln k_i, a
+    // normal fp32 number (s + ln k_i < 80): the paper's s = 64 fits up to k_i ~ 1e7 per shard
+    const double span = (double)c->cfg.scale + std::log((double)sz.k_max);
+    const bool ok = c->cfg.scale <= 80.f && span < 80.0 && !(e && e[0] == '0');
+    c->eform = ok && c->use_dwx && sz.d <= 1024;   // dwx.cu sums <= 8 d-tile partials
+    c->eform_pair = ok && c->use_tc && !c->fused_gather && logits_pair_enabled(sz) && sz.M_pad <= 16384;
   }
-  if (c->eform) {
+  if (c->eform || c->eform_pair) {
     ALLOC(c->ef_f, Mp * 4);
     ALLOC(c->Xt, Mp * d * 2);
     ALLOC(c->dcorr, kp * 4);
+  }
+  if (c->eform) {
     ALLOC(c->xch, kp * (size_t)(d / 128) * 4);
     ALLOC(c->cnt, (kp / 128) * 4);
   }
@@ -332,7 +340,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   cudaMemset(c->V, 0, (size_t)sz.C_local * d * 4);
   cudaMemset(c->X32, 0, Mp * d * 4);
   cudaMemset(c->Xb, 0, Mp * d * 2);
-  if (c->eform) {
+  if (c->eform || c->eform_pair) {
     cudaMemset(c->ef_f, 0, Mp * 4);
     cudaMemset(c->Xt, 0, Mp * d * 2);
   }
@@ -459,7 +467,7 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
                                  fused && c->eform, s);
   else if (c->use_tc && logits_pair_enabled(sz))
     n += launch_logits_pair_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->st, c->mp, (__half*)c->cosv,
-                               c->partials, s);
+                               c->partials, fused && c->eform_pair, s);
   else if (c->use_tc)
     n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);
@@ -493,6 +501,17 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
     c->launches += n;
     return;
   }
+  if (fused && c->eform_pair) {
+    // E-form at M > 256: f, X~, the target entries and the radial dots, then dX_hat = f (E' W_s)
+    n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
+                           (__nv_bfloat16*)c->cosv, c->dcorr, s);
+    n += launch_eform_dotw(sz, (const __nv_bfloat16*)c->cosv, c->ef_f, c->dcorr, c->st, c->mp, c->dotw, s);
+    mark(c, 6, s);
+    n += launch_dx_tc(sz, (const __nv_bfloat16*)c->cosv, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
+                      c->ef_f, s);
+    c->launches += n;
+    return;
+  }
   n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
                            fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr, s);
   mark(c, 6, s);
@@ -500,7 +519,8 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
     SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
     n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, nullptr, s);
   } else if (c->use_tc)
-    n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws, s);
+    n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
+                      nullptr, s);
   else
     n += launch_dx_simt(sz, c->bf16, c->G, c->Ws, c->st, c->dXh, s);
   c->launches += n;
@@ -515,7 +535,10 @@ void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
   } else if (c->use_tc && fused) {
     SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
               c->fused_gather ? 1 : 0};
-    n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, s);
+    if (c->eform_pair)   // dW_hat = E'^T X~ (E-form): same contraction, other operands
+      n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, s);
+    else
+      n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, s);
   } else {
     if (c->use_tc)
       n += launch_dw_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, c->dWh, s);
@@ -906,7 +929,7 @@ int64_t pfc_launch_count(const pfc_ctx* c) { return c ? c->launches : 0; }
 uint32_t pfc_path_flags(const pfc_ctx* c) {
   if (!c) return 0u;
   return (c->use_tc ? PFC_PATH_TENSOR_CORES : 0u) | (c->fused_gather ? PFC_PATH_FUSED_GATHER : 0u) |
-         (c->use_dwx ? PFC_PATH_FUSED_DWX : 0u) | (c->eform ? PFC_PATH_EFORM : 0u);
+         (c->use_dwx ? PFC_PATH_FUSED_DWX : 0u) | (c->eform || c->eform_pair ? PFC_PATH_EFORM : 0u);
 }
 
 static const char* kSectionNames[PFC_PROF_SECTIONS] = {

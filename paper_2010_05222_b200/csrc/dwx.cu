@@ -439,34 +439,6 @@ __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const 
   *reinterpret_cast<float4*>(out + i) = acc;
 }
 
-// E-form preparation, after the global LSE (Alg.1 L8-9 in this representation): f_n = (s/M) e^{-LSE_n};
-// X~ = bf16(f_n x_hat_n) (the dW operand); the target entry E'[t_n][n] = G_t / f_n with
-// G_t = (s/M)(p_t - 1) phi'(c_t) (the cancellation-free p_t - 1 of finalize), and dcorr[t_n] += G_t c_t for the
-// radial dot (several rows may share a class; dcorr zeroed before).
-__global__ void k_eform_prep(int M, int ldm, int d, const float* __restrict__ X32, const float* __restrict__ lse,
-                             const float* __restrict__ gt, const int32_t* __restrict__ tcol,
-                             const float* __restrict__ ct, MarginParams mp, float* __restrict__ f,
-                             __nv_bfloat16* __restrict__ Xt, __nv_bfloat16* __restrict__ E, float* __restrict__ dcorr) {
-  const int n = blockIdx.x;
-  if (n >= M) return;
-  const float gs = mp.s / (float)M;
-  const float fn = gs * expf(-lse[n]);
-  for (int c = threadIdx.x * 2; c < d; c += blockDim.x * 2) {
-    const float2 v = *reinterpret_cast<const float2*>(X32 + (int64_t)n * d + c);
-    *reinterpret_cast<__nv_bfloat162*>(Xt + (int64_t)n * d + c) = __floats2bfloat162_rn(fn * v.x, fn * v.y);
-  }
-  if (threadIdx.x == 0) {
-    f[n] = fn;
-    const int j = tcol[n];
-    if (j >= 0) {
-      const float c_t = ct[n];
-      const float g_t = gs * gt[n] * margin_dphi(mp, c_t);
-      E[(int64_t)j * ldm + n] = __float2bfloat16_rn(g_t / fn);
-      atomicAdd(dcorr + j, g_t * c_t);
-    }
-  }
-}
-
 int dwx_gper(const Sizes& sz) { return std::max(1, num_sms() / (sz.d / 128)); }
 
 }  // namespace
@@ -507,14 +479,6 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   const int64_t n = (int64_t)sz.M * sz.d;
   k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh);
   return 2;
-}
-
-int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
-                      const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
-                      cudaStream_t s) {
-  cudaMemsetAsync(dcorr, 0, (size_t)sz.k_pad * sizeof(float), s);
-  k_eform_prep<<<sz.M, 128, 0, s>>>(sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr);
-  return 1;
 }
 
 }  // namespace pfc

@@ -556,14 +556,18 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
 }
 
 // Deterministic split-K reduction: dX[r][c] = sum_s ws[s][r][c] (fixed split order).
-__global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, const float* __restrict__ ws,
-                                float* __restrict__ out) {
+__global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
+                                const float* __restrict__ rowscale, float* __restrict__ out) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
   for (int s = 1; s < nsplit; ++s) {
     float4 v = *reinterpret_cast<const float4*>(ws + s * stride + i);
     acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+  }
+  if (rowscale) {   // E-form: dX_hat_n = f_n sum_j E'_nj w_hat_j
+    const float r = rowscale[i / d];
+    acc.x *= r; acc.y *= r; acc.z *= r; acc.w *= r;
   }
   *reinterpret_cast<float4*>(out + i) = acc;
 }
@@ -619,7 +623,7 @@ int64_t dx_split_ws_floats(const Sizes& sz) {
 }
 
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st, float* dXh,
-                 float* split_ws, cudaStream_t s) {
+                 float* split_ws, const float* rowscale, cudaStream_t s) {
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 64);      // Gc class-major, MN-major A
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 64);
   TcParams p{};
@@ -631,7 +635,7 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
   if (dtile(sz) == 256) launch<DX>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
   else launch<DX128>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
   const int64_t n = (int64_t)sz.M * sz.d;
-  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, split_ws, dXh);
+  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, sz.d, split_ws, rowscale, dXh);
   return 2;
 }
 

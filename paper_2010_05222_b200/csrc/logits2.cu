@@ -13,6 +13,7 @@
 //   warps 2-17 epilogue (each CTA its 128 rows): four sets of 4 warps, 64 columns each; the two sets of a
 //              128-column logits tile combine their (max, sum) through shared memory; TMEM release is signalled
 //              to the leader's barrier (remote arrive for the peer CTA)
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <algorithm>
 #include <cstdlib>
@@ -43,6 +44,10 @@ struct L2Params {
   int n_ltiles;
 };
 
+// EF (E-form train step, DESIGN.md f1): store E = bf16(e^{s c}) of the fp16-rounded cosine the partials use (0 at
+// the target and padding columns) instead of the cosine; the softmax-gradient pass then disappears (dX / dW
+// contract E directly, see k_eform_prep / k_eform_dotw)
+template <bool EF>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     k_logits_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, L2Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -172,15 +177,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         if (nmx > -INFINITY) {
           const float nb = nmx * sl;
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+          if (EF) {   // the terms are kept: E_j = 2^{c sl - nb} 2^{nb}
 #pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
-            s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
-            s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
-            s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+            for (int j = 0; j < 32; ++j) cf[j] = ex2_ftz(fmaf(cf[j], sl, -nb));
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) { s0 += cf[j]; s1 += cf[j + 1]; s2 += cf[j + 2]; s3 += cf[j + 3]; }
+            const float eb = exp2f(nb);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const __nv_bfloat162 b = __floats2bfloat162_rn(cf[2 * i] * eb, cf[2 * i + 1] * eb);
+              h2[i] = *reinterpret_cast<const __half2*>(&b);   // bit pattern carried through the store below
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) {
+              s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
+              s1 += ex2_ftz(fmaf(cf[j + 1], sl, -nb));
+              s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
+              s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
+            }
           }
           sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
           mx = nmx;
+        } else if (EF) {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) h2[i] = __half2(__ushort_as_half(0), __ushort_as_half(0));
         }
         const bool odd = lane & 1;
         __half* cb = p.cosv + (row & ~1);
@@ -231,10 +252,12 @@ bool logits_pair_enabled(const Sizes& sz) {
 }
 
 int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
-                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, cudaStream_t s) {
+                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
+                          cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_logits_pair, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
@@ -245,7 +268,8 @@ int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_b
   p.n_ltiles = sz.n_ltiles;
   const int64_t units = ((sz.M + 255) / 256) * (sz.k_pad / 256);
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));
-  k_logits_pair<<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+  if (eform) k_logits_pair<true><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+  else k_logits_pair<false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
   return 1;
 }
 

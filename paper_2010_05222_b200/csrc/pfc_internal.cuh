@@ -177,9 +177,11 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
 // logits2.cu — K6 on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) for M > 256
 bool logits_pair_enabled(const Sizes& sz);
 int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
-                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, cudaStream_t s);
+                          const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
+                          cudaStream_t s);
+// dX_hat = G W_s (split-K + fixed-order reduction); rowscale (E-form f_n, or NULL) multiplies each output row
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,
-                 float* dXh, float* split_ws, cudaStream_t s);
+                 float* dXh, float* split_ws, const float* rowscale, cudaStream_t s);
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                  float* dWh, cudaStream_t s);
 // Fused K11 + K12: dW_hat tile in TMEM -> g = (dw_hat - w_hat dot)/||w||,
@@ -203,8 +205,11 @@ struct EformArgs {
 };
 int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                   const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, cudaStream_t s);
+// eform.cu — E-form preparation (f_n, X~, target entries of E) and the radial dots for the unfused-dX path
 int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
                       const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
                       cudaStream_t s);
+int launch_eform_dotw(const Sizes& sz, const __nv_bfloat16* E, const float* f, const float* dcorr,
+                      const SamplerState* st, MarginParams mp, float* dotw, cudaStream_t s);
 
 }  // namespace pfc

@@ -256,14 +256,43 @@ def test_fused_kernels_shapes(case, eform, monkeypatch):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
+PAIR_SHAPES = [
+    # train step at M > 256: CTA-pair logits, split-K dX, DWF / DWF2 / pair dW + SGD kernels
+    (40000, 512, 300, 0.1, "arcface", 0.5, "init", 0.0),      # M = 300 (M_pad 384): DWF, ragged M tile
+    (30000, 256, 520, 0.1, "cosface", 0.4, "init", 0.0),      # d = 256 (256-wide dX tiles), M = 520
+    (60000, 512, 1024, 0.05, "arcface", 0.5, "trained", 0.055),  # M = 1024: DWF2, trained-like (peaked softmax)
+    (60000, 512, 2048, 0.05, "arcface", 0.5, "init", 0.0),    # M = 2048: pair dW + SGD (the per-rank C4 shape)
+]
+
+
+@pytest.mark.parametrize("eform", [True, False], ids=["eform", "softmax-grad"])
+@pytest.mark.parametrize("case", PAIR_SHAPES, ids=_case_id)
+def test_pair_kernels_train_step(case, eform, monkeypatch):
+    """bf16 train step at M > 256 (path flags 1, plus 8 in E-form: the pair logits kernel stores E = e^{s c},
+    k_eform_dotw forms the radial dots, dX and dW + SGD contract E directly); two steps against the oracle."""
+    if not eform:
+        monkeypatch.setenv("PFC_EFORM", "0")
+    C, d, B = case[0], case[1], case[2]
+    probe = make_layer(C, d, B, case[3], case[4], case[5], "bf16")
+    assert probe.path_flags() == (9 if eform else 1)
+    probe.close()
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
+        assert abs(L - Lr) / abs(Lr) <= 1e-3
+        assert maxrel(gx, gxr) <= 2e-2
+        assert maxrel(Vn, Vnr) <= 2e-2
+        assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
 def test_path_flags():
-    """PFC_PATH_* bits: fused kernels (and the E-form train step) only for bf16 at M <= 256; fp32 runs the SIMT
-    contractions."""
+    """PFC_PATH_* bits: fused kernels only for bf16 at M <= 256, the E-form train step for bf16 at any M (CTA-pair
+    logits at M > 256); fp32 runs the SIMT contractions."""
     a = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "bf16")
     b = make_layer(5000, 256, 257, 0.1, "arcface", 0.5, "bf16")
     c = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "fp32")
-    assert (a.path_flags(), b.path_flags(), c.path_flags()) == (15, 1, 0)
-    for L in (a, b, c):
+    # E = e^{s c} would overflow bf16 / fp32 past s ~ 88 (and f_n underflow past s + ln k ~ 80): no E-form
+    e = make_layer(5000, 256, 64, 0.1, "arcface", 0.5, "bf16", scale=96.0)
+    assert (a.path_flags(), b.path_flags(), c.path_flags(), e.path_flags()) == (15, 9, 0, 7)
+    for L in (a, b, c, e):
         L.close()
 
 
