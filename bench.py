@@ -121,6 +121,8 @@ def kernel_work(section, M, k, d):
         return [(16.0 * k * d, "byte", "hbm")]
     if section == "softmax_grad":
         return [(4.0 * M * k, "byte", "hbm")]          # fp16 cosine in, bf16 gradient out (design minimum)
+    if section == "eform_dotw":
+        return [(2.0 * M * k, "byte", "hbm")]          # E-form radial dots: the bf16 E entries read once
     return None
 
 
@@ -321,8 +323,9 @@ def main():
         rename |= {"logits_gemm": "gather_logits", "gather_w": "target_cos"}
     if flags & layer.PATH_FUSED_DWX:
         rename |= {"dx_gemm": "dwx_sgd"}
-    if flags & layer.PATH_EFORM:                 # E-form: no softmax-gradient pass, section 5 = per-row preparation
-        rename |= {"softmax_grad": "eform_prep"}
+    if flags & layer.PATH_EFORM:                 # E-form: no softmax-gradient pass; section 5 = per-row preparation
+        # (+ the radial-dot pass over E when dX is not fused into the dW kernel)
+        rename |= {"softmax_grad": "eform_prep" if flags & layer.PATH_FUSED_DWX else "eform_dotw"}
     prof = {rename.get(s, s): v for s, v in prof.items()}
     if flags & layer.PATH_FUSED_DWX:
         prof.pop("dw_gemm_sgd", None)        # empty: dW + SGD ran inside dwx_sgd
