@@ -148,7 +148,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
-      float mx = -INFINITY, sum = 0.f;
+      float mx = EF ? 0.f : -INFINITY, sum = 0.f;   // EF: unshifted sums (s + ln k < 80, api.cu)
 #pragma unroll 1
       for (int c = eset * 2; c < eset * 2 + 2; ++c) {
         uint32_t v[32];
@@ -168,27 +168,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           for (int j = 0; j < 32; ++j)
             if (col0 + j >= k || col0 + j == tc) cf[j] = -INFINITY;
         }
-        float q0 = cf[0], q1 = cf[1], q2 = cf[2], q3 = cf[3];
-#pragma unroll
-        for (int j = 4; j < 32; j += 4) {
-          q0 = fmaxf(q0, cf[j]); q1 = fmaxf(q1, cf[j + 1]); q2 = fmaxf(q2, cf[j + 2]); q3 = fmaxf(q3, cf[j + 3]);
-        }
-        const float nmx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
-        if (nmx > -INFINITY) {
-          const float nb = nmx * sl;
+        if (EF) {   // E_j = e^{s c_j} = 2^{c_j s log2 e} unshifted (0 at the target / padding columns: c = -inf)
           float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
-          if (EF) {   // the terms are kept: E_j = 2^{c sl - nb} 2^{nb}
 #pragma unroll
-            for (int j = 0; j < 32; ++j) cf[j] = ex2_ftz(fmaf(cf[j], sl, -nb));
+          for (int j = 0; j < 32; ++j) cf[j] = ex2_ftz(cf[j] * sl);
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) { s0 += cf[j]; s1 += cf[j + 1]; s2 += cf[j + 2]; s3 += cf[j + 3]; }
-            const float eb = exp2f(nb);
+          for (int j = 0; j < 32; j += 4) { s0 += cf[j]; s1 += cf[j + 1]; s2 += cf[j + 2]; s3 += cf[j + 3]; }
+          sum += (s0 + s1) + (s2 + s3);
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const __nv_bfloat162 b = __floats2bfloat162_rn(cf[2 * i] * eb, cf[2 * i + 1] * eb);
-              h2[i] = *reinterpret_cast<const __half2*>(&b);   // bit pattern carried through the store below
-            }
-          } else {
+          for (int i = 0; i < 16; ++i) {
+            const __nv_bfloat162 b = __floats2bfloat162_rn(cf[2 * i], cf[2 * i + 1]);
+            h2[i] = *reinterpret_cast<const __half2*>(&b);   // bit pattern carried through the store below
+          }
+        } else {
+          float q0 = cf[0], q1 = cf[1], q2 = cf[2], q3 = cf[3];
+#pragma unroll
+          for (int j = 4; j < 32; j += 4) {
+            q0 = fmaxf(q0, cf[j]); q1 = fmaxf(q1, cf[j + 1]); q2 = fmaxf(q2, cf[j + 2]); q3 = fmaxf(q3, cf[j + 3]);
+          }
+          const float nmx = fmaxf(mx, fmaxf(fmaxf(q0, q1), fmaxf(q2, q3)));
+          if (nmx > -INFINITY) {
+            const float nb = nmx * sl;
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
 #pragma unroll
             for (int j = 0; j < 32; j += 4) {
               s0 += ex2_ftz(fmaf(cf[j], sl, -nb));
@@ -196,12 +197,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
               s2 += ex2_ftz(fmaf(cf[j + 2], sl, -nb));
               s3 += ex2_ftz(fmaf(cf[j + 3], sl, -nb));
             }
+            sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
+            mx = nmx;
           }
-          sum = (mx > -INFINITY ? sum * ex2_ftz((mx - nmx) * sl) : 0.f) + ((s0 + s1) + (s2 + s3));
-          mx = nmx;
-        } else if (EF) {
-#pragma unroll
-          for (int i = 0; i < 16; ++i) h2[i] = __half2(__ushort_as_half(0), __ushort_as_half(0));
         }
         const bool odd = lane & 1;
         __half* cb = p.cosv + (row & ~1);

@@ -233,16 +233,22 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
       g = 0.f;
     } else if (!(gm > -INFINITY) || S == 0.f) {   // no negative in the sampled set: p_t = 1
       ls = z; L = 0.f; g = 0.f;
-    } else if (z >= gm) {
-      const float q = S * __expf(gm - z);
-      L = log1pf(q);
-      ls = z + L;
-      g = -q / (1.f + q);
     } else {
-      const float t = __expf(z - gm);
-      ls = gm + __logf(S + t);
-      L = ls - z;
-      g = t / (S + t) - 1.f;
+      // lS = log of the non-target sum; whichever side dominates, the exponent is <= 0 (no overflow) and
+      // neither p_t - 1 nor the loss is formed by cancellation (R22). Holds for any shift gm (the E-form
+      // logits kernels report unshifted sums, gm = 0).
+      const float lS = gm + __logf(S);
+      if (z >= lS) {
+        const float q = __expf(lS - z);
+        L = log1pf(q);
+        ls = z + L;
+        g = -q / (1.f + q);
+      } else {
+        const float r = __expf(z - lS);
+        ls = lS + log1pf(r);
+        L = ls - z;
+        g = -1.f / (1.f + r);
+      }
     }
     lse[n] = ls;
     gt[n] = g;

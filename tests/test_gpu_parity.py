@@ -471,10 +471,11 @@ def test_nccl_collectives_single_rank(monkeypatch, B):
     solo.close()
 
 
-def test_cuda_graph_replay_matches_eager():
+@pytest.mark.parametrize("B", [64, 640], ids=["fused-M64", "pair-M640"])
+def test_cuda_graph_replay_matches_eager(B):
     """pfc_train_step on a capturable stream is captured once and replayed as a CUDA graph (device-side step
-    counter and learning rate); results must match the eager launches on the legacy stream."""
-    C, d, B = 30000, 512, 64
+    counter and learning rate; both kernel paths); results must match the eager launches on the legacy stream."""
+    C, d = 30000, 512
     eager = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
     graph = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
     ys = [synth.make_labels(3, i, 1, B, C)[0] for i in range(4)]
