@@ -247,8 +247,9 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
         dst[t + 64] = kc * B1;
         asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
         if (t == 0) {
-          __threadfence();
-          atomicAdd(p.cnt + ct, 1);
+          // release (cumulative over the bar.sync above): the 64 threads' partials are visible at gpu scope
+          // before the count (the epilogues poll it with acquire loads)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.cnt + ct) : "memory");
         }
       }
     }
