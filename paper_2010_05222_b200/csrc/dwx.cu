@@ -283,7 +283,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
       mbar_wait(&d1_full[acc], aph);
       tc_fence_after();
-      float rad16 = 0.f;   // E-form: lane l < 16 holds the radial dot of row ew * 16 + l
+      float rad16 = 0.f;   // E-form: lane l < 16 forms the radial dot of row ew * 16 + l
       float radp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (EF) {
         // the radial dots of this warp's 16 rows: the n_dt d-tile CTAs' partials (all CTAs are resident: one per
@@ -327,9 +327,11 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       // (3) momentum-SGD row updates (rows L2-prefetched a tile ahead), 8 rows in flight per lane; the old w
       // also goes to the bf16 dX operand tile, once dX(t - 1) has read the previous one
       mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));
-      if (EF) {
+      if (EF) {   // into the per-row slot the update loop reads (a shuffle there serialises the row updates)
 #pragma unroll
         for (int q = 0; q < 8; ++q) rad16 += radp[q];
+        if (lane < 16) s_rad[ew * 16 + lane] = rad16;
+        __syncwarp();
       }
 #pragma unroll 1
       for (int r0 = 0; r0 < 16; r0 += 8) {
@@ -361,7 +363,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           }
           if (jr[r] >= 0) {
             const float inv = s_inv[rr];
-            const float rad = (EF ? __shfl_sync(0xffffffffu, rad16, r0 + r) : s_rad[rr]) * inv;
+            const float rad = s_rad[rr] * inv;
             const float4 g4 = s_tile[rr * 32 + (lane ^ (rr & 31))];
             float4 w = wv[r], m = mv[r];
             const float oi = p.sgd.gsc ? 1.f : inv;
