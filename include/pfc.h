@@ -235,9 +235,12 @@ int64_t pfc_launch_count(const pfc_ctx* ctx);
 #define PFC_PATH_FUSED_GATHER 2u  /* gather + bf16 + norms + logits in one kernel (global batch M <= 256):
                                      profile section 3 then holds it and section 2 only the target cosines */
 #define PFC_PATH_FUSED_DWX    4u  /* train step: dW + momentum SGD + dX_hat in one kernel (section 6; 8 empty) */
-#define PFC_PATH_EFORM        8u  /* train step with FUSED_DWX: the logits kernel stores E = exp(s c) (bf16) and the
-                                     dW/dX kernel consumes it directly (no softmax-gradient pass; section 5 then
-                                     holds the small per-row preparation). PFC_EFORM=0 at init disables. */
+#define PFC_PATH_EFORM        8u  /* train step (bf16, tensor cores, s <= 80 and s + ln k_i < 80; R26): the
+                                     logits kernel stores E = exp(s c) (bf16) and the dX / dW + SGD kernels contract
+                                     it directly, no softmax-gradient pass. Section 5 then holds the per-row
+                                     preparation (with FUSED_DWX) or that plus the radial-dot pass over E (M > 256).
+                                     pfc_forward_backward keeps the softmax-gradient form. PFC_EFORM=0 at init
+                                     disables. */
 /* Returns the PFC_PATH_* bits (0 for a NULL context). */
 uint32_t pfc_path_flags(const pfc_ctx* ctx);
 
