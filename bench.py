@@ -213,6 +213,8 @@ def main():
     ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--params", default="device", choices=["device", "host"],
+                    help="where W and V live: HBM (default) or page-locked host memory (capacity mode, f4)")
     ap.add_argument("--cpu-budget", type=float, default=20.0)
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
@@ -246,11 +248,21 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     layer = pfc.PartialFC.from_process_group(**dict(
         num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m, momentum=MOMENTUM,
-        weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local)) if world > 1 else \
+        weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
+        param_location=args.params)) if world > 1 else \
         pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m,
-                      momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local)
+                      momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
+                      param_location=args.params)
     W, V = layer.params()
-    synth.fill_w_shard(W, 1, layer.shard_start)
+    if args.params == "host":       # page-locked host shard: rows generated on the GPU, copied
+        tmp = torch.empty(1 << 18, d, device="cuda")
+        for r0 in range(0, layer.shard_size, tmp.shape[0]):
+            n = min(tmp.shape[0], layer.shard_size - r0)
+            synth.fill_w_shard(tmp[:n], 1, layer.shard_start + r0)
+            W[r0:r0 + n].copy_(tmp[:n])
+        del tmp
+    else:
+        synth.fill_w_shard(W, 1, layer.shard_start)
     V.zero_()
     M, k = layer.global_batch, layer.k_max
     # synthetic init-like batches, resident in HBM before the timed region
@@ -376,7 +388,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": desc, "num_classes": C, "dim": d, "batch_per_gpu": B, "global_batch": M,
                        "sample_rate": r, "k_per_gpu": k, "shard_rows": layer.shard_size, "margin": f"{mt} {m}",
-                       "scale": SCALE, "parallelism": f"class-parallel x{world}",
+                       "scale": SCALE, "parallelism": f"class-parallel x{world}", "params": args.params,
                        "l2": "inputs larger than L2 (W+V shard %.1f GB, %.1f GB of sampled rows per step)"
                              % (2 * layer.shard_size * d * 4 / 1e9, k * d * 4 / 1e9)},
             "clocks": clk.summary(),

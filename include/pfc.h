@@ -65,6 +65,14 @@ typedef enum { PFC_COMM_NCCL = 0, PFC_COMM_LOOPBACK = 1 } pfc_comm_mode;
  *                       sampled set and gets no positive pull. */
 typedef enum { PFC_SAMPLE_PPRN = 0, PFC_SAMPLE_PPRN_PAPER = 1, PFC_SAMPLE_RANDOM = 2 } pfc_sample_mode;
 
+/* Where the W and V shards live (the paper keeps W in host RAM past GPU memory, PAPER.md:344,
+ * PAPER.md:357).
+ * PFC_PARAMS_DEVICE  HBM (the default; up to ~100M classes per 8 B200).
+ * PFC_PARAMS_HOST    page-locked, device-mapped host memory: the same kernels gather the sampled rows and write
+ *                    their updates through the mapping (PCIe / C2C bandwidth instead of HBM); capacity mode for
+ *                    shards beyond HBM. The rest of the workspace stays in HBM. */
+typedef enum { PFC_PARAMS_DEVICE = 0, PFC_PARAMS_HOST = 1 } pfc_param_location;
+
 typedef struct {
   int64_t num_classes;   /* C >= world_size      */
   int32_t dim;           /* d, multiple of 128 in [128, 1024] (512 in the paper)      */
@@ -85,6 +93,7 @@ typedef struct {
                                  comm_mode == PFC_COMM_NCCL                                               */
   int32_t comm_mode;     /* pfc_comm_mode                                                                */
   int32_t sample_mode;   /* pfc_sample_mode                                                              */
+  int32_t param_location; /* pfc_param_location                                                         */
 } pfc_config;
 
 typedef struct pfc_ctx pfc_ctx;
@@ -171,9 +180,10 @@ pfc_status pfc_shard_range(const pfc_ctx* ctx, int64_t* start, int64_t* count);
 /* Sizes: M = world_size * B, k_max = max(ceil(r C_local), min(M, C_local)) (the workspace bound). */
 pfc_status pfc_sizes(const pfc_ctx* ctx, int64_t* M, int64_t* k_max);
 
-/* Device pointers to the library-owned W and V shards ([C_local][d] float32). The caller may read or
- * write them between calls (stream-ordered on the stream it uses). */
-pfc_status pfc_param_ptrs(pfc_ctx* ctx, float** W_dev, float** V_dev);
+/* Pointers to the library-owned W and V shards ([C_local][d] float32): device pointers with
+ * PFC_PARAMS_DEVICE, host pointers (page-locked) with PFC_PARAMS_HOST. The caller may read or write them
+ * between calls (stream-ordered on the stream it uses; host memory after synchronising it). */
+pfc_status pfc_param_ptrs(pfc_ctx* ctx, float** W, float** V);
 
 /* Sampled global class ids of the last forward_backward, ascending (R4), and k_i.
  * idx_host has room for `capacity` entries (>= k_i, else PFC_ERR_CONTRACT with *k_out set). */

@@ -43,13 +43,16 @@ class PfcError(RuntimeError):
         self.status = status
 
 
+PARAM_LOCATIONS = {"device": 0, "host": 1}
+
+
 class _Config(ctypes.Structure):
     _fields_ = [("num_classes", ctypes.c_int64), ("dim", ctypes.c_int32), ("batch", ctypes.c_int32),
                 ("sample_rate", ctypes.c_double), ("scale", ctypes.c_float), ("margin_type", ctypes.c_int32),
                 ("margin", ctypes.c_float), ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("precision", ctypes.c_int32), ("seed", ctypes.c_uint64), ("rank", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("comm_mode", ctypes.c_int32), ("sample_mode", ctypes.c_int32)]
+                ("comm_mode", ctypes.c_int32), ("sample_mode", ctypes.c_int32), ("param_location", ctypes.c_int32)]
 
 
 _lib = None
@@ -133,8 +136,9 @@ class PartialFC:
 
     def __init__(self, num_classes, dim, batch, sample_rate=0.1, scale=64.0, margin_type="arcface", margin=0.5,
                  momentum=0.9, weight_decay=0.0, precision="bf16", seed=0, rank=0, world_size=1, device=0,
-                 nccl_unique_id=None, comm_mode="nccl", sample_mode="pprn"):
+                 nccl_unique_id=None, comm_mode="nccl", sample_mode="pprn", param_location="device"):
         self._lib = load_library()
+        self.param_location = param_location
         self.rank, self.world_size, self.device = rank, world_size, device
         self.dim, self.batch, self.num_classes = dim, batch, num_classes
         self._id_buf = ctypes.create_string_buffer(bytes(nccl_unique_id), 128) if nccl_unique_id else None
@@ -144,7 +148,8 @@ class PartialFC:
                       PRECISIONS[precision] if isinstance(precision, str) else int(precision), int(seed), rank,
                       world_size, device, ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf else None,
                       COMM_MODES[comm_mode] if isinstance(comm_mode, str) else int(comm_mode),
-                      SAMPLE_MODES[sample_mode] if isinstance(sample_mode, str) else int(sample_mode))
+                      SAMPLE_MODES[sample_mode] if isinstance(sample_mode, str) else int(sample_mode),
+                      PARAM_LOCATIONS[param_location])
         h = ctypes.c_void_p()
         s = self._lib.pfc_init(ctypes.byref(cfg), ctypes.byref(h))
         if s:
@@ -217,11 +222,16 @@ class PartialFC:
 
     # -------------------------------------------------------------- state / introspection
     def params(self):
-        """(W, V) zero-copy torch views of the library-owned [C_local, d] float32 shards."""
+        """(W, V) zero-copy torch views of the library-owned [C_local, d] float32 shards: CUDA tensors, or CPU
+        tensors over the page-locked host memory with param_location="host" (synchronise before touching them)."""
         import torch
         W, V = ctypes.c_void_p(), ctypes.c_void_p()
         self._check(self._lib.pfc_param_ptrs(self._h, ctypes.byref(W), ctypes.byref(V)))
         shape = (self.shard_size, self.dim)
+        if self.param_location == "host":
+            n = self.shard_size * self.dim
+            return tuple(torch.frombuffer((ctypes.c_float * n).from_address(p.value), dtype=torch.float32).view(shape)
+                         for p in (W, V))
         dev = torch.device("cuda", self.device)
         return (torch.as_tensor(_DevArray(W.value, shape, "<f4"), device=dev),
                 torch.as_tensor(_DevArray(V.value, shape, "<f4"), device=dev))

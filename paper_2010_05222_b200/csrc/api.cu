@@ -40,6 +40,9 @@ struct pfc_ctx {
   cudaStream_t last_stream = nullptr;
   int64_t launches = 0;
   std::vector<void*> allocs;
+  std::vector<void*> host_allocs;   // PFC_PARAMS_HOST: page-locked, device-mapped W and V
+  float* W_host = nullptr;          // host addresses of W / V in that mode (c->W / c->V are the device mapping)
+  float* V_host = nullptr;
 
   // parameters
   float* W = nullptr;
@@ -183,6 +186,8 @@ pfc_status validate(const pfc_config* c) {
   if (!(c->weight_decay >= 0.f)) return set_err(nullptr, PFC_ERR_CONFIG, "weight_decay must be >= 0");
   if (c->sample_mode < PFC_SAMPLE_PPRN || c->sample_mode > PFC_SAMPLE_RANDOM)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown sample_mode");
+  if (c->param_location != PFC_PARAMS_DEVICE && c->param_location != PFC_PARAMS_HOST)
+    return set_err(nullptr, PFC_ERR_CONFIG, "unknown param_location");
   if (c->comm_mode != PFC_COMM_NCCL && c->comm_mode != PFC_COMM_LOOPBACK)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown comm_mode");
   if (c->comm_mode == PFC_COMM_LOOPBACK && c->world_size > kMaxLoopback)
@@ -275,8 +280,30 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   pfc_status s = PFC_OK;
 #define ALLOC(p, bytes) \
   if ((s = dalloc(c, &(p), (bytes))) != PFC_OK) { g_init_error = c->err; pfc_destroy(c); return s; }
-  ALLOC(c->W, (size_t)sz.C_local * d * 4);
-  ALLOC(c->V, (size_t)sz.C_local * d * 4);
+  if (cfg->param_location == PFC_PARAMS_HOST) {
+    for (int t = 0; t < 2; ++t) {
+      void* h = nullptr;
+      void* dp = nullptr;
+      const size_t bytes = (size_t)sz.C_local * d * 4;
+      cudaError_t e = cudaHostAlloc(&h, std::max<size_t>(bytes, 16), cudaHostAllocMapped | cudaHostAllocPortable);
+      if (e == cudaSuccess) e = cudaHostGetDevicePointer(&dp, h, 0);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        if (h) cudaFreeHost(h);
+        s = set_err(c, PFC_ERR_OOM, std::string("page-locked host allocation of W / V failed: ") + cudaGetErrorString(e));
+        g_init_error = c->err;
+        pfc_destroy(c);
+        return s;
+      }
+      c->host_allocs.push_back(h);
+      std::memset(h, 0, bytes);
+      (t == 0 ? c->W_host : c->V_host) = static_cast<float*>(h);
+      (t == 0 ? c->W : c->V) = static_cast<float*>(dp);
+    }
+  } else {
+    ALLOC(c->W, (size_t)sz.C_local * d * 4);
+    ALLOC(c->V, (size_t)sz.C_local * d * 4);
+  }
   ALLOC(c->xh_local, B * d * 4);
   ALLOC(c->xnorm, B * 4);
   ALLOC(c->X32, Mp * d * 4);
@@ -336,8 +363,10 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->y_in, B * 8);
   ALLOC(c->gx_out, B * d * 4);
 #undef ALLOC
-  cudaMemset(c->W, 0, (size_t)sz.C_local * d * 4);
-  cudaMemset(c->V, 0, (size_t)sz.C_local * d * 4);
+  if (!c->W_host) {
+    cudaMemset(c->W, 0, (size_t)sz.C_local * d * 4);
+    cudaMemset(c->V, 0, (size_t)sz.C_local * d * 4);
+  }
   cudaMemset(c->X32, 0, Mp * d * 4);
   cudaMemset(c->Xb, 0, Mp * d * 2);
   if (c->eform || c->eform_pair) {
@@ -405,6 +434,7 @@ pfc_status pfc_destroy(pfc_ctx* c) {
   for (auto& ev : c->prof_ev)
     for (auto& e : ev) cudaEventDestroy(e);
   for (void* p : c->allocs) cudaFree(p);
+  for (void* p : c->host_allocs) cudaFreeHost(p);
   delete c;
   return PFC_OK;
 }
@@ -816,8 +846,8 @@ pfc_status pfc_sizes(const pfc_ctx* c, int64_t* M, int64_t* k_max) {
 
 pfc_status pfc_param_ptrs(pfc_ctx* c, float** W, float** V) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
-  if (W) *W = c->W;
-  if (V) *V = c->V;
+  if (W) *W = c->W_host ? c->W_host : c->W;
+  if (V) *V = c->V_host ? c->V_host : c->V;
   return PFC_OK;
 }
 
@@ -904,8 +934,8 @@ pfc_status pfc_get_state(pfc_ctx* c, float* W_host, float* V_host, uint64_t* ste
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   const size_t bytes = (size_t)c->sz.C_local * c->sz.d * sizeof(float);
   CUDA_TRY(c, cudaDeviceSynchronize());
-  if (W_host) CUDA_TRY(c, cudaMemcpy(W_host, c->W, bytes, cudaMemcpyDeviceToHost));
-  if (V_host) CUDA_TRY(c, cudaMemcpy(V_host, c->V, bytes, cudaMemcpyDeviceToHost));
+  if (W_host) CUDA_TRY(c, cudaMemcpy(W_host, c->W, bytes, cudaMemcpyDefault));
+  if (V_host) CUDA_TRY(c, cudaMemcpy(V_host, c->V, bytes, cudaMemcpyDefault));
   if (step) *step = c->step;
   return device_error(c);
 }
@@ -914,8 +944,8 @@ pfc_status pfc_set_state(pfc_ctx* c, const float* W_host, const float* V_host, c
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   const size_t bytes = (size_t)c->sz.C_local * c->sz.d * sizeof(float);
   CUDA_TRY(c, cudaDeviceSynchronize());
-  if (W_host) CUDA_TRY(c, cudaMemcpy(c->W, W_host, bytes, cudaMemcpyHostToDevice));
-  if (V_host) CUDA_TRY(c, cudaMemcpy(c->V, V_host, bytes, cudaMemcpyHostToDevice));
+  if (W_host) CUDA_TRY(c, cudaMemcpy(c->W, W_host, bytes, cudaMemcpyDefault));
+  if (V_host) CUDA_TRY(c, cudaMemcpy(c->V, V_host, bytes, cudaMemcpyDefault));
   if (step) {
     CUDA_TRY(c, cudaMemcpy(c->step_dev, step, sizeof(*step), cudaMemcpyHostToDevice));
     c->step = *step;

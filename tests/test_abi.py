@@ -30,7 +30,7 @@ def test_library_loads_and_exports_every_declared_symbol():
 def _cfg(**kw):
     base = dict(num_classes=1000, dim=128, batch=8, sample_rate=0.1, scale=64.0, margin_type=1, margin=0.5,
                 momentum=0.9, weight_decay=0.0, precision=1, seed=0, rank=0, world_size=1, device=0,
-                nccl_unique_id=None, comm_mode=0, sample_mode=0)
+                nccl_unique_id=None, comm_mode=0, sample_mode=0, param_location=0)
     base.update(kw)
     return pfc._Config(**base)
 
@@ -39,7 +39,8 @@ def _cfg(**kw):
     dict(sample_rate=0.0), dict(sample_rate=1.5), dict(num_classes=3, world_size=4, rank=0, comm_mode=1),
     dict(dim=100), dict(batch=0), dict(scale=0.0), dict(margin_type=1, margin=1.6), dict(margin_type=2, margin=1.0),
     dict(margin_type=7), dict(precision=3), dict(rank=2, world_size=2, comm_mode=1), dict(world_size=2, rank=0),
-    dict(momentum=1.0), dict(comm_mode=5), dict(sample_mode=3), dict(sample_mode=-1),
+    dict(momentum=1.0), dict(comm_mode=5), dict(sample_mode=3), dict(sample_mode=-1), dict(param_location=2),
+    dict(param_location=-1),
 ])
 def test_config_errors_are_reported_synchronously(bad):
     lib = pfc.load_library()

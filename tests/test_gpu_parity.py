@@ -34,10 +34,10 @@ def maxrel(a, b):
 
 
 def make_layer(C, d, B, r, margin_type, m, precision, seed=0, wseed=1, world=1, rank=0, comm="nccl", mu=0.9,
-               lam=5e-4, scale=64.0):
+               lam=5e-4, scale=64.0, params="device"):
     layer = pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, scale=scale, margin_type=margin_type,
                           margin=m, momentum=mu, weight_decay=lam, precision=precision, seed=seed, rank=rank,
-                          world_size=world, comm_mode=comm)
+                          world_size=world, comm_mode=comm, param_location=params)
     W, V = layer.params()
     synth.fill_w_shard(W, wseed, layer.shard_start)
     V.zero_()
@@ -281,6 +281,39 @@ def test_pair_kernels_train_step(case, eform, monkeypatch):
         assert maxrel(gx, gxr) <= 2e-2
         assert maxrel(Vn, Vnr) <= 2e-2
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
+@pytest.mark.parametrize("B,fused", [(96, True), (640, True), (96, False)], ids=["fused-M96", "pair-M640", "fb+step"])
+def test_host_resident_params_match_device(B, fused):
+    """SURVEY.md §8(f) f4 (capacity mode): W and V in page-locked, device-mapped host memory run the same kernels
+    through the mapping — the results equal the HBM-resident layer's bit for bit (loss, grad_x, W, V)."""
+    C, d = 40000, 512
+    dev = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=6)
+    host = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=6, params="host")
+    Wh, Vh = host.params()
+    assert Wh.device.type == "cpu" and Wh.shape == (C, d)
+    for i in range(2):
+        y = torch.from_numpy(synth.make_labels(5, i, 1, B, C)[0]).cuda()
+        x = torch.from_numpy(synth.make_features(5, i, 1, B, d)[0]).cuda()
+        out = []
+        for L in (dev, host):
+            gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+            if fused:
+                L.train_step(x, y, gx, loss, lr=0.1)
+            else:
+                L.forward_backward(x, y, gx, loss)
+                L.step(0.1)
+            L.check()
+            out.append((loss.item(), gx.cpu()))
+        assert out[0][0] == out[1][0]
+        assert torch.equal(out[0][1], out[1][1])
+    torch.cuda.synchronize()
+    Wd, Vd = dev.params()
+    assert torch.equal(Wd.cpu(), Wh) and torch.equal(Vd.cpu(), Vh)
+    W2, V2, st = host.get_state()
+    assert np.array_equal(W2, Wh.numpy()) and st == 2
+    dev.close()
+    host.close()
 
 
 def test_path_flags():
