@@ -5,6 +5,9 @@ timeout 600 python bench.py > gpurun_out/prof/bench_c4.json 2> gpurun_out/prof/b
 timeout 300 python bench.py --config c4rank --steps 30 --warmup 5 > gpurun_out/prof/bench_c4rank.json 2>/dev/null
 timeout 300 python bench.py --config c4rank2 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c4rank2.json 2>/dev/null
 timeout 300 python bench.py --config c4rank4 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c4rank4.json 2>/dev/null
+timeout 300 python bench.py --config c3 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c3.json 2>/dev/null
+timeout 300 python bench.py --config c2 --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/prof/bench_c2.json 2>/dev/null
+timeout 600 python bench.py --config c3 --params host --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c3_host.json 2>/dev/null
 timeout 600 python bench.py --config c5rank --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/prof/bench_c5rank.json 2>/dev/null
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:^k_ -c 300 --csv --log-file gpurun_out/prof/launches_c4.csv python bench.py --config c4 --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_launch.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:^k_ -c 300 --csv --log-file gpurun_out/prof/launches_c4rank.csv python bench.py --config c4rank --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/prof/ncu_launch2.log 2>&1

@@ -108,11 +108,11 @@ TINY_CASES = [
 ]
 
 
-def _run_single(case, precision, steps=2, fused=False):
+def _run_single(case, precision, steps=2, fused=False, scale=64.0):
     C, d, B, r, mt, m, dist, sigma = case
     lr = 0.1
-    layer = make_layer(C, d, B, r, mt, m, precision, seed=3, wseed=1)
-    cfg = ocfg(C, d, B, r, mt, m, seed=3)
+    layer = make_layer(C, d, B, r, mt, m, precision, seed=3, wseed=1, scale=scale)
+    cfg = ocfg(C, d, B, r, mt, m, seed=3, scale=scale)
     Vh = {}
     Wcur = {}
 
@@ -314,6 +314,21 @@ def test_host_resident_params_match_device(B, fused):
     assert np.array_equal(W2, Wh.numpy()) and st == 2
     dev.close()
     host.close()
+
+
+@pytest.mark.parametrize("B", [96, 320], ids=["fused-M96", "pair-M320"])
+@pytest.mark.parametrize("scale", [16.0, 72.0])
+def test_eform_scale_range(B, scale):
+    """E-form (R26) at the ends of its scale gate: E = e^{s c} unshifted and f_n = (s/M) e^{-LSE_n} at s = 72
+    (the gate's edge: s + ln k = 79.6 < 80 with k = 2000) and at a small s; train step against the oracle."""
+    case = (40000, 512, B, 0.05, "arcface", 0.5, "init", 0.0)
+    probe = make_layer(40000, 512, B, 0.05, "arcface", 0.5, "bf16", scale=scale)
+    assert probe.path_flags() & probe.PATH_EFORM
+    probe.close()
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True, scale=scale):
+        assert abs(L - Lr) / abs(Lr) <= 1e-3
+        assert maxrel(gx, gxr) <= 2e-2
+        assert maxrel(Vn, Vnr) <= 2e-2
 
 
 def test_path_flags():
