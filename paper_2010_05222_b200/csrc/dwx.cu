@@ -26,7 +26,10 @@ namespace pfc {
 namespace {
 
 constexpr int DX_EPI = 8;
-constexpr int DX_DOTW = 2;                  // E-form: warps forming the radial dot from the E chunks
+#ifndef PFC_DX_DOTW
+#define PFC_DX_DOTW 2
+#endif
+constexpr int DX_DOTW = PFC_DX_DOTW;        // E-form: warps forming the radial dot from the E chunks
 constexpr int DX_THREADS = 64 + 32 * DX_EPI;
 constexpr int DX_THREADS_EF = DX_THREADS + 32 * DX_DOTW;
 constexpr int G_CHUNK = 128 * 64 * 2;       // 128 classes x 64 batch columns (bf16, 128-byte swizzle)
@@ -200,14 +203,17 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
     // chunks kb = dt mod n_dt of its class tiles and publishes its partial per class row; the epilogues of the
     // n_dt d-tile CTAs sum them.
     if (EF) {
-      const int t = threadIdx.x - 32 * (2 + DX_EPI);    // rows t and t + 64 of the tile
+      constexpr int RPT = 128 / (32 * DX_DOTW);        // tile rows per thread: t, t + 32 DX_DOTW, ...
+      const int t = threadIdx.x - 32 * (2 + DX_EPI);
       const int n_dt = p.d / 128, dt = blockIdx.x / p.gper;
       const float kc = 0.69314718f / p.s;
       int xs = 0;
       uint32_t xph = 0;
       for (int i = 0; i < ntl; ++i) {
         const int ct = g + i * p.gper;
-        float B0 = 0.f, B1 = 0.f;   // sum_n f_n E lg2(E) over this CTA's chunks
+        float B[RPT];   // sum_n f_n E lg2(E) over this CTA's chunks
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) B[q] = 0.f;
         for (int kb = 0; kb < nkb; ++kb) {
           mbar_wait(&x_full[xs], xph);
           if (kb % n_dt == dt) {
@@ -215,26 +221,22 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
             const float4* f4 = reinterpret_cast<const float4*>(p.f + kb * 64);
 #pragma unroll 2
             for (int u = 0; u < 8; ++u) {
-              const uint4 q0 = *reinterpret_cast<const uint4*>(ga + t * 128 + ((u ^ (t & 7)) << 4));
-              const uint4 q1 = *reinterpret_cast<const uint4*>(ga + (t + 64) * 128 + ((u ^ (t & 7)) << 4));
               const float4 fa = __ldg(f4 + 2 * u), fb = __ldg(f4 + 2 * u + 1);
               const float fv[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
-              const uint32_t r0[4] = {q0.x, q0.y, q0.z, q0.w}, r1[4] = {q1.x, q1.y, q1.z, q1.w};
 #pragma unroll
-              for (int e2 = 0; e2 < 4; ++e2) {
-                const float e0l = fmaxf(__uint_as_float(r0[e2] << 16), 1e-37f);
-                const float e0h = fmaxf(__uint_as_float(r0[e2] & 0xFFFF0000u), 1e-37f);
-                const float e1l = fmaxf(__uint_as_float(r1[e2] << 16), 1e-37f);
-                const float e1h = fmaxf(__uint_as_float(r1[e2] & 0xFFFF0000u), 1e-37f);
-                float l0l, l0h, l1l, l1h;
-                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0l) : "f"(e0l));
-                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l0h) : "f"(e0h));
-                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1l) : "f"(e1l));
-                asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(l1h) : "f"(e1h));
-                const float w0l = e0l * fv[2 * e2], w0h = e0h * fv[2 * e2 + 1];
-                const float w1l = e1l * fv[2 * e2], w1h = e1h * fv[2 * e2 + 1];
-                B0 = fmaf(w0l, l0l, fmaf(w0h, l0h, B0));
-                B1 = fmaf(w1l, l1l, fmaf(w1h, l1h, B1));
+              for (int q = 0; q < RPT; ++q) {
+                const int row = t + q * 32 * DX_DOTW;
+                const uint4 qv = *reinterpret_cast<const uint4*>(ga + row * 128 + ((u ^ (row & 7)) << 4));
+                const uint32_t r[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                  const float el = fmaxf(__uint_as_float(r[e2] << 16), 1e-37f);
+                  const float eh = fmaxf(__uint_as_float(r[e2] & 0xFFFF0000u), 1e-37f);
+                  float ll, lh;
+                  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(ll) : "f"(el));
+                  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lh) : "f"(eh));
+                  B[q] = fmaf(el * fv[2 * e2], ll, fmaf(eh * fv[2 * e2 + 1], lh, B[q]));
+                }
               }
             }
           }
@@ -243,12 +245,13 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
         }
         float* dst = p.xch + ((int64_t)ct * n_dt + dt) * 128;
-        dst[t] = kc * B0;
-        dst[t + 64] = kc * B1;
-        asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) dst[t + q * 32 * DX_DOTW] = kc * B[q];
+        if (DX_DOTW > 1) asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
+        else __syncwarp();
         if (t == 0) {
-          // release (cumulative over the bar.sync above): the 64 threads' partials are visible at gpu scope
-          // before the count (the epilogues poll it with acquire loads)
+          // release (cumulative over the barrier above): the partials are visible at gpu scope before the count
+          // (the epilogues poll it with acquire loads)
           asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.cnt + ct) : "memory");
         }
       }
