@@ -434,6 +434,38 @@ def test_host_buffer_entry_matches_device_entry():
     assert torch.equal(gh, gd.cpu()) and lh.item() == ld.item()
 
 
+@pytest.mark.parametrize("B", [32, 320], ids=["fused-M32", "pair-M320"])
+def test_host_train_step_graph_matches_device(B):
+    """pfc_train_step_host on a capturable stream (the step itself graph-replayed between the copies): four steps
+    with changing inputs in the same pinned buffers must equal the device-buffer entry's results exactly."""
+    C, d = 30000, 256
+    a = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=2)
+    b = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=2)
+    xh = torch.empty(B, d).pin_memory()
+    yh = torch.empty(B, dtype=torch.int64).pin_memory()
+    gh = torch.empty(B, d).pin_memory()
+    lh = torch.zeros(1).pin_memory()
+    xd, yd = torch.empty(B, d, device="cuda"), torch.empty(B, dtype=torch.int64, device="cuda")
+    gd, ld = torch.empty(B, d, device="cuda"), torch.zeros(1, device="cuda")
+    side = torch.cuda.Stream()
+    for i in range(4):
+        xh.copy_(torch.from_numpy(synth.make_features(6, i, 1, B, d)[0]))
+        yh.copy_(torch.from_numpy(synth.make_labels(6, i, 1, B, C)[0]))
+        with torch.cuda.stream(side):
+            a.train_step_host(xh, yh, gh, lh, lr=0.05, stream=side)
+            xd.copy_(xh)
+            yd.copy_(yh)
+            b.train_step(xd, yd, gd, ld, lr=0.05, stream=side)
+        torch.cuda.synchronize()
+        assert torch.equal(gh, gd.cpu()) and lh.item() == ld.item(), i
+        assert np.array_equal(a.sampled(), b.sampled())
+    Wa, Va = a.params()
+    Wb, Vb = b.params()
+    assert torch.equal(Wa, Wb) and torch.equal(Va, Vb)
+    a.close()
+    b.close()
+
+
 def test_device_errors_are_reported():
     C, d, B = 1000, 128, 8
     layer = make_layer(C, d, B, 0.1, "arcface", 0.5, "fp32")
