@@ -331,6 +331,25 @@ def test_eform_scale_range(B, scale):
         assert maxrel(Vn, Vnr) <= 2e-2
 
 
+@pytest.mark.parametrize("cfg", ["c4", "c4rank"])
+def test_full_size_bench_workloads(cfg):
+    """The bench's own workloads at full size, in the launch configuration bench.py times (bf16 fused train step):
+    C4 on one GPU (10M classes, B = 256, k = 1M: fused gather + logits and dW + SGD + dX kernels, E-form) and the
+    per-rank shape of the 8-GPU C4 job (1.25M classes, M = 2048: CTA-pair kernels, radial-dot pass). One step
+    against the float64 oracle: sampled ids bit-exact, loss, grad_x, and the updated W / V of every sampled row."""
+    case = {"c4": (10_000_000, 512, 256, 0.1, "arcface", 0.5, "init", 0.0),
+            "c4rank": (1_250_000, 512, 2048, 0.1, "arcface", 0.5, "init", 0.0)}[cfg]
+    probe = make_layer(case[0], 512, case[2], 0.1, "arcface", 0.5, "bf16")
+    assert probe.path_flags() == (15 if cfg == "c4" else 9)
+    probe.close()
+    torch.cuda.empty_cache()
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", steps=1, fused=True):
+        assert abs(L - Lr) / abs(Lr) <= 1e-3
+        assert maxrel(gx, gxr) <= 2e-2
+        assert maxrel(Vn, Vnr) <= 2e-2
+        assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
 def test_path_flags():
     """PFC_PATH_* bits: fused kernels only for bf16 at M <= 256, the E-form train step for bf16 at any M (CTA-pair
     logits at M > 256); fp32 runs the SIMT contractions."""
