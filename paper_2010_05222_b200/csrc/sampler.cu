@@ -40,8 +40,20 @@ __global__ void __launch_bounds__(kThreads) k_keys_hist(int64_t a, int64_t C_loc
   __shared__ int sh[2048];
   for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
   __syncthreads();
-  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < C_local; j += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t h = philox_class_key((uint64_t)(a + j), step, seed);
+  // two independent Philox chains per thread and iteration (the 10 dependent rounds of one key leave the
+  // integer-multiply pipe idle otherwise)
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; j + stride < C_local; j += 2 * stride) {
+    const uint32_t h0 = philox_class_key((uint64_t)(a + j), step, seed);
+    const uint32_t h1 = philox_class_key((uint64_t)(a + j + stride), step, seed);
+    keys[j] = h0;
+    keys[j + stride] = h1;
+    if (!is_pos(bits, j)) atomicAdd(&sh[h0 >> 21], 1);
+    if (!is_pos(bits, j + stride)) atomicAdd(&sh[h1 >> 21], 1);
+  }
+  if (j < C_local) {
+    const uint32_t h = philox_class_key((uint64_t)(a + j), step, seed);
     keys[j] = h;
     if (!is_pos(bits, j)) atomicAdd(&sh[h >> 21], 1);
   }
