@@ -350,6 +350,28 @@ def test_full_size_bench_workloads(cfg):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
+@pytest.mark.parametrize("B", [64, 512], ids=["fused-M64", "pair-M512"])
+def test_training_reduces_the_loss(B):
+    """Functional check of the whole optimiser loop: repeated train steps on a fixed batch (the sampler redraws the
+    negatives every step; every positive is always sampled) pull the features' class centres in, so the loss
+    falls steadily; parameters and gradients stay finite."""
+    C, d = 20000, 256
+    L = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=9)
+    y = torch.from_numpy(synth.make_labels(9, 0, 1, B, C)[0]).cuda()
+    x = torch.from_numpy(synth.make_features(9, 0, 1, B, d)[0]).cuda()
+    gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+    losses = []
+    for i in range(30):
+        L.train_step(x, y, gx, loss, lr=0.5)
+        losses.append(loss.item())
+    L.check()
+    W, V = L.params()
+    assert torch.isfinite(W).all() and torch.isfinite(V).all() and torch.isfinite(gx).all()
+    assert losses[-1] < 0.9 * losses[0], losses
+    assert sum(b < a for a, b in zip(losses, losses[1:])) >= 25, losses
+    L.close()
+
+
 def test_path_flags():
     """PFC_PATH_* bits: fused kernels only for bf16 at M <= 256, the E-form train step for bf16 at any M (CTA-pair
     logits at M > 256); fp32 runs the SIMT contractions."""
