@@ -33,6 +33,13 @@ constexpr int L2_HALF = 128 * L2_BK * 2;                // 16 KB: 128 rows x 64 
 constexpr int L2_STAGE = 2 * L2_HALF;                   // A half + B half
 constexpr int L2_PART = L2_ACC * 2 * 128 * 8;           // s_part: [acc][ltile pair][row] float2
 constexpr int L2_SMEM = L2_STAGES * L2_STAGE + 1024 + 256 + L2_PART;
+// ARES (A resident, d <= 512): this CTA's 128 rows of X_hat stay in shared memory for the whole kernel (each pair
+// keeps one 256-row M tile and walks class tiles), only the W_s tiles stream: half the operand traffic from L2
+constexpr int L2R_KB = 8;                               // d / 64 <= 8
+constexpr int L2R_A = L2R_KB * L2_HALF;                 // 128 KB
+constexpr int L2R_STAGES = 5;                           // B ring: 16 KB stages
+constexpr int L2R_SMEM = L2R_A + L2R_STAGES * L2_HALF + 1024 + 256 + L2_PART;
+static_assert(L2_SMEM <= 232448 && L2R_SMEM <= 232448, "shared memory overflow");
 static_assert(L2_SMEM <= 232448, "shared memory overflow");
 struct L2Params {
   int M, ldm, d;
@@ -47,29 +54,44 @@ struct L2Params {
 // EF (E-form train step, DESIGN.md f1): store E = bf16(e^{s c}) of the fp16-rounded cosine the partials use (0 at
 // the target and padding columns) instead of the cosine; the softmax-gradient pass then disappears (dX / dW
 // contract E directly, see k_eform_prep / k_eform_dotw)
-template <bool EF>
+template <bool EF, bool ARES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     k_logits_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, L2Params p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L2_STAGES * L2_STAGE);   // leader: both CTAs' bytes
-  uint64_t* empty = full + L2_STAGES;                                           // each CTA: MMA done with stage
-  uint64_t* acc_full = empty + L2_STAGES;                                       // each CTA
+  constexpr int NST = ARES ? L2R_STAGES : L2_STAGES;               // ring stages
+  constexpr int STB = ARES ? L2_HALF : L2_STAGE;                   // ring stage bytes (ARES: B only)
+  constexpr int RING0 = ARES ? L2R_A : 0;                          // ring offset (ARES: after the resident A)
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + RING0 + NST * STB);   // leader: both CTAs' bytes
+  uint64_t* empty = full + NST;                                                 // each CTA: MMA done with stage
+  uint64_t* acc_full = empty + NST;                                             // each CTA
   uint64_t* acc_empty = acc_full + L2_ACC;                                      // leader: both CTAs' epilogues
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + L2_ACC);
-  float2* s_part = reinterpret_cast<float2*>(smem + L2_STAGES * L2_STAGE + 256);
+  uint64_t* a_full = acc_empty + L2_ACC;                                        // ARES: the resident A landed
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(a_full + 1);
+  float2* s_part = reinterpret_cast<float2*>(smem + RING0 + NST * STB + 256);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
   const bool leader = rank == 0;
   const int k = p.st->k;
   const int mt = (p.M + 255) / 256, nt = (k + 255) / 256;
-  const int n_units = mt * nt, n_kb = p.d / L2_BK;
+  const int n_kb = p.d / L2_BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // units: M fastest, so concurrent pairs share the W_s tile in L2. ARES: pair p keeps M tile p % mt and takes
+  // the class tiles g, g + G, ... of its group g = p / mt (npairs = G mt); the pairs of a group run the same class
+  // tile at the same time
+  const int G = ARES ? npairs / mt : 1;
+  const int n_units = ARES ? (pair / mt < G ? (nt - pair / mt + G - 1) / G : 0) : mt * nt;
+  auto unit = [&](int i, int& m0, int& n0) {
+    if (ARES) { m0 = (pair % mt) * 256; n0 = (pair / mt + i * G) * 256; }
+    else { const int u = pair + i * npairs; m0 = (u % mt) * 256; n0 = (u / mt) * 256; }
+  };
+  const int n_iter = ARES ? n_units : (pair < n_units ? (n_units - pair + npairs - 1) / npairs : 0);
 
   if (threadIdx.x == 0) {
-    for (int i = 0; i < L2_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
+    for (int i = 0; i < NST; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
     for (int i = 0; i < L2_ACC; ++i) { mbar_init(&acc_full[i], 1); mbar_init(&acc_empty[i], 2 * L2_EPI); }
+    mbar_init(a_full, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_smem();
   }
@@ -89,15 +111,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < n_units; u += npairs) {
-        const int m0 = (u % mt) * 256, n0 = (u / mt) * 256;
+      if (ARES && n_iter > 0) {   // this CTA's 128 rows of X_hat, all K blocks, once
+        int m0, n0;
+        unit(0, m0, n0);
+        if (leader) mbar_expect_tx(a_full, (uint32_t)(2 * n_kb * L2_HALF));
+        for (int kb = 0; kb < n_kb; ++kb)
+          tma_load_2d_pair(smem + kb * L2_HALF, &tmA, a_full, kb * L2_BK, m0 + 128 * (int)rank);
+      }
+      for (int it = 0; it < n_iter; ++it) {
+        int m0, n0;
+        unit(it, m0, n0);
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
-          if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * L2_HALF));
-          uint8_t* sa = smem + stage * L2_STAGE;
-          tma_load_2d_pair(sa, &tmA, &full[stage], kb * L2_BK, m0 + 128 * (int)rank);
-          tma_load_2d_pair(sa + L2_HALF, &tmB, &full[stage], kb * L2_BK, n0 + 128 * (int)rank);
-          if (++stage == L2_STAGES) { stage = 0; phase ^= 1; }
+          uint8_t* sa = smem + RING0 + stage * STB;
+          if (ARES) {
+            if (leader) mbar_expect_tx(&full[stage], (uint32_t)(2 * L2_HALF));
+            tma_load_2d_pair(sa, &tmB, &full[stage], kb * L2_BK, n0 + 128 * (int)rank);
+          } else {
+            if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * L2_HALF));
+            tma_load_2d_pair(sa, &tmA, &full[stage], kb * L2_BK, m0 + 128 * (int)rank);
+            tma_load_2d_pair(sa + L2_HALF, &tmB, &full[stage], kb * L2_BK, n0 + 128 * (int)rank);
+          }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
       }
     }
@@ -107,7 +142,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       constexpr uint32_t IDESC = make_idesc(256, 256, false, false);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = pair; u < n_units; u += npairs) {
+      if (ARES && n_iter > 0) {
+        mbar_wait(a_full, 0);
+        tc_fence_after();
+      }
+      for (int it = 0; it < n_iter; ++it) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tacc = tmem_base + acc * 256;
@@ -115,7 +154,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           mbar_wait(&full[stage], phase);
           tc_fence_after();
           if (lane == 0) {
-            const uint32_t sa = smem_u32(smem + stage * L2_STAGE), sb = sa + L2_HALF;
+            const uint32_t sst = smem_u32(smem + RING0 + stage * STB);
+            const uint32_t sa = ARES ? smem_u32(smem + kb * L2_HALF) : sst, sb = ARES ? sst : sst + L2_HALF;
 #pragma unroll
             for (int kk = 0; kk < L2_BK / 16; ++kk)
               tc_mma_pair(tacc, make_desc(sa + kk * 32, 16, 1024), make_desc(sb + kk * 32, 16, 1024), IDESC,
@@ -123,7 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
             tc_commit_pair(&empty[stage]);
           }
           __syncwarp();
-          if (++stage == L2_STAGES) { stage = 0; phase ^= 1; }
+          if (++stage == NST) { stage = 0; phase ^= 1; }
         }
         if (lane == 0) tc_commit_pair(&acc_full[acc]);
         __syncwarp();
@@ -140,8 +180,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     const uint32_t acc_empty_leader = leader_addr(&acc_empty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < n_units; u += npairs) {
-      const int m0 = (u % mt) * 256, n0 = (u / mt) * 256;
+    for (int it = 0; it < n_iter; ++it) {
+      int m0, n0;
+      unit(it, m0, n0);
       const int row = m0 + 128 * (int)rank + row_in;
       const bool rv = row < p.M;
       const int tc = rv ? p.tcol[row] : -1;
@@ -254,8 +295,10 @@ int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_b
                           cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_logits_pair<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
-    cudaFuncSetAttribute(k_logits_pair<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2R_SMEM);
+    cudaFuncSetAttribute(k_logits_pair<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2R_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
@@ -264,10 +307,21 @@ int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_b
   p.M = sz.M; p.ldm = (int)sz.M_pad; p.d = sz.d; p.st = st; p.tcol = tcol;
   p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
-  const int64_t units = ((sz.M + 255) / 256) * (sz.k_pad / 256);
-  const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));
-  if (eform) k_logits_pair<true><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
-  else k_logits_pair<false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+  const int mt = (int)((sz.M + 255) / 256);
+  const int max_pairs = num_sms() / 2;
+  static const bool ares_on = [] { const char* e = std::getenv("PFC_LOGITS_ARES"); return !e || std::atoi(e) != 0; }();
+  if (ares_on && sz.d <= 64 * L2R_KB && mt <= max_pairs) {
+    const int64_t nt = sz.k_pad / 256;
+    const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / mt, nt));
+    const int pairs = groups * mt;
+    if (eform) k_logits_pair<true, true><<<2 * pairs, L2_THREADS, L2R_SMEM, s>>>(a, b, p);
+    else k_logits_pair<false, true><<<2 * pairs, L2_THREADS, L2R_SMEM, s>>>(a, b, p);
+  } else {
+    const int64_t units = (int64_t)mt * (sz.k_pad / 256);
+    const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, max_pairs));
+    if (eform) k_logits_pair<true, false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+    else k_logits_pair<false, false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+  }
   return 1;
 }
 
