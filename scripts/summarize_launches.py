@@ -27,7 +27,9 @@ sec = {'k_tc_gemm<5>': 'dw_gemm_sgd', 'k_tc_gemm<6>': 'dw_gemm_sgd', 'k_tc_gemm<
        # E-form train step (template <HINT, EF> / <EF>)
        'k_dwx_t<1, 1>': 'dwx_sgd', 'k_dwx_t<1, 0>': 'dwx_sgd', 'k_dwx_t<0, 1>': 'dwx_sgd', 'k_dwx_t<0, 0>': 'dwx_sgd',
        'k_logits_gather<1>': 'gather_logits', 'k_logits_gather<0>': 'gather_logits',
-       'k_logits_pair<1>': 'logits_gemm', 'k_logits_pair<0>': 'logits_gemm', 'k_eform_dotw': 'eform_dotw'}
+       'k_logits_pair<1>': 'logits_gemm', 'k_logits_pair<0>': 'logits_gemm', 'k_eform_dotw': 'eform_dotw',
+       'k_logits_pair<1, 1>': 'logits_gemm', 'k_logits_pair<0, 1>': 'logits_gemm', 'k_logits_pair<1, 0>': 'logits_gemm',
+       'k_logits_pair<0, 0>': 'logits_gemm'}
 lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU): cold-cache, serialised launches",
          "# k_logits_gather = K5+K6 (gather, norms, bf16, logits), k_dwx_t = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
          "# k_tc_gemm<0> = logits (K6), <1> = dx split-K (K9), <5>/<6> = dW + fused momentum SGD (K11+K12) otherwise",
