@@ -197,12 +197,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         const int col0 = n0 + c * 32;
         __half2 h2[16];
         float cf[32];
+        if (EF) {   // E is formed from the fp32 cosine (no cosine is stored: no fp16 rounding to match, R26)
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          const float2 f = __half22float2(h2[i]);
-          cf[2 * i] = f.x;
-          cf[2 * i + 1] = f.y;
+          for (int j = 0; j < 32; ++j) cf[j] = __uint_as_float(v[j]);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+            const float2 f = __half22float2(h2[i]);
+            cf[2 * i] = f.x;
+            cf[2 * i + 1] = f.y;
+          }
         }
         if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
 #pragma unroll

@@ -285,17 +285,29 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
           __half2 h2[16];
           float cf[32];
 #pragma unroll
-          for (int q = 0; q < 8; ++q) {
-            const float4 s4 = iv[q];
-            h2[2 * q] = __floats2half2_rn(__uint_as_float(v[4 * q]) * s4.x, __uint_as_float(v[4 * q + 1]) * s4.y);
-            h2[2 * q + 1] =
-                __floats2half2_rn(__uint_as_float(v[4 * q + 2]) * s4.z, __uint_as_float(v[4 * q + 3]) * s4.w);
-          }
+          if (EF) {   // E is formed from the fp32 cosine (no cosine is stored: no fp16 rounding to match, R26)
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            const float2 f = __half22float2(h2[i]);
-            cf[2 * i] = f.x;
-            cf[2 * i + 1] = f.y;
+            for (int q = 0; q < 8; ++q) {
+              const float4 s4 = iv[q];
+              cf[4 * q] = __uint_as_float(v[4 * q]) * s4.x;
+              cf[4 * q + 1] = __uint_as_float(v[4 * q + 1]) * s4.y;
+              cf[4 * q + 2] = __uint_as_float(v[4 * q + 2]) * s4.z;
+              cf[4 * q + 3] = __uint_as_float(v[4 * q + 3]) * s4.w;
+            }
+          } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+              const float4 s4 = iv[q];
+              h2[2 * q] = __floats2half2_rn(__uint_as_float(v[4 * q]) * s4.x, __uint_as_float(v[4 * q + 1]) * s4.y);
+              h2[2 * q + 1] =
+                  __floats2half2_rn(__uint_as_float(v[4 * q + 2]) * s4.z, __uint_as_float(v[4 * q + 3]) * s4.w);
+            }
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const float2 f = __half22float2(h2[i]);
+              cf[2 * i] = f.x;
+              cf[2 * i + 1] = f.y;
+            }
           }
           if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
 #pragma unroll
