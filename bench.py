@@ -83,15 +83,18 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.005)
+            time.sleep(0.001)
 
-    def __enter__(self):
+    def start(self):
         if self.nv:
             self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        return self
+            while not self.samples and self.t.is_alive():   # first sample taken before the timed region opens
+                time.sleep(0.0005)
+            self.samples.clear()
+            self.reasons.clear()
 
-    def __exit__(self, *a):
+    def stop(self):
         self._stop.set()
         if self.nv:
             self.t.join()
@@ -105,42 +108,60 @@ class ClockSampler:
 
 # ------------------------------------------------------------------------------------------------ roofline
 def kernel_work(section, M, k, d):
-    """Algorithmic work per launch: (amount, unit, bound) — for the fused kernels
-    both the HBM bytes and the flops, as [(amount, unit, bound), ...]; the entry reports the closer roofline."""
+    """Work per launch of each timed section: [(amount, unit, bound), ...] plus the implementation's extra HBM bytes.
+
+    The HBM amounts are the METHOD's algorithmic bytes of SURVEY.md §8(d) (20 k d per step: the W-row gather reads
+    4 B per sampled element, the W / V read-modify-write moves 16 B per element); the E / logits round trip is an
+    implementation choice and is reported separately as impl_bytes, never in the fraction. The tensor amounts are
+    the contractions' 2 M k d flops each."""
     if section in ("logits_gemm", "dx_gemm", "dw_gemm"):
-        return [(2.0 * M * k * d, "flop", "tensor")]
+        return [(2.0 * M * k * d, "flop", "tensor")], (2.0 * M * k if section == "logits_gemm" else 0.0)
     if section == "gather_w":
-        return [(4.0 * k * d, "byte", "hbm")]          # read the sampled fp32 rows once
-    if section == "gather_logits":                     # fp32 rows once + fp16 cosines out; the logits contraction
-        return [(4.0 * k * d + 2.0 * M * k, "byte", "hbm"), (2.0 * M * k * d, "flop", "tensor")]
-    if section == "dw_gemm_sgd":                       # W, V read-modify-write of the sampled rows; dW contraction
-        return [(16.0 * k * d, "byte", "hbm"), (2.0 * M * k * d, "flop", "tensor")]
-    if section == "dwx_sgd":                           # W, V RMW + G' in; dW and dX contractions
-        return [(16.0 * k * d + 2.0 * M * k, "byte", "hbm"), (4.0 * M * k * d, "flop", "tensor")]
-    if section == "sgd":
-        return [(16.0 * k * d, "byte", "hbm")]
+        return [(4.0 * k * d, "byte", "hbm")], 2.0 * k * d             # + the bf16 W_s write
+    if section == "gather_logits":                     # fp32 rows once; the logits contraction (E written: impl)
+        return [(4.0 * k * d, "byte", "hbm"), (2.0 * M * k * d, "flop", "tensor")], 2.0 * M * k
+    if section in ("dw_gemm_sgd", "sgd"):              # W, V read-modify-write of the sampled rows; dW contraction
+        w = [(16.0 * k * d, "byte", "hbm")]
+        return (w + [(2.0 * M * k * d, "flop", "tensor")] if section == "dw_gemm_sgd" else w), 2.0 * M * k
+    if section in ("dwx_sgd", "dwx_pair"):             # W, V RMW; dW and dX contractions (E' read: impl)
+        return [(16.0 * k * d, "byte", "hbm"), (4.0 * M * k * d, "flop", "tensor")], 2.0 * M * k
     if section == "softmax_grad":
-        return [(4.0 * M * k, "byte", "hbm")]          # fp16 cosine in, bf16 gradient out (design minimum)
+        return [], 4.0 * M * k                          # fp16 cosine in, bf16 gradient out: implementation only
     if section == "eform_dotw":
-        return [(2.0 * M * k, "byte", "hbm")]          # E-form radial dots: the bf16 E entries read once
+        return [], 2.0 * M * k                          # E-form radial dots: the bf16 E entries read once
     return None
 
 
 def roofline_entry(section, ms, launches, M, k, d, peaks, traffic):
-    works = kernel_work(section, M, k, d)
-    if works is None or launches == 0:
+    """Achieved / peak for the timed section. Tensor fractions use the BURST bf16 peak (these kernels run inside a
+    ~50 ms timed loop, far shorter than the seconds-long loop of the sustained figure; the sustained fraction is
+    reported beside it); HBM fractions use the measured copy peak."""
+    kw = kernel_work(section, M, k, d)
+    if kw is None or launches == 0:
         return None
+    works, impl = kw
     t = ms / launches / 1e3
     cands = []
     for amount, unit, bound in works:
         if bound == "tensor":
-            achieved, peak, u, src = amount / t / 1e12, peaks["bf16_tflops_sustained"], "TFLOP/s", "sustained bf16"
+            achieved = amount / t / 1e12
+            c = {"bound": bound, "achieved": round(achieved, 2), "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                 "frac": round(achieved / peaks["bf16_tflops"], 4),
+                 "frac_of_sustained": round(achieved / peaks["bf16_tflops_sustained"], 4),
+                 "per_launch": amount, "peak_src": f"{peaks['src']} (burst bf16)"}
         else:
-            achieved, peak, u, src = amount / t / 1e9, peaks["hbm_gbs"], "GB/s", "copy"
-        cands.append({"bound": bound, "achieved": round(achieved, 2), "peak": peak, "unit": u,
-                      "frac": round(achieved / peak, 4), "per_launch": amount, "peak_src": f"{peaks['src']} ({src})"})
+            achieved = amount / t / 1e9
+            c = {"bound": bound, "achieved": round(achieved, 2), "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                 "frac": round(achieved / peaks["hbm_gbs"], 4), "per_launch": amount,
+                 "peak_src": f"{peaks['src']} (copy)"}
+        cands.append(c)
+    e = {"kernel": section, "avg_ms": round(ms / launches, 4), "impl_bytes": impl,
+         "impl_gbs": round((impl + sum(a for a, u, b in works if u == "byte")) / t / 1e9, 1),
+         "traffic": traffic.get(section)}
+    if not cands:
+        return e | {"bound": "hbm", "achieved": None, "frac": None}
     best = max(cands, key=lambda c: c["frac"])          # the roofline the kernel is closest to
-    e = {"kernel": section} | best | {"traffic": traffic.get(section), "avg_ms": round(ms / launches, 4)}
+    e = {"kernel": section} | best | e
     others = [{kk: c[kk] for kk in ("bound", "achieved", "frac")} for c in cands if c is not best]
     if others:
         e["other_bound"] = others[0]
@@ -148,111 +169,112 @@ def roofline_entry(section, ms, launches, M, k, d, peaks, traffic):
 
 
 # ------------------------------------------------------------------------------------------------ CPU baseline
-def cpu_baseline(cfgname, budget_s=25.0, steps=1, warm=0):
-    """The oracle (oracle/, float64 numpy, as it stands) on the host cores, on a bounded sample of the
-    workload: a contiguous C_ref-class slice of the shard (r, margin, d as the workload), one full oracle step
-    (sampler, forward, backward, momentum SGD) with 8 and with 16 samples; the per-step fixed cost and the
-    per-sample cost are fitted from the two and extrapolated to the workload's batch B, then scaled by class count
-    (every part of the oracle step is proportional to it): samples/s ~ B (C_ref / C) / (t_fix + B t_row)."""
-    import torch
-    import oracle
-    import synth
-    from oracle import OracleConfig
-    C, d, B, r, mt, m, _ = CONFIGS[cfgname]
-    MT = {"none": 0, "arcface": 1, "cosface": 2}
+def host_cpu():
+    """Cores the oracle can use (affinity), the BLAS thread pool numpy actually runs, and the CPU model."""
+    info = {"nproc": len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()}
+    try:
+        import threadpoolctl
+        pools = threadpoolctl.threadpool_info()
+        info["blas"] = [{"api": p.get("internal_api"), "threads": p.get("num_threads")} for p in pools
+                        if p.get("user_api") == "blas"]
+    except Exception:
+        info["blas"] = []
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["model"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
 
-    def one(C_ref, B_ref, step):
-        cfg = OracleConfig(num_classes=C_ref, dim=d, batch=B_ref, sample_rate=r, scale=SCALE, margin_type=MT[mt],
-                           margin=m, momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, seed=0)
-        ys = synth.make_labels(0, step, 1, B_ref, C_ref)
-        xs = synth.make_features(0, step, 1, B_ref, d)
-        idx, _ = oracle.sample_shard(ys[0], 0, C_ref, r, 0, step)   # untimed: only to pre-generate input rows
-        rows = synth.w_rows_np(1, idx, d)
-        cache = {"ids": idx, "rows": rows}
+
+class OracleStep:
+    """The oracle (oracle/, float64 numpy, as it stands — never tuned) timing REAL steps on the host cores: one
+    step = sampler + forward + backward + momentum SGD (oracle.forward_backward + oracle.sgd_momentum_rows) with
+    the workload's batch B, d, r and margin, on a contiguous C_ref-class slice of the shard (C_ref sized from a
+    probe so that one step takes about `target_s`). Every part of the oracle step is proportional to the class
+    count at fixed B, so the workload's samples/s = B (C_ref / C) / t_step; nothing else is extrapolated."""
+
+    def __init__(self, cfgname, target_s):
+        import oracle
+        import synth
+        from oracle import OracleConfig
+        self.oracle, self.synth, self.OC = oracle, synth, OracleConfig
+        self.C, self.d, self.B, self.r, mt, self.m, _ = CONFIGS[cfgname]
+        self.mt = {"none": 0, "arcface": 1, "cosface": 2}[mt]
+        probe_c = min(self.C, 50_000)
+        tp = self.run(probe_c, 0)
+        self.C_ref = int(min(self.C, max(probe_c, target_s / (tp / probe_c))))
+
+    def run(self, C_ref, step):
+        np_ = np
+        cfg = self.OC(num_classes=C_ref, dim=self.d, batch=self.B, sample_rate=self.r, scale=SCALE,
+                      margin_type=self.mt, margin=self.m, momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, seed=0)
+        ys = self.synth.make_labels(0, step, 1, self.B, C_ref)
+        xs = self.synth.make_features(0, step, 1, self.B, self.d)
+        # input rows (the synthetic W, not the method's work) generated before the clock starts
+        idx, _ = self.oracle.sample_shard(ys[0], 0, C_ref, self.r, 0, step)
+        rows = self.synth.w_rows_np(1, idx, self.d)
 
         def w_rows(ids):
-            ids = np.asarray(ids)
-            if ids.shape == cache["ids"].shape and np.array_equal(ids, cache["ids"]):
-                return cache["rows"]
-            return synth.w_rows_np(1, ids, d)
+            ids = np_.asarray(ids)
+            if ids.shape == idx.shape and np_.array_equal(ids, idx):
+                return rows
+            return self.synth.w_rows_np(1, ids, self.d)
         t0 = time.perf_counter()
-        out = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
-        oracle.sgd_momentum_rows(rows, np.zeros_like(rows), out["dW"][0], LR, MOMENTUM, WEIGHT_DECAY)
+        out = self.oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
+        self.oracle.sgd_momentum_rows(rows, np_.zeros_like(rows), out["dW"][0], LR, MOMENTUM, WEIGHT_DECAY)
         return time.perf_counter() - t0
 
-    probe_c = min(C, 100_000)
-    tp = one(probe_c, 8, 0)
-    per_class = tp / probe_c
-    C_ref = int(min(C, max(20_000, budget_s / (2 * max(steps, 1)) / per_class)))
-    t8, t16 = [], []
-    for i in range(warm + steps):
-        a, b = one(C_ref, 8, 2 * i + 1), one(C_ref, 16, 2 * i + 2)
-        if i >= warm:
-            t8.append(a)
-            t16.append(b)
-    a, b = float(np.mean(t8)), float(np.mean(t16))
-    t_row = max((b - a) / 8.0, 0.0)
-    t_fix = max(a - 8 * t_row, 0.0)
-    t_step = t_fix + B * t_row
-    value = B * (C_ref / C) / t_step
-    return {"value": value, "unit": "samples/s", "cores": torch.get_num_threads(), "kind": "oracle",
-            "sample": f"oracle steps on a {C_ref}-class slice of the {C}-class shard (r={r}, d={d}) with 8 and 16 "
-                      f"samples ({a:.3f} s, {b:.3f} s per full step: sampler, fwd, bwd, SGD, float64 numpy); fitted "
-                      f"{t_fix:.3f} s/step + {t_row*1e3:.1f} ms/sample, extrapolated to B={B} and scaled by class "
-                      f"count C/C_ref; {len(t8)} step pair(s)",
-            "seconds_per_step": t_step * C / C_ref}
+    def value(self, t_step):
+        return self.B * (self.C_ref / self.C) / t_step
+
+    def describe(self, times):
+        return (f"{len(times)} real oracle step(s) (sampler, fwd, bwd, momentum SGD; float64 numpy) with the "
+                f"workload's B={self.B}, d={self.d}, r={self.r} on a {self.C_ref}-class slice of the {self.C}-class "
+                f"shard: {np.mean(times):.2f} s/step measured; samples/s = B (C_ref/C) / t_step")
 
 
-# ------------------------------------------------------------------------------------------------ main
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
-    ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
-    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
-    ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--params", default="device", choices=["device", "host"],
-                    help="where W and V live: HBM (default) or page-locked host memory (capacity mode, f4)")
-    ap.add_argument("--cpu-budget", type=float, default=20.0)
-    args = ap.parse_args()
-    assert args.warmup >= 3, "W >= 3 warm-up steps"
+def cpu_baseline(cfgname, target_s=12.0, steps=2):
+    ob = OracleStep(cfgname, target_s)
+    times = [ob.run(ob.C_ref, i + 1) for i in range(steps)]
+    t = float(np.mean(times))
+    return {"value": ob.value(t), "unit": "samples/s", "cores": host_cpu()["nproc"], "kind": "oracle",
+            "sample": ob.describe(times), "host": host_cpu(), "seconds_per_sample_step": t}
 
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    C, d, B, r, mt, m, desc = CONFIGS[args.config]
 
-    if args.impl == "reference":
-        if rank != 0:
-            return
-        budget = max(30.0, 150.0 / max(1, args.steps + args.warmup)) * (args.steps + args.warmup)
-        cb = cpu_baseline(args.config, budget_s=min(budget, 150.0), steps=args.steps, warm=args.warmup)
-        line = {"impl": "reference", "metric": METRIC, "value": cb["value"], "unit": "samples/s", "n_gpus": args.gpus,
-                "steps": args.steps, "warmup": args.warmup, "ms_per_step": cb["seconds_per_step"] * 1e3,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": {"workload": desc, "oracle": "oracle/pfc.py (float64 numpy, CPU)"},
-                "cpu_baseline": {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")},
-                "e2e": {"value": cb["value"], "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-        print(json.dumps(line), flush=True)
-        return
+# ------------------------------------------------------------------------------------------------ GPU arm
+def section_names(layer, prof):
+    """Section names by the kernel path (include/pfc.h PFC_PATH_*): the train step fuses the momentum-SGD update
+    into the dW contraction; with the fused gather the logits section holds gather + logits (section 2 keeps the
+    target cosines); with the fused dW/dX kernel section 6 holds dW + SGD + dX and section 8 is empty."""
+    flags = layer.path_flags()
+    rename = {"dw_gemm": "dw_gemm_sgd"}
+    if flags & layer.PATH_FUSED_GATHER:
+        rename |= {"logits_gemm": "gather_logits", "gather_w": "target_cos"}
+    if flags & layer.PATH_FUSED_DWX:
+        rename |= {"dx_gemm": "dwx_sgd"}
+    if flags & layer.PATH_EFORM:                 # E-form: no softmax-gradient pass; section 5 = per-row preparation
+        # (+ the radial-dot pass over E when dX is not fused into the dW kernel)
+        rename |= {"softmax_grad": "eform_prep" if flags & layer.PATH_FUSED_DWX else "eform_dotw"}
+    prof = {rename.get(s_, s_): v for s_, v in prof.items()}
+    if flags & layer.PATH_FUSED_DWX:
+        prof.pop("dw_gemm_sgd", None)        # empty: dW + SGD ran inside dwx_sgd
+    return prof
 
+
+def measure(cfgname, args, world, rank, local, dist, e2e=True, clocks=True):
+    """Build one rank's layer for `cfgname`, warm up, time K graph-replayed train steps (device-resident inputs),
+    then the same K steps eagerly with per-kernel events, then (e2e) K steps through the host-buffer entry."""
     import torch
-    import torch.distributed as dist
     import synth
     import paper_2010_05222_b200 as pfc
-
-    torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    layer = pfc.PartialFC.from_process_group(**dict(
-        num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m, momentum=MOMENTUM,
-        weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
-        param_location=args.params)) if world > 1 else \
-        pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m,
-                      momentum=MOMENTUM, weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
-                      param_location=args.params)
+    C, d, B, r, mt, m, desc = CONFIGS[cfgname]
+    kw = dict(num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m, momentum=MOMENTUM,
+              weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
+              param_location=args.params)
+    layer = pfc.PartialFC.from_process_group(**kw) if world > 1 else pfc.PartialFC(**kw)
     W, V = layer.params()
     if args.params == "host":       # page-locked host shard (SURVEY §8(f) f4): rows generated on the GPU, copied
         tmp = torch.empty(1 << 18, d, device="cuda")
@@ -286,6 +308,12 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def max_over_ranks(v):
+        t = torch.tensor([v], device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
@@ -296,22 +324,22 @@ def main():
     barrier()
     torch.cuda.synchronize()
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clk:
-        ev0.record(stream)
-        for i in range(args.steps):
-            step(i)
-        ev1.record(stream)
-        torch.cuda.synchronize()
+    clk = ClockSampler(local) if clocks else None
+    if clk:
+        clk.start()
+    ev0.record(stream)
+    for i in range(args.steps):
+        step(i)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if clk:
+        clk.stop()
     barrier()
     ms_total = ev0.elapsed_time(ev1)
     launches = layer.launch_count() - l0
     loss_val = float(loss.item())
     layer.check()
-    t = torch.tensor([ms_total], device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
-    value = M * args.steps / (ms_max / 1e3)
+    ms_max = max_over_ranks(ms_total)
 
     # ---------------- per-kernel times: the same K steps again with CUDA events between the kernels (eager
     # launches on the same stream: event records are not replayable per step inside one graph)
@@ -322,95 +350,205 @@ def main():
     for i in range(args.steps):
         step(i)
     p1.record(stream)
-    prof = layer.profile_read()
+    prof = section_names(layer, layer.profile_read())
     layer.profile(False)
     ms_prof = p0.elapsed_time(p1)
-    # section names by the kernel path (include/pfc.h PFC_PATH_*): the train step fuses the momentum-SGD update
-    # into the dW contraction (section 8; sgd 9 empty); with the fused gather the logits section holds
-    # gather + logits (section 2 keeps the target cosines); with the fused dW/dX kernel section 6 holds
-    # dW + SGD + dX and section 8 is empty
-    flags = layer.path_flags()
-    rename = {"dw_gemm": "dw_gemm_sgd"}
-    if flags & layer.PATH_FUSED_GATHER:
-        rename |= {"logits_gemm": "gather_logits", "gather_w": "target_cos"}
-    if flags & layer.PATH_FUSED_DWX:
-        rename |= {"dx_gemm": "dwx_sgd"}
-    if flags & layer.PATH_EFORM:                 # E-form: no softmax-gradient pass; section 5 = per-row preparation
-        # (+ the radial-dot pass over E when dX is not fused into the dW kernel)
-        rename |= {"softmax_grad": "eform_prep" if flags & layer.PATH_FUSED_DWX else "eform_dotw"}
-    prof = {rename.get(s, s): v for s, v in prof.items()}
-    if flags & layer.PATH_FUSED_DWX:
-        prof.pop("dw_gemm_sgd", None)        # empty: dW + SGD ran inside dwx_sgd
+
+    res = {"cfg": cfgname, "desc": desc, "C": C, "d": d, "B": B, "r": r, "mt": mt, "m": m, "M": M, "k": k,
+           "shard": layer.shard_size, "ms_total": ms_total, "ms_max": ms_max, "launches": launches, "loss": loss_val,
+           "prof": prof, "ms_prof": ms_prof, "clocks": clk.summary() if clk else None, "flags": layer.path_flags()}
 
     # ---------------- end-to-end through the C-ABI with host buffers (pinned), copies inside the timed region
-    xh = [x.cpu().pin_memory() for x in xs]
-    yh = [y.cpu().pin_memory() for y in ys]
-    gh = torch.empty(B, d).pin_memory()
-    lh = torch.zeros(1).pin_memory()
-    for i in range(2):
-        layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
-    barrier()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for i in range(args.steps):
-        layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
-    e1.record(stream)
-    torch.cuda.synchronize()
-    barrier()
-    te = torch.tensor([e0.elapsed_time(e1)], device="cuda")
+    if e2e:
+        xh = [x.cpu().pin_memory() for x in xs]
+        yh = [y.cpu().pin_memory() for y in ys]
+        gh = torch.empty(B, d).pin_memory()
+        lh = torch.zeros(1).pin_memory()
+        for i in range(2):
+            layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for i in range(args.steps):
+            layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        res["e2e_ms"] = max_over_ranks(e0.elapsed_time(e1))
+    layer.close()
+    del W, V, xs, ys
+    torch.cuda.set_stream(torch.cuda.default_stream())
+    torch.cuda.empty_cache()
+    return res
+
+
+def kernel_entries(res, peaks, world):
+    traffic = {}
+    tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tp):
+        tj = json.load(open(tp)).get("workloads", {}).get(f"{res['cfg']}/{world}", {})
+        traffic = tj.get("bytes_per_launch", {})
+    M, k, d = res["M"], res["k"], res["d"]
+    return [e for e in (roofline_entry(s_, ms, n, M, k, d, peaks, traffic) for s_, (ms, n) in res["prof"].items())
+            if e]
+
+
+def gemm_tensor_frac(res, peaks):
+    """The three contractions' 6 M k d flops / the summed event time of the kernels holding them / burst bf16."""
+    prof = res["prof"]
+    gemm = [prof[s_] for s_ in ("logits_gemm", "gather_logits", "dx_gemm", "dwx_sgd", "dwx_pair", "dw_gemm_sgd")
+            if s_ in prof and prof[s_][1]]
+    gemm_ms = sum(ms / n for ms, n in gemm)
+    if not gemm_ms:
+        return None
+    return round(6.0 * res["M"] * res["k"] * res["d"] / (gemm_ms / 1e3) / 1e12 / peaks["bf16_tflops"], 4)
+
+
+def sections(res, steps):
+    return {s_: {"ms_per_step": round(ms / steps, 4), "share": round(ms / res["ms_prof"], 4)}
+            for s_, (ms, n) in res["prof"].items() if n}
+
+
+def spawn_ranks(args):
+    """`bench.py --gpus N` without torchrun: relaunch this script under torch.distributed.run with N ranks
+    (127.0.0.1 rendezvous), so that --gpus always means N processes, one per GPU."""
+    import socket
+    import subprocess
+    sk = socket.socket()
+    sk.bind(("127.0.0.1", 0))
+    port = sk.getsockname()[1]
+    sk.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+def reference_arm(args):
+    """The reference arm (--impl reference): this tier has no reference code, so it is the oracle, as it stands,
+    timing K real steps (after W real warm-up steps) on the host cores, each a bounded sample of the workload
+    (the workload's B, d, r on a class slice sized so the whole run ends within a few minutes)."""
+    C, d, B, r, mt, m, desc = CONFIGS[args.config]
+    per_step = max(0.5, min(8.0, 150.0 / max(1, args.steps + args.warmup)))
+    ob = OracleStep(args.config, per_step)
+    for i in range(args.warmup):
+        ob.run(ob.C_ref, 100 + i)
+    times = [ob.run(ob.C_ref, i + 1) for i in range(args.steps)]
+    t = float(np.mean(times))
+    v = ob.value(t)
+    hc = host_cpu()
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": desc, "oracle": "oracle/pfc.py (float64 numpy, CPU)",
+                       "sample": f"{ob.C_ref} of {C} classes per step (B={B}, d={d}, r={r})"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": hc["nproc"], "kind": "oracle",
+                             "sample": ob.describe(times), "host": hc},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "ms_per_step_note": "real measured seconds of one oracle step on the class slice (the timed region is "
+                                "steps x ms_per_step); value scales it to the whole workload by C_ref / C"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="c4", choices=sorted(CONFIGS))
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-proxy", action="store_true", help="skip the per-rank proxy block (c4rank) of the N=1 line")
+    ap.add_argument("--params", default="device", choices=["device", "host"],
+                    help="where W and V live: HBM (default) or page-locked host memory (capacity mode, f4)")
+    ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds per oracle step of the cpu_baseline")
+    args = ap.parse_args()
+    assert args.warmup >= 3, "W >= 3 warm-up steps"
+
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        sys.exit(spawn_ranks(args))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        sys.exit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world} ranks were launched")
+
+    if args.impl == "reference":
+        if rank == 0:
+            reference_arm(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(local)
     if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_value = M * args.steps / (float(te.item()) / 1e3)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    res = measure(args.config, args, world, rank, local, dist)
+    proxy = None
+    if world == 1 and args.config == "c4" and not args.no_proxy:
+        # the shape the north star is judged on: one rank's exact work of the 8-GPU C4 job (1.25M-class shard,
+        # global batch 2048), where the contractions are tensor-bound
+        proxy = measure("c4rank", args, 1, 0, local, dist, e2e=False, clocks=True)
 
     if rank == 0:
         peaks = load_peaks()
-        traffic = {}
-        tp = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-        if os.path.exists(tp):
-            tj = json.load(open(tp)).get("workloads", {}).get(f"{args.config}/{world}", {})
-            traffic = tj.get("bytes_per_launch", {})
-        entries = [e for e in (roofline_entry(s, ms, n, M, k, d, peaks, traffic) for s, (ms, n) in prof.items()) if e]
-        gemm = [prof[s_] for s_ in ("logits_gemm", "gather_logits", "dx_gemm", "dwx_sgd", "dw_gemm_sgd")
-                if s_ in prof and prof[s_][1]]
-        gemm_ms = sum(ms / n for ms, n in gemm)
-        gemm_tensor_frac = (3 * 2.0 * M * k * d / (gemm_ms / 1e3) / 1e12 / peaks["bf16_tflops_sustained"]
-                            if gemm_ms else None)
+        M, k, d, B = res["M"], res["k"], res["d"], res["B"]
+        value = M * args.steps / (res["ms_max"] / 1e3)
+        entries = kernel_entries(res, peaks, world)
+        prof = res["prof"]
         dominant = max(prof.items(), key=lambda kv: kv[1][0])[0]
-        dom = next((e for e in entries if e["kernel"] == dominant), None)
+        dom = next((e for e in entries if e["kernel"] == dominant and e.get("frac") is not None), None)
         if dom is None and entries:
-            dom = max(entries, key=lambda e: e["avg_ms"])
-        sections = {s: {"ms_per_step": round(ms / args.steps, 4), "share": round(ms / ms_prof, 4)}
-                    for s, (ms, n) in prof.items() if n}
+            dom = max((e for e in entries if e.get("frac") is not None), key=lambda e: e["avg_ms"], default=None)
         line = {
             "metric": METRIC, "value": round(value, 1), "unit": "samples/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_max / args.steps, 4), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(res["ms_max"] / args.steps, 4), "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
-            "config": {"workload": desc, "num_classes": C, "dim": d, "batch_per_gpu": B, "global_batch": M,
-                       "sample_rate": r, "k_per_gpu": k, "shard_rows": layer.shard_size, "margin": f"{mt} {m}",
-                       "scale": SCALE, "parallelism": f"class-parallel x{world}", "params": args.params,
+            "config": {"workload": res["desc"], "num_classes": res["C"], "dim": d, "batch_per_gpu": B,
+                       "global_batch": M, "sample_rate": res["r"], "k_per_gpu": k, "shard_rows": res["shard"],
+                       "margin": f"{res['mt']} {res['m']}", "scale": SCALE, "parallelism": f"class-parallel x{world}",
+                       "params": args.params,
                        "l2": "inputs larger than L2 (W+V shard %.1f GB, %.1f GB of sampled rows per step)"
-                             % (2 * layer.shard_size * d * 4 / 1e9, k * d * 4 / 1e9)},
-            "clocks": clk.summary(),
-            "e2e": {"value": round(e2e_value, 1), "unit": "samples/s", "h2d_bytes_per_step": B * d * 4 + B * 8,
-                    "d2h_bytes_per_step": B * d * 4 + 4},
-            "gpu_launches": launches,
-            "roofline": {kk: dom[kk] for kk in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | {
-                "kernel": dom["kernel"], "peak_src": dom["peak_src"]} if dom else None,
-            "kernels": entries, "sections": sections, "loss": loss_val,
-            "gemm_tensor_frac": round(gemm_tensor_frac, 4) if gemm_tensor_frac else None,
-            "gemm_tensor_frac_note": "the three contractions' 6 M k d flops / the summed event time of the kernels holding them / bf16 "
-                                     "peak (the metric's tensor-pipe share; at N = 1 the fused dW kernel is HBM-bound)",
-            "step_ms_rank0": round(ms_total / args.steps, 4),
-            "step_ms_eager_profiled": round(ms_prof / args.steps, 4),
+                             % (2 * res["shard"] * d * 4 / 1e9, k * d * 4 / 1e9)},
+            "clocks": res["clocks"],
+            "e2e": {"value": round(M * args.steps / (res["e2e_ms"] / 1e3), 1), "unit": "samples/s",
+                    "h2d_bytes_per_step": B * d * 4 + B * 8, "d2h_bytes_per_step": B * d * 4 + 4},
+            "gpu_launches": res["launches"],
+            "roofline": ({kk: dom.get(kk) for kk in ("bound", "achieved", "peak", "unit", "frac", "traffic")} | {
+                "kernel": dom["kernel"], "peak_src": dom["peak_src"], "impl_bytes": dom["impl_bytes"],
+                "algorithmic": "SURVEY.md §8(d) method bytes per launch (20 k d per step: gather 4 k d, W/V RMW "
+                               "16 k d); E traffic is impl_bytes"}) if dom else None,
+            "kernels": entries, "sections": sections(res, args.steps), "loss": res["loss"],
+            "gemm_tensor_frac": gemm_tensor_frac(res, peaks),
+            "gemm_tensor_frac_note": "the three contractions' 6 M k d flops / the summed event time of the kernels "
+                                     "holding them / burst bf16 peak (at N = 1 the fused dW kernel is HBM-bound)",
+            "step_hbm_roofline": {"algorithmic_bytes": 20.0 * k * d,
+                                  "samples_per_s_at_peak": round(M / (20.0 * k * d / (peaks["hbm_gbs"] * 1e9)), 1),
+                                  "frac": round(value / (M / (20.0 * k * d / (peaks["hbm_gbs"] * 1e9))), 4)},
+            "step_ms_rank0": round(res["ms_total"] / args.steps, 4),
+            "step_ms_eager_profiled": round(res["ms_prof"] / args.steps, 4),
             "kernel_timing": "CUDA events between the kernels on the launching stream, same K steps run eagerly "
                              "right after the graph-replayed timed region",
         }
+        if proxy:
+            pe = kernel_entries(proxy, peaks, 1)
+            pv = proxy["M"] * args.steps / (proxy["ms_max"] / 1e3)
+            line["per_rank_proxy"] = {
+                "workload": proxy["desc"], "global_batch": proxy["M"], "k_per_gpu": proxy["k"],
+                "ms_per_step": round(proxy["ms_max"] / args.steps, 4), "samples_per_s_per_gpu": round(pv, 1),
+                "projected_8gpu_samples_per_s_without_collectives": round(8 * pv, 1),
+                "gemm_tensor_frac": gemm_tensor_frac(proxy, peaks), "clocks": proxy["clocks"],
+                "kernels": [{kk: e.get(kk) for kk in ("kernel", "avg_ms", "bound", "achieved", "unit", "frac",
+                                                       "frac_of_sustained", "other_bound", "impl_gbs")} for e in pe],
+                "sections": sections(proxy, args.steps),
+                "note": "one rank's exact per-GPU work of the 8-GPU C4 job (1.25M-class shard, M = 2048, k = 125k) "
+                        "on this GPU, graph-replayed like the main line; the collectives are not in it"}
         if world == 1 and not args.no_cpu_baseline:
-            cb = cpu_baseline(args.config, budget_s=args.cpu_budget)
-            line["cpu_baseline"] = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample")}
+            cb = cpu_baseline(args.config, target_s=args.cpu_budget)
+            line["cpu_baseline"] = {kk: cb[kk] for kk in ("value", "unit", "cores", "kind", "sample", "host")}
         print(json.dumps(line), flush=True)
-    layer.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -278,30 +278,48 @@ def spot_rows(cfg, X, Y, S, w_rows, rows, step_unused=None):
     return res
 
 
+def row_lse(cfg, Xh, Y, S, Wh, block=64):
+    """lse_n = log sum_{j in S} e^{z_nj} (R12: shifted by the row max) and the target cosine c_t for every row n,
+    with z = s c except z_t = s phi(c_t) (R11) — the same definitions as forward_backward, evaluated for `block`
+    rows at a time so that the M x |S| cosine matrix never has to exist at once (C5: 2048 x 1.25M). Each row's
+    sum still runs over the whole of S in one np.sum."""
+    s, mt, m = float(cfg.scale), cfg.margin_type, float(cfg.margin)
+    pos = {int(g): t for t, g in enumerate(S)}
+    tcol = np.array([pos[int(y)] for y in Y])
+    M = Xh.shape[0]
+    lse, ct = np.empty(M), np.empty(M)
+    for r0 in range(0, M, block):
+        r1 = min(M, r0 + block)
+        rows = np.arange(r1 - r0)
+        z = s * (Xh[r0:r1] @ Wh.T)                                   # block x |S|
+        ct[r0:r1] = z[rows, tcol[r0:r1]] / s
+        z[rows, tcol[r0:r1]] = s * margin_phi(ct[r0:r1], mt, m)
+        zmax = z.max(axis=1)
+        lse[r0:r1] = zmax + np.log(np.sum(np.exp(z - zmax[:, None]), axis=1))
+    return lse, ct, tcol
+
+
 def spot_cols(cfg, X, Y, S, w_rows, cols):
     """Gradient w.r.t. the raw W rows of the sampled classes S[cols] (same definitions as forward_backward:
     Alg.1 L10 grad w = X^T grad logits, then the l2-norm backprop R14), for sizes where only a few columns are
-    wanted. The row log-sum-exps need every row over the whole sampled set S, computed as one product."""
+    wanted. The row log-sum-exps need every row over the whole sampled set S (row_lse).
+    Returns (dW rows for cols, lse for every row, target cosine for every row)."""
     s, mt, m = float(cfg.scale), cfg.margin_type, float(cfg.margin)
     M = X.shape[0]
     Xh, _ = normalize_rows(X)
-    Wh, _ = normalize_rows(w_rows(S))
-    cos = Xh @ Wh.T                                                  # M x |S|
-    pos = {int(g): t for t, g in enumerate(S)}
-    tcol = np.array([pos[int(y)] for y in Y])
-    rows = np.arange(M)
-    ct = cos[rows, tcol]
-    cos[rows, tcol] = margin_phi(ct, mt, m)                          # z / s (margin at the target, R11)
-    zmax = s * cos.max(axis=1)
-    lse = zmax + np.log(np.sum(np.exp(s * cos - zmax[:, None]), axis=1))
+    Wraw = np.asarray(w_rows(S), dtype=np.float64)
+    Wh, _ = normalize_rows(Wraw)
+    lse, ct, tcol = row_lse(cfg, Xh, Y, S, Wh)
     out = []
     for t in cols:
-        gc = s * np.exp(s * cos[:, t] - lse) / M                    # dL/dcos for non-target rows
+        c = Xh @ Wh[t]                                               # cosines of every row with class S[t]
         hit = tcol == t
-        gc[hit] = s * (np.exp(s * cos[hit, t] - lse[hit]) - 1.0) / M * margin_dphi(ct[hit], mt, m)
+        c[hit] = margin_phi(ct[hit], mt, m)                          # z / s (margin at the target, R11)
+        gc = s * np.exp(s * c - lse) / M                             # dL/dcos for non-target rows
+        gc[hit] = s * (np.exp(s * c[hit] - lse[hit]) - 1.0) / M * margin_dphi(ct[hit], mt, m)
         dwh = gc @ Xh
-        wr = np.asarray(w_rows(S[t:t + 1]), dtype=np.float64)[0]
+        wr = Wraw[t]
         wn = np.sqrt(np.sum(wr * wr))
         wh = wr / max(wn, NORM_EPS)
         out.append((dwh - wh * np.dot(wh, dwh)) / max(wn, NORM_EPS))
-    return np.array(out), lse
+    return np.array(out), lse, ct

@@ -13,6 +13,8 @@
 #include <cstring>
 #include <string>
 #include <array>
+#include <chrono>
+#include <thread>
 #include <vector>
 
 #include "pfc_internal.cuh"
@@ -93,6 +95,8 @@ struct pfc_ctx {
   float* xch = nullptr;              // k_pad x (d/128): radial-dot partials
   int* cnt = nullptr;                // k_pad/128
   int* err_dev = nullptr;
+  int* err_host = nullptr;           // page-locked mirror of err_dev written by the step's last kernel
+  int* err_host_dev = nullptr;       // its device mapping
   // host-buffer entry point
   float* x_in = nullptr;
   int64_t* y_in = nullptr;
@@ -153,15 +157,60 @@ pfc_status dalloc(pfc_ctx* c, T** p, size_t bytes) {
   return PFC_OK;
 }
 
-pfc_status device_error(pfc_ctx* c) {
-  int h = 0;
-  CUDA_TRY(c, cudaMemcpy(&h, c->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
-  if (!h) return PFC_OK;
-  CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(int)));
+pfc_status decode_error(pfc_ctx* c, int h) {
   if (h & ERR_DATA) return set_err(c, PFC_ERR_DATA, "a label is outside [0, num_classes)");
   if (h & ERR_DEGENERATE) return set_err(c, PFC_ERR_DEGENERATE, "a feature or class-centre row has zero norm");
   if (h & ERR_NUMERIC) return set_err(c, PFC_ERR_NUMERIC, "non-finite loss");
   return set_err(c, PFC_ERR_CUDA, "internal consistency check failed (sampler count != k_i, or a radial-dot exchange timed out)");
+}
+
+// NCCL: a failed or hung peer surfaces as an asynchronous communicator error; poll it while waiting for the stream
+// and abort the communicator on error or after PFC_NCCL_TIMEOUT_S seconds (default 600), so that no call blocks
+// forever on a dead rank (SURVEY.md §5 failure detection).
+pfc_status wait_stream(pfc_ctx* c, cudaStream_t s) {
+  if (!c->comm) {
+    CUDA_TRY(c, cudaStreamSynchronize(s));
+    return PFC_OK;
+  }
+  static const double timeout_s = [] { const char* e = std::getenv("PFC_NCCL_TIMEOUT_S"); return e ? std::atof(e) : 600.0; }();
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    cudaError_t q = cudaStreamQuery(s);
+    if (q == cudaSuccess) break;
+    if (q != cudaErrorNotReady) CUDA_TRY(c, q);
+    ncclResult_t ar = ncclSuccess;
+    ncclCommGetAsyncError(c->comm, &ar);
+    const double el = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if ((ar != ncclSuccess && ar != ncclInProgress) || el > timeout_s) {
+      std::string m = ar != ncclSuccess ? std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar)
+                                        : "collective did not complete within PFC_NCCL_TIMEOUT_S";
+      ncclCommAbort(c->comm);
+      c->comm = nullptr;
+      return set_err(c, PFC_ERR_NCCL, m + " (communicator aborted)");
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  ncclResult_t ar = ncclSuccess;
+  ncclCommGetAsyncError(c->comm, &ar);
+  if (ar != ncclSuccess && ar != ncclInProgress) return set_err(c, PFC_ERR_NCCL, std::string("NCCL asynchronous error: ") + ncclGetErrorString(ar));
+  return PFC_OK;
+}
+
+pfc_status device_error(pfc_ctx* c) {
+  int h = 0;
+  CUDA_TRY(c, cudaMemcpy(&h, c->err_dev, sizeof(int), cudaMemcpyDeviceToHost));
+  if (c->err_host) *(volatile int*)c->err_host = 0;
+  if (!h) return PFC_OK;
+  CUDA_TRY(c, cudaMemset(c->err_dev, 0, sizeof(int)));
+  return decode_error(c, h);
+}
+
+// cheap check at the start of every hot-path call: the error word of an earlier, completed step, as published to
+// host memory by that step's last kernel (no synchronisation; include/pfc.h "device-detected errors")
+pfc_status pending_error(pfc_ctx* c) {
+  if (!c->err_host || !*(volatile int*)c->err_host) return PFC_OK;
+  CUDA_TRY(c, cudaDeviceSynchronize());
+  return device_error(c);
 }
 
 pfc_status validate(const pfc_config* c) {
@@ -357,6 +406,19 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->dWh, kp * d * 4);
   ALLOC(c->dotw, kp * 4);
   ALLOC(c->err_dev, 16);
+  {
+    void* h = nullptr;
+    void* dp = nullptr;
+    if (cudaHostAlloc(&h, 64, cudaHostAllocMapped) == cudaSuccess && cudaHostGetDevicePointer(&dp, h, 0) == cudaSuccess) {
+      c->host_allocs.push_back(h);
+      c->err_host = static_cast<int*>(h);
+      c->err_host_dev = static_cast<int*>(dp);
+      *c->err_host = 0;
+    } else {
+      cudaGetLastError();
+      if (h) cudaFreeHost(h);
+    }
+  }
   ALLOC(c->step_dev, 16);
   ALLOC(c->lr_dev, 16);
   ALLOC(c->x_in, B * d * 4);
@@ -595,7 +657,7 @@ pfc_status finish_fb(pfc_ctx* c, bool fused, cudaStream_t s) {
   c->fb_done = !fused;
   c->last_stream = s;
   if (c->sync_check) {
-    CUDA_TRY(c, cudaStreamSynchronize(s));
+    if (pfc_status w = wait_stream(c, s)) return w;
     return device_error(c);
   }
   return PFC_OK;
@@ -658,7 +720,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     }
     phase_e(c, dxh, grad_x, fused, s);
   }
-  c->launches += launch_advance_step(c->step_dev, s);
+  c->launches += launch_advance_step(c->step_dev, c->err_dev, c->err_host_dev, s);
 }
 
 static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss, bool fused,
@@ -668,15 +730,18 @@ static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, fl
   if (a != PFC_OK) return a;
   if (c->sz.world > 1 && c->cfg.comm_mode == PFC_COMM_LOOPBACK)
     return set_err(c, PFC_ERR_CONTRACT, "loopback contexts are driven by pfc_group_forward_backward");
+  if (pfc_status pe = pending_error(c)) return pe;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   float* loss_out = loss ? loss : c->loss_dev;
   if (fused) c->launches += launch_set_scalar(c->lr_dev, lr, s);   // outside any graph: a kernel argument
+  tmap_error() = 0;
   ncclResult_t nres = ncclSuccess;
   const bool use_graph = c->graph_on && !c->prof && s != nullptr;
   if (!use_graph) {
     prof_begin_step(c);
     enqueue_step(c, x, labels, grad_x, loss_out, fused, s, &nres);
     if (nres != ncclSuccess) return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres));
+    if (tmap_error()) return set_err(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(tmap_error()) + "): kernels not launched");
     return finish_fb(c, fused, s);
   }
   // CUDA graph of the whole step, cached per (pointers, stream, fused); the first call of a context runs eagerly
@@ -692,6 +757,7 @@ static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, fl
     prof_begin_step(c);
     enqueue_step(c, x, labels, grad_x, loss_out, fused, s, &nres);
     if (nres != ncclSuccess) return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres));
+    if (tmap_error()) return set_err(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(tmap_error()) + "): kernels not launched");
     return finish_fb(c, fused, s);
   }
   cudaGraph_t graph = nullptr;
@@ -703,6 +769,10 @@ static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, fl
   c->graph_launches = c->launches - l0;
   c->launches = l0;
   if (nres != ncclSuccess) { if (graph) cudaGraphDestroy(graph); return set_err(c, PFC_ERR_NCCL, ncclGetErrorString(nres)); }
+  if (tmap_error()) {
+    if (graph) cudaGraphDestroy(graph);
+    return set_err(c, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(tmap_error()) + "): kernels not launched");
+  }
   CUDA_TRY(c, ce);
   cudaGraphExec_t exec = nullptr;
   ce = cudaGraphInstantiate(&exec, graph, 0);
@@ -741,6 +811,9 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
     pfc_status a = check_fb_args(c, x[r], labels[r], grad_x[r]);
     if (a != PFC_OK) return a;
   }
+  for (int r = 0; r < n; ++r)
+    if (pfc_status pe = pending_error(ctxs[r])) return pe;
+  tmap_error() = 0;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   for (int r = 0; r < n; ++r) ctxs[r]->prof_cur = nullptr;  // no event timing in loopback groups
   if (fused)
@@ -773,8 +846,9 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   }
   for (int r = 0; r < n; ++r) {
     phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], fused, s);
-    ctxs[r]->launches += launch_advance_step(ctxs[r]->step_dev, s);
+    ctxs[r]->launches += launch_advance_step(ctxs[r]->step_dev, ctxs[r]->err_dev, ctxs[r]->err_host_dev, s);
   }
+  if (tmap_error()) return set_err(c0, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed: kernels not launched");
   for (int r = 0; r < n; ++r) {
     pfc_status f = finish_fb(ctxs[r], fused, s);
     if (f != PFC_OK) return f;
@@ -794,8 +868,7 @@ static pfc_status host_step(pfc_ctx* c, const float* x_host, const int64_t* labe
   if (r != PFC_OK) return r;
   CUDA_TRY(c, cudaMemcpyAsync(grad_x_host, c->gx_out, xb, cudaMemcpyDeviceToHost, s));
   if (loss_host) CUDA_TRY(c, cudaMemcpyAsync(loss_host, c->loss_dev, 4, cudaMemcpyDeviceToHost, s));
-  CUDA_TRY(c, cudaStreamSynchronize(s));
-  return PFC_OK;
+  return wait_stream(c, s);
 }
 
 pfc_status pfc_forward_backward_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
@@ -811,6 +884,7 @@ pfc_status pfc_train_step_host(pfc_ctx* c, const float* x_host, const int64_t* l
 pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   if (!c->fb_done) return set_err(c, PFC_ERR_CONTRACT, "pfc_step without a preceding pfc_forward_backward");
+  if (pfc_status pe = pending_error(c)) return pe;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   c->last_stream = s;
   if (c->prof) {
@@ -853,6 +927,7 @@ pfc_status pfc_param_ptrs(pfc_ctx* c, float** W, float** V) {
 
 static pfc_status sync_and_check(pfc_ctx* c) {
   CUDA_TRY(c, cudaSetDevice(c->cfg.device));
+  if (pfc_status w = wait_stream(c, c->last_stream)) return w;
   CUDA_TRY(c, cudaDeviceSynchronize());
   return device_error(c);
 }

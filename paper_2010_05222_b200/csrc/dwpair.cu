@@ -283,6 +283,7 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
   }
   const CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);    // G class-major: 128 classes x 64 batch
   const CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);        // X_hat: 64 batch rows x 64 columns
+  TC_MAPS_OK();
   DpParams p{};
   p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa;
   const int64_t units = (sz.k_pad / 256) * (sz.d / 256);

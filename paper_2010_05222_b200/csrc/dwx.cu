@@ -473,6 +473,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   }
   const CUtensorMap tg = make_map(G, sz.k_pad, sz.M_pad, 64, 128);   // G' (or E') class-major: 128 classes x 64 batch
   const CUtensorMap tx = make_map(Xb, sz.M_pad, sz.d, 64, 64);       // X_hat (or X~): 64 batch rows x 64 columns
+  TC_MAPS_OK();
   DwxParams p{};
   p.M = sz.M; p.d = sz.d; p.nkb = (int)(sz.M_pad / 64); p.gper = dwx_gper(sz); p.st = st; p.sgd = sa; p.ws = ws;
   if (ef) {
@@ -481,7 +482,24 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     cudaMemsetAsync(ef->cnt, 0, (size_t)(sz.k_pad / 128) * sizeof(int), s);
   }
   const int grid = p.gper * (sz.d / 128);
-  kern<<<grid, ef ? DX_THREADS_EF : DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+  if (ef) {
+    // the E-form epilogue waits on radial-dot partials published by the other d-tile CTAs of its class tile: a
+    // cooperative launch guarantees that the whole grid (<= one CTA per SM) is co-resident, or fails loudly
+    // (cudaErrorCooperativeLaunchTooLarge, reported by the step) instead of spinning on a CTA that never runs
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(DX_THREADS_EF);
+    lc.dynamicSmemBytes = DX_SMEM;
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, kern, tg, tx, p);
+  } else {
+    kern<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+  }
   const int64_t n = (int64_t)sz.M * sz.d;
   k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh);
   return 2;

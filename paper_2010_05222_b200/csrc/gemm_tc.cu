@@ -584,6 +584,11 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int g
 
 }  // namespace
 
+int& tmap_error() {
+  static thread_local int e = 0;
+  return e;
+}
+
 bool tc_available() {
   int dev = 0, major = 0, minor = 0;
   if (cudaGetDevice(&dev) != cudaSuccess) return false;
@@ -598,6 +603,7 @@ int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat
   (void)ct;
   CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  TC_MAPS_OK();
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.tcol = tcol;
   p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials; p.n_ltiles = sz.n_ltiles;
@@ -626,6 +632,7 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
                  float* split_ws, const float* rowscale, cudaStream_t s) {
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 64);      // Gc class-major, MN-major A
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 64);
+  TC_MAPS_OK();
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.split_ws = split_ws;
   const int tiles = ((sz.M + 255) / 256) * (sz.d / dtile(sz));
@@ -644,6 +651,7 @@ int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat1
   if (dw_sgd_pair_enabled(sz)) return launch_dw_sgd_pair_tc(sz, G, Xb, st, sa, s);   // dwpair.cu (CTA pairs)
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);     // Gc class-major, K-major A (= Gc^T)
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
+  TC_MAPS_OK();
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
   // 256-class tiles pay off when the contraction is long (K = M >= 1024: operand-bandwidth bound); at small M
@@ -664,6 +672,7 @@ int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* X
                  cudaStream_t s) {
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);
+  TC_MAPS_OK();
   TcParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.dWh = dWh;
   const int64_t units = (sz.k_pad / 128) * (sz.d / dtile(sz));

@@ -308,6 +308,7 @@ int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_b
   }
   const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
   const CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  TC_MAPS_OK();
   L2Params p{};
   p.M = sz.M; p.ldm = (int)sz.M_pad; p.d = sz.d; p.st = st; p.tcol = tcol;
   p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;

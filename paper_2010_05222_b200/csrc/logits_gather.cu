@@ -413,6 +413,7 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   }
   const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
   const CUtensorMap ws = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  TC_MAPS_OK();
   LgParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.st = st; p.W = W; p.idx = idx; p.inv_norm = inv_norm; p.err = err;
   p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;

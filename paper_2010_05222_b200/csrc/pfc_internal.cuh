@@ -141,7 +141,7 @@ int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_loc
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
                const SamplerState* st, const float* lr_dev, float mu, float lambda, int gsc, cudaStream_t s);
 int launch_set_scalar(float* dst, float v, cudaStream_t s);
-int launch_advance_step(uint64_t* step_dev, cudaStream_t s);
+int launch_advance_step(uint64_t* step_dev, const int* err_dev, int* err_host_mapped, cudaStream_t s);
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
                     const SamplerState* st, float* out, int gsc, cudaStream_t s);
 
@@ -165,6 +165,7 @@ int launch_dw_simt(const Sizes& sz, bool bf16, const void* G, const void* X, con
 // gemm_tc.cu — tcgen05 / TMEM / TMA bf16 contractions (sm_100a)
 constexpr int kMaxSplits = 64;   // split-K bound of the dx contraction
 bool tc_available();
+int& tmap_error();   // tc_common.cuh: status of the last failed tensor-map encode (per host thread)
 int64_t dx_split_ws_floats(const Sizes& sz);
 int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
                      const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,

@@ -604,7 +604,12 @@ int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int3
 
 namespace {
 __global__ void k_set_f32(float* dst, float v) { *dst = v; }
-__global__ void k_add_u64(uint64_t* dst, uint64_t v) { *dst += v; }
+// end of a step: advance the device step counter and publish the sticky device error word to the host-mapped word
+// (plain store into page-locked memory; the host reads it at the next hot-path call without synchronising)
+__global__ void k_end_step(uint64_t* dst, uint64_t v, const int* err, volatile int* err_host) {
+  *dst += v;
+  if (err_host) *err_host = *err;
+}
 }  // namespace
 
 int launch_set_scalar(float* dst, float v, cudaStream_t s) {
@@ -612,8 +617,8 @@ int launch_set_scalar(float* dst, float v, cudaStream_t s) {
   return 1;
 }
 
-int launch_advance_step(uint64_t* step_dev, cudaStream_t s) {
-  k_add_u64<<<1, 1, 0, s>>>(step_dev, 1);
+int launch_advance_step(uint64_t* step_dev, const int* err_dev, int* err_host_mapped, cudaStream_t s) {
+  k_end_step<<<1, 1, 0, s>>>(step_dev, 1, err_dev, err_host_mapped);
   return 1;
 }
 

@@ -5,9 +5,14 @@
 #include <cuda_runtime.h>
 #include <cstdint>
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 namespace pfc {
+// Sticky (per host thread) status of the last failed tensor-map encode: the tcgen05 launchers skip their launch
+// when it is set and the step returns PFC_ERR_CUDA (api.cu clears it before and reads it after each step).
+int& tmap_error();
+
 namespace {
 
 // ------------------------------------------------------------------------------------------------ PTX helpers
@@ -221,19 +226,34 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2D bf16 tensor [rows][cols] (cols contiguous), box {box_cols, box_rows}, 128-byte swizzle.
+// 2D bf16 tensor [rows][cols] (cols contiguous), box {box_cols, box_rows}, 128-byte swizzle. On failure the map
+// is zeroed and tmap_error() set: the caller must not launch with it (TC_MAPS_OK below).
 CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
   CUtensorMap m;
+  std::memset(&m, 0, sizeof(m));
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) {
+    tmap_error() = (int)CUDA_ERROR_NOT_FOUND;
+    return m;
+  }
   cuuint64_t dims[2] = {cols, rows};
   cuuint64_t strides[1] = {cols * 2};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) fprintf(stderr, "pfc: cuTensorMapEncodeTiled failed (%d)\n", (int)r);
+  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    tmap_error() = (int)r;
+    std::memset(&m, 0, sizeof(m));
+  }
   return m;
 }
+// in a launcher, after its make_map calls: skip the launch when an encode failed
+#define TC_MAPS_OK() \
+  do {               \
+    if (::pfc::tmap_error()) return 0; \
+  } while (0)
 
 int num_sms() {
   static int n = 0;

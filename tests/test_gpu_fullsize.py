@@ -115,10 +115,8 @@ def test_c4_ten_million_ids_one_gpu_sampled_outputs():
         assert abs(lse[n] - lse_r) / abs(lse_r) <= 1e-3 * 0.1     # log-sum-exp ~ 48: well inside the loss bar
         assert maxrel(gx_h[n], g) <= 2e-2
     cols = sorted(set([0, 1, 500_000, 999_999] + [int(np.searchsorted(S, Y[n])) for n in rows]))
-    dW_ref, lse_all = oracle.spot_cols(cfg, X, Y, S, w_rows, cols)
-    loss_ref = float(np.mean(lse_all - 64.0 * oracle.margin_phi(
-        np.sum(oracle.normalize_rows(X)[0] * oracle.normalize_rows(w_rows(S)[np.searchsorted(S, Y)])[0], axis=1),
-        oracle.MARGIN_ARCFACE, m)))
+    dW_ref, lse_all, ct_all = oracle.spot_cols(cfg, X, Y, S, w_rows, cols)
+    loss_ref = float(np.mean(lse_all - 64.0 * oracle.margin_phi(ct_all, oracle.MARGIN_ARCFACE, m)))
     assert abs(loss.item() - loss_ref) / loss_ref <= 1e-3
     dW = L.sampled_grad()
     assert maxrel(dW[cols], dW_ref) <= 2e-2
@@ -131,4 +129,60 @@ def test_c4_ten_million_ids_one_gpu_sampled_outputs():
     _, Vr = oracle.sgd_momentum_rows(Wrows[cols], np.zeros((len(cols), d)), dW_ref, 0.1, 0.9, 5e-4)
     assert maxrel(V_rows, Vr) <= 2e-2
     assert not torch.equal(W_before, W_after)
+    L.close()
+
+
+def _w_rows_chunked(wseed, ids, d, chunk=1 << 16):
+    ids = np.asarray(ids)
+    return np.concatenate([synth.w_rows_np(wseed, ids[i:i + chunk], d) for i in range(0, len(ids), chunk)])
+
+
+def test_c5_per_rank_shape_spot_parity():
+    """BASELINE configs[4] (100M identities over 8 B200) at one rank's exact shape: a 12.5M-class shard (51 GB of
+    W + V in HBM), M = 2048 (the all-gathered batch of 8 x 256), k = 1.25M, the bf16 E-form train step the bench
+    times (CTA-pair logits and dW + SGD; E has 2.56e9 > 2^31 entries). Sampled ids bit-exact over the whole
+    shard; the loss over all 2048 rows; grad_x on spot rows (oracle.spot_rows); the updated V and W of spot
+    sampled classes (V = dW + lambda w from zero momentum; oracle.spot_cols) — all at the north-star bars."""
+    import _parity
+    C, d, B, r, m, seed, wseed, lr, lam = 12_500_000, 512, 2048, 0.1, 0.5, 77, 2, 0.1, 5e-4
+    L = pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=r, margin_type="arcface", margin=m, momentum=0.9,
+                      weight_decay=lam, precision="bf16", seed=seed)
+    assert L.path_flags() == 9      # CTA-pair kernels, E-form
+    W, V = L.params()
+    synth.fill_w_shard(W, wseed, 0)
+    V.zero_()
+    ys = synth.make_labels(91, 0, 1, B, C)
+    xs = synth.make_features(91, 0, 1, B, d)
+    x, y = torch.from_numpy(xs[0]).cuda(), torch.from_numpy(ys[0]).cuda()
+    gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+    L.train_step(x, y, gx, loss, lr=lr)
+    torch.cuda.synchronize()
+    L.check()
+    idx = L.sampled()
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, sample_rate=r, margin_type=oracle.MARGIN_ARCFACE, margin=m,
+                       weight_decay=lam, seed=seed)
+    S, _ = oracle.sample_shard(ys[0], 0, C, r, seed, 0)
+    assert len(S) == 1_250_000 and np.array_equal(idx, S)        # bit-exact over the 12.5M-class shard
+    Wrows = _w_rows_chunked(wseed, S, d)
+
+    def w_rows(ids):
+        ids = np.asarray(ids)
+        return Wrows if ids.shape == S.shape and ids[0] == S[0] and ids[-1] == S[-1] else synth.w_rows_np(wseed, ids, d)
+
+    X, Y = xs[0].astype(np.float64), ys[0]
+    rows = [0, 1, 777, 1500, 2047]
+    cols = sorted(set([0, 1, 625_000, 1_249_999] + [int(np.searchsorted(S, Y[n])) for n in rows[:3]]))
+    dW_ref, lse_all, ct_all = oracle.spot_cols(cfg, X, Y, S, w_rows, cols)
+    loss_ref = float(np.mean(lse_all - 64.0 * oracle.margin_phi(ct_all, oracle.MARGIN_ARCFACE, m)))
+    gx_h = gx.cpu().numpy()
+    gx_err = max(maxrel(gx_h[n], g) for (_, _, g), n in zip(oracle.spot_rows(cfg, X, Y, S, w_rows, rows), rows))
+    _, Vr = oracle.sgd_momentum_rows(Wrows[cols], np.zeros((len(cols), d)), dW_ref, lr, 0.9, lam)
+    Wr = Wrows[cols] - lr * Vr
+    loc = torch.from_numpy(S[cols]).cuda()
+    v_err = maxrel(V[loc].cpu().numpy(), Vr)
+    w_err = maxrel(W[loc].cpu().numpy(), Wr)
+    errs = _parity.record("test_c5_per_rank_shape_spot_parity", "bf16", loss_rel=abs(loss.item() - loss_ref) / loss_ref,
+                          grad_x=gx_err, V=v_err, W=w_err, L=loss_ref)
+    assert errs["loss_rel"] <= 1e-3 and gx_err <= 2e-2 and v_err <= 2e-2, errs
+    assert w_err <= 1e-6 + lr * 2e-2 * np.max(np.abs(Vr)) / np.max(np.abs(Wr)), errs
     L.close()

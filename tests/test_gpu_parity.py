@@ -4,6 +4,7 @@ Bars (BASELINE.json north_star; R19 metrics): sampled indices bit-exac
 on loss and max-relative (max|a-b| / max|b|) on grad_x and dW; bf16 mode 1e-3 on loss and 2e-2 on
 grad_x / dW. Inputs come from synth/ (W rows are bit-identical on both sides)."""
 import math
+import os
 
 import numpy as np
 import pytest
@@ -11,6 +12,7 @@ import torch
 
 import oracle
 import synth
+import _parity
 from oracle import OracleConfig
 
 pytestmark = pytest.mark.gpu
@@ -169,23 +171,31 @@ def _case_id(c):
 
 
 def r21_bounds(d):
-    """DESIGN.md R21: rounding x_hat and w_hat to bf16 (unit roundoff u = 2^-9) perturbs every scaled logit
-    by dz ~ N(0, sigma_z^2), sigma_z <= s u sqrt(2/d), whatever the loss. The loss error of row n is
-    sum_{j != t} p_nj dz_nj (the target logit is refined in fp32), a p-weighted average of dz times
-    (1 - p_t) <= L_n, so |dL| / L <= 4 sigma_z (4-sigma), and likewise for the gradients. The north-star bars
-    (1e-3 / 2e-2) are met where sigma_z is small against that (d = 512, init-like losses); elsewhere this
-    derived bound is the test."""
+    """DESIGN.md R21, used ONLY in the tiny-loss regime (L << 0.05): rounding x_hat and
+    w_hat to bf16 (u = 2^-9) perturbs every scaled logit by sigma_z <= s u sqrt(2/d) whatever the loss, so the
+    relative loss error cannot shrink with L there; |dL| / L <= 4 sigma_z. Every other case holds the north-star
+    bars (1e-3 / 2e-2)."""
     return 4 * 64.0 * 2.0 ** -9 * math.sqrt(2.0 / d)
 
 
-def check_bf16(L, Lr, gx, gxr, dW, dWr, d, north_star):
-    if north_star:
-        assert abs(L - Lr) / abs(Lr) <= 1e-3, (L, Lr)
-        assert maxrel(gx, gxr) <= 2e-2 and maxrel(dW, dWr) <= 2e-2
-    else:
-        g = r21_bounds(d)
-        assert abs(L - Lr) / abs(Lr) <= g, (L, Lr)
-        assert maxrel(gx, gxr) <= g and maxrel(dW, dWr) <= g
+def check(precision, L, Lr, gx, gxr, dW=None, dWr=None, Vn=None, Vnr=None, tiny_d=None):
+    """Record the measured errors (tests/_parity.py, printed in the terminal summary) and assert the bars:
+    fp32 1e-4 / 1e-4, bf16 1e-3 / 2e-2 (north_star), except the bf16 tiny-loss regime (tiny_d = d), where the
+    derived R21 bound applies."""
+    errs = {"loss_rel": abs(L - Lr) / abs(Lr), "grad_x": maxrel(gx, gxr), "L": Lr}
+    if dW is not None:
+        errs["dW"] = maxrel(dW, dWr)
+    if Vn is not None:
+        errs["V"] = maxrel(Vn, Vnr)
+    _parity.record(os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], precision, **errs)
+    tl, tg = TOL[precision]
+    if precision == "bf16" and tiny_d is not None:
+        tl = tg = r21_bounds(tiny_d)
+    assert errs["loss_rel"] <= tl, errs
+    for key in ("grad_x", "dW", "V"):
+        if key in errs:
+            assert errs[key] <= tg, (key, errs)
+    return errs
 
 
 @pytest.mark.parametrize("case", FB_CASES, ids=_case_id)
@@ -194,12 +204,7 @@ def test_forward_backward_step_parity(case, precision):
     tl, tg = TOL[precision]
     d, dist = case[1], case[6]
     for (L, Lr, gx, gxr, dW, dWr, Wn, Wnr, Vn, Vnr) in _run_single(case, precision):
-        if precision == "fp32":
-            assert abs(L - Lr) / abs(Lr) <= tl, (L, Lr)
-            assert maxrel(gx, gxr) <= tg
-            assert maxrel(dW, dWr) <= tg
-        else:
-            check_bf16(L, Lr, gx, gxr, dW, dWr, d, north_star=(d >= 512 or dist == "init"))
+        check(precision, L, Lr, gx, gxr, dW, dWr, Vn, Vnr)
         # updated rows (lr = 0.1): V within the gradient tolerance; W = W - lr V, so its error is lr times
         # V's error on top of fp32 rounding of W
         assert maxrel(Vn, Vnr) <= tg
@@ -214,13 +219,7 @@ def test_fused_train_step_parity(case, precision):
     tl, tg = TOL[precision]
     d, dist = case[1], case[6]
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, precision, fused=True):
-        if precision == "fp32" or d >= 512 or dist == "init":
-            assert abs(L - Lr) / abs(Lr) <= tl
-            assert maxrel(gx, gxr) <= tg
-            assert maxrel(Vn, Vnr) <= tg
-        else:
-            g = r21_bounds(d)
-            assert abs(L - Lr) / abs(Lr) <= g and maxrel(gx, gxr) <= g and maxrel(Vn, Vnr) <= g
+        check(precision, L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
         bound = 1e-6 + 0.1 * max(tg, 1e-4) * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
         assert maxrel(Wn, Wnr) <= bound
 
@@ -249,9 +248,7 @@ def test_fused_kernels_shapes(case, eform, monkeypatch):
     assert probe.path_flags() == (15 if eform else 7)
     probe.close()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
-        assert abs(L - Lr) / abs(Lr) <= 1e-3
-        assert maxrel(gx, gxr) <= 2e-2
-        assert maxrel(Vn, Vnr) <= 2e-2
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
         # W moves by lr * V: its error is lr times V's (the same derived bound as test_fused_train_step_parity)
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
@@ -277,9 +274,7 @@ def test_pair_kernels_train_step(case, eform, monkeypatch):
     assert probe.path_flags() == (9 if eform else 1)
     probe.close()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
-        assert abs(L - Lr) / abs(Lr) <= 1e-3
-        assert maxrel(gx, gxr) <= 2e-2
-        assert maxrel(Vn, Vnr) <= 2e-2
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
@@ -326,9 +321,7 @@ def test_eform_scale_range(B, scale):
     assert probe.path_flags() & probe.PATH_EFORM
     probe.close()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True, scale=scale):
-        assert abs(L - Lr) / abs(Lr) <= 1e-3
-        assert maxrel(gx, gxr) <= 2e-2
-        assert maxrel(Vn, Vnr) <= 2e-2
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
 
 
 @pytest.mark.parametrize("cfg", ["c4", "c4rank"])
@@ -344,9 +337,7 @@ def test_full_size_bench_workloads(cfg):
     probe.close()
     torch.cuda.empty_cache()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", steps=1, fused=True):
-        assert abs(L - Lr) / abs(Lr) <= 1e-3
-        assert maxrel(gx, gxr) <= 2e-2
-        assert maxrel(Vn, Vnr) <= 2e-2
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
@@ -393,11 +384,7 @@ def test_tiny_loss_regime(case, precision):
     within 1e-3 * max(L, 0.05) absolute and the gradients within 4 s u sqrt(2/d) max-relative."""
     d = case[1]
     for (L, Lr, gx, gxr, dW, dWr, Wn, Wnr, Vn, Vnr) in _run_single(case, precision):
-        if precision == "fp32":
-            assert abs(L - Lr) / abs(Lr) <= 1e-4
-            assert maxrel(gx, gxr) <= 1e-4 and maxrel(dW, dWr) <= 1e-4
-        else:
-            check_bf16(L, Lr, gx, gxr, dW, dWr, d, north_star=False)
+        check(precision, L, Lr, gx, gxr, dW, dWr, tiny_d=d)
 
 
 @pytest.mark.parametrize("world", [2, 4])

@@ -453,9 +453,10 @@ def test_spot_cols_agree_with_full_forward_backward():
     S = np.concatenate(out["idx"])
     X = np.concatenate(xs).astype(np.float64); Y = np.concatenate(ys)
     cols = [0, 3, len(S) // 2, int(np.searchsorted(S, Y[0]))]
-    dW, lse = oracle.spot_cols(cfg, X, Y, S, lambda i: w_rows_np(0, i, d), cols)
+    dW, lse, ct = oracle.spot_cols(cfg, X, Y, S, lambda i: w_rows_np(0, i, d), cols)
     full = np.concatenate(out["dW"])
     assert np.allclose(lse, out["lse"], rtol=1e-13)
+    assert np.allclose(ct, out["target_cos"], rtol=1e-13, atol=1e-15)
     assert np.allclose(dW, full[cols], rtol=1e-10, atol=1e-16)
 
 
