@@ -53,8 +53,23 @@ typedef enum { PFC_FP32 = 0, PFC_BF16 = 1 } pfc_precision;
  * PFC_COMM_LOOPBACK: all world_size contexts live in ONE process (any devices, typically one GPU) and are
  *   driven together by pfc_group_forward_backward; the collectives are rank-ordered device copies and
  *   rank-ascending sums (the single-matrix form of Alg.1). Used for multi-rank parity on one GPU and for the
- *   per-rank solo timing of the scaling study. pfc_forward_backward rejects such a context when world_size > 1. */
-typedef enum { PFC_COMM_NCCL = 0, PFC_COMM_LOOPBACK = 1 } pfc_comm_mode;
+ *   per-rank solo timing of the scaling study. pfc_forward_backward rejects such a context when world_size > 1.
+ * PFC_COMM_NCCL_FUSED: one process per GPU, the collectives fused into the step's kernels over NVLink peer memory
+ *   (Fig.4): the normalisation kernel stores x_hat and the labels straight into
+ *   every peer (Alg.1 L2), the row-combine / prep kernels store the row maxima and sums into the peers' slots and
+ *   read all ranks' in rank order (Alg.1 L6-7), the dX reduction stores each owner's rows into the
+ *   owner's slot (Alg.1 L12-13). The exchange region is an NCCL 2.28 symmetric window (ncclMemAlloc +
+ *   ncclCommWindowRegister), synchronised by device-side LSA barriers; all ranks must share one NVLink domain.
+ *   At world_size 1 it runs the same kernels and barriers on a 1-rank communicator. Results are deterministic
+ *   (rank-ordered reductions) and equal PFC_COMM_LOOPBACK_FUSED's.
+ * PFC_COMM_LOOPBACK_FUSED: a loopback group (as PFC_COMM_LOOPBACK, driven by pfc_group_forward_backward) whose
+ *   collectives are those fused kernels storing into the other contexts' exchange regions. */
+typedef enum {
+  PFC_COMM_NCCL = 0,
+  PFC_COMM_LOOPBACK = 1,
+  PFC_COMM_NCCL_FUSED = 2,
+  PFC_COMM_LOOPBACK_FUSED = 3
+} pfc_comm_mode;
 
 /* Which classes a shard samples (R1, R23, R24).
  * PFC_SAMPLE_PPRN       north_star rule: every positive + negatives up to k_i = max(ceil(r C_local), |P_i|).
@@ -90,7 +105,7 @@ typedef struct {
   int32_t device;        /* CUDA device ordinal for this rank                                            */
   const void* nccl_unique_id; /* 128-byte ncclUniqueId from pfc_get_unique_id on rank 0, broadcast by the
                                  caller (e.g. over torch.distributed); required iff world_size > 1 and
-                                 comm_mode == PFC_COMM_NCCL                                               */
+                                 comm_mode is PFC_COMM_NCCL or PFC_COMM_NCCL_FUSED                        */
   int32_t comm_mode;     /* pfc_comm_mode                                                                */
   int32_t sample_mode;   /* pfc_sample_mode                                                              */
   int32_t param_location; /* pfc_param_location                                                         */

@@ -22,7 +22,7 @@ LIB_PATH = os.environ.get("PFC_LIB") or os.path.join(_HERE, "_lib", "libpfc.so")
 
 MARGINS = {"none": 0, "arcface": 1, "cosface": 2}
 PRECISIONS = {"fp32": 0, "bf16": 1}
-COMM_MODES = {"nccl": 0, "loopback": 1}
+COMM_MODES = {"nccl": 0, "loopback": 1, "nccl_fused": 2, "loopback_fused": 3}
 SAMPLE_MODES = {"pprn": 0, "pprn_paper": 1, "random": 2}
 STATUS = {0: "PFC_OK", 1: "PFC_ERR_CONFIG", 2: "PFC_ERR_CONTRACT", 3: "PFC_ERR_DATA", 4: "PFC_ERR_DEGENERATE",
           5: "PFC_ERR_NUMERIC", 6: "PFC_ERR_CUDA", 7: "PFC_ERR_NCCL", 8: "PFC_ERR_OOM"}

@@ -37,6 +37,13 @@ struct pfc_ctx {
   cudaStream_t side = nullptr;                    // multi-rank: dX exchange overlapping the dW kernel
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   bool nccl_solo = false;      // PFC_NCCL_SOLO=1 at world size 1: run the NCCL collectives on a 1-rank communicator
+  // collectives fused into the kernels: PFC_COMM_NCCL_FUSED (NCCL device-API symmetric window,
+  // LSA barriers) or PFC_COMM_LOOPBACK_FUSED (the loopback group's contexts writing into each other's regions)
+  bool fused_nccl = false;
+  FusedNccl* fnccl = nullptr;
+  char* sym = nullptr;         // this rank's exchange region (pfc_internal.cuh SymLayout); X32 and Y live in it
+  Peers peers{};
+  const Peers* P() const { return peers.n ? &peers : nullptr; }
   uint64_t step = 0;
   bool fb_done = false;      // a forward_backward happened and its gradient was not yet applied
   cudaStream_t last_stream = nullptr;
@@ -44,6 +51,17 @@ struct pfc_ctx {
   std::vector<void*> allocs;
   std::vector<void*> host_allocs;   // PFC_PARAMS_HOST: page-locked, device-mapped W and V
   float* W_host = nullptr;          // host addresses of W / V in that mode (c->W / c->V are the device mapping)
+  // PFC_PARAMS_HOST with staging (default; PFC_HOST_STAGE=0: zero-copy in every kernel): the
+  // sampled rows are gathered once into HBM (Wst / Vst, k_pad x d, by position), every kernel works on them with
+  // the identity index idx_id, and the updated rows are scattered back into the host shard at the end of the step
+  bool stage = false;
+  float* Wst = nullptr;
+  float* Vst = nullptr;
+  int32_t* idx_id = nullptr;
+  // what the W / V consumers address: (W, V, idx) in HBM mode, (Wst, Vst, idx_id) when staging
+  float* Wk() const { return stage ? Wst : W; }
+  float* Vk() const { return stage ? Vst : V; }
+  const int32_t* idxk() const { return stage ? idx_id : idx; }
   float* V_host = nullptr;
 
   // parameters
@@ -55,6 +73,7 @@ struct pfc_ctx {
   float* X32 = nullptr;        // M_pad x d (all-gathered x_hat)
   int64_t* Y = nullptr;        // M
   __nv_bfloat16* Xb = nullptr; // M_pad x d
+  __half* Xh16 = nullptr;      // M_pad x d fp16: the logits operand (bf16 mode, R27)
   // sampler
   uint32_t* bits = nullptr;
   uint32_t* keys = nullptr;
@@ -65,6 +84,7 @@ struct pfc_ctx {
   int32_t* tcol = nullptr;     // M
   // sampled centres
   void* Ws = nullptr;          // k_pad x d (bf16 or fp32)
+  __half* Ws16 = nullptr;      // k_pad x d fp16 copy: the logits operand of the unfused-gather tcgen05 paths (R27)
   float* inv_norm = nullptr;   // k_pad
   float* ct = nullptr;         // M
   // logits and softmax
@@ -237,11 +257,12 @@ pfc_status validate(const pfc_config* c) {
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown sample_mode");
   if (c->param_location != PFC_PARAMS_DEVICE && c->param_location != PFC_PARAMS_HOST)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown param_location");
-  if (c->comm_mode != PFC_COMM_NCCL && c->comm_mode != PFC_COMM_LOOPBACK)
+  if (c->comm_mode < PFC_COMM_NCCL || c->comm_mode > PFC_COMM_LOOPBACK_FUSED)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown comm_mode");
-  if (c->comm_mode == PFC_COMM_LOOPBACK && c->world_size > kMaxLoopback)
-    return set_err(nullptr, PFC_ERR_CONFIG, "loopback groups support at most 16 ranks");
-  if (c->world_size > 1 && c->comm_mode == PFC_COMM_NCCL && !c->nccl_unique_id)
+  if (c->comm_mode != PFC_COMM_NCCL && c->world_size > kMaxLoopback)
+    return set_err(nullptr, PFC_ERR_CONFIG, "loopback groups and fused collectives support at most 16 ranks");
+  if (c->world_size > 1 && (c->comm_mode == PFC_COMM_NCCL || c->comm_mode == PFC_COMM_NCCL_FUSED) &&
+      !c->nccl_unique_id)
     return set_err(nullptr, PFC_ERR_CONFIG, "world_size > 1 needs nccl_unique_id");
   if ((int64_t)c->world_size * c->batch > (1 << 24)) return set_err(nullptr, PFC_ERR_CONFIG, "global batch too large");
   return PFC_OK;
@@ -355,15 +376,59 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   }
   ALLOC(c->xh_local, B * d * 4);
   ALLOC(c->xnorm, B * 4);
-  ALLOC(c->X32, Mp * d * 4);
-  ALLOC(c->Y, M * 8);
+  if (cfg->comm_mode == PFC_COMM_NCCL_FUSED || cfg->comm_mode == PFC_COMM_LOOPBACK_FUSED) {
+    // the exchange region of the fused collectives holds the all-gather targets X32 and Y (SymLayout)
+    if (cfg->comm_mode == PFC_COMM_NCCL_FUSED) {
+      // the communicator first (1 rank at world size 1: the fused code path on one GPU)
+      ncclResult_t r = ncclSuccess;
+      if (k > 1) {
+        ncclUniqueId id;
+        std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        r = ncclCommInitRank(&c->comm, k, id, i);
+      } else {
+        int dev = cfg->device;
+        r = ncclCommInitAll(&c->comm, 1, &dev);
+      }
+      if (r != ncclSuccess) {
+        std::string m = std::string("NCCL communicator: ") + ncclGetErrorString(r);
+        pfc_destroy(c);
+        return set_err(nullptr, PFC_ERR_NCCL, m);
+      }
+      std::string m;
+      pfc_status fs = fused_nccl_create(c->comm, sz, &c->fnccl, &c->sym, &c->peers, &m);
+      if (fs != PFC_OK) {
+        pfc_destroy(c);
+        return set_err(nullptr, fs, m);
+      }
+      c->fused_nccl = true;
+    } else {
+      ALLOC(c->sym, (size_t)sym_layout(sz).bytes);
+      cudaMemset(c->sym, 0, (size_t)sym_layout(sz).bytes);
+    }
+    c->X32 = reinterpret_cast<float*>(c->sym + sym_layout(sz).x32);
+    c->Y = reinterpret_cast<int64_t*>(c->sym + sym_layout(sz).y);
+  } else {
+    ALLOC(c->X32, Mp * d * 4);
+    ALLOC(c->Y, M * 8);
+  }
   ALLOC(c->Xb, Mp * d * 2);
+  if (c->bf16) ALLOC(c->Xh16, Mp * d * 2);
   ALLOC(c->bits, ((sz.C_local + 31) / 32) * 4);
   ALLOC(c->keys, (size_t)sz.ntiles_sel * kSelTile * 4);   // padded to whole compaction tiles (vector loads)
   ALLOC(c->hist, 5120 * 4);
   ALLOC(c->tile_cnt, (size_t)sz.ntiles_sel * 4 * 4);
   ALLOC(c->st, sizeof(SamplerState));
   ALLOC(c->idx, kp * 4);
+  if (cfg->param_location == PFC_PARAMS_HOST) {
+    const char* e = std::getenv("PFC_HOST_STAGE");
+    c->stage = !(e && e[0] == '0');
+  }
+  if (c->stage) {
+    ALLOC(c->Wst, kp * d * 4);
+    ALLOC(c->Vst, kp * d * 4);
+    ALLOC(c->idx_id, kp * 4);
+    launch_iota(c->idx_id, kp, 0);
+  }
   ALLOC(c->tcol, M * 4);
   ALLOC(c->Ws, kp * d * esz);
   ALLOC(c->inv_norm, kp * 4);
@@ -384,6 +449,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   ALLOC(c->dxh_local, B * d * 4);
   c->fused_gather = c->use_tc && logits_gather_supported(sz);
   c->use_dwx = c->fused_gather && dwx_supported(sz);
+  if (c->use_tc && !c->fused_gather) ALLOC(c->Ws16, kp * d * 2);
   ALLOC(c->split_ws, (size_t)(c->use_tc ? std::max(dx_split_ws_floats(sz), c->use_dwx ? dwx_ws_floats(sz) : 0) : 1) * 4);
   {
     const char* e = std::getenv("PFC_EFORM");
@@ -431,6 +497,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
   }
   cudaMemset(c->X32, 0, Mp * d * 4);
   cudaMemset(c->Xb, 0, Mp * d * 2);
+  if (c->Xh16) cudaMemset(c->Xh16, 0, Mp * d * 2);
   if (c->eform || c->eform_pair) {
     cudaMemset(c->ef_f, 0, Mp * 4);
     cudaMemset(c->Xt, 0, Mp * d * 2);
@@ -462,7 +529,7 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
     }
     c->nccl_solo = true;
   }
-  if (k > 1 && cfg->comm_mode == PFC_COMM_NCCL) {
+  if (k > 1 && cfg->comm_mode == PFC_COMM_NCCL) {   // (PFC_COMM_NCCL_FUSED created its communicator above)
     ncclUniqueId id;
     std::memcpy(&id, cfg->nccl_unique_id, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, k, id, i);
@@ -489,6 +556,7 @@ pfc_status pfc_destroy(pfc_ctx* c) {
   cudaSetDevice(c->cfg.device);
   cudaDeviceSynchronize();
   for (auto& g : c->graphs) cudaGraphExecDestroy(g.exec);
+  if (c->fnccl) fused_nccl_destroy(c->comm, c->fnccl);
   if (c->comm) ncclCommDestroy(c->comm);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
@@ -537,7 +605,7 @@ void prof_begin_step(pfc_ctx* c) {
 
 // K1: normalise this rank's features into its all-gather slot; copy labels into theirs.
 void phase_a(pfc_ctx* c, const float* x, const int64_t* labels, cudaStream_t s) {
-  c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, s);
+  c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, c->P(), s);
 }
 
 // K1b, sampler K2-K4, K5, K5b, K6 logits + partial den_i, K7 local row (max, sum).
@@ -546,50 +614,54 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
   const bool bf = c->bf16;
   int n = 0;
   mark(c, 1, s);
-  if (bf) n += launch_x_to_bf16(sz, c->X32, c->Xb, s);
+  if (bf) n += launch_x_to_bf16(sz, c->X32, c->Xb, c->Xh16, s);
   n += launch_sampler(sz, c->Y, c->cfg.seed, c->step_dev, c->bits, c->keys, c->hist, c->tile_cnt, c->st, c->idx,
                       c->tcol, c->err_dev, s);
+  if (c->stage)   // f4: the sampled W / V rows of the host shard into HBM, once
+    n += launch_stage_rows(sz, c->W, c->V, c->idx, c->st, c->Wst, c->Vst, /*to_host=*/false, s);
   mark(c, 2, s);
-  if (!c->fused_gather) n += launch_gather_w(sz, bf, c->W, c->idx, c->st, c->Ws, c->inv_norm, c->err_dev, s);
+  if (!c->fused_gather)
+    n += launch_gather_w(sz, bf, c->Wk(), c->idxk(), c->st, c->Ws, c->Ws16, c->inv_norm, c->err_dev, s);
   n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tile_cnt, c->tcol, c->ct, s);
   mark(c, 3, s);
   if (c->fused_gather)
-    n += launch_logits_gather_tc(sz, c->W, c->idx, c->Xb, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
+    n += launch_logits_gather_tc(sz, c->Wk(), c->idxk(), c->Xh16, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
                                  c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev,
                                  fused && c->eform, s);
   else if (c->use_tc && logits_pair_enabled(sz))
-    n += launch_logits_pair_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->st, c->mp, (__half*)c->cosv,
+    n += launch_logits_pair_tc(sz, c->Xh16, c->Ws16, c->tcol, c->st, c->mp, (__half*)c->cosv,
                                c->partials, fused && c->eform_pair, s);
   else if (c->use_tc)
-    n += launch_logits_tc(sz, c->Xb, (const __nv_bfloat16*)c->Ws, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
+    n += launch_logits_tc(sz, c->Xh16, c->Ws16, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);
   else
     n += launch_logits_simt(sz, bf, bf ? (const void*)c->Xb : (const void*)c->X32, c->Ws, c->tcol, c->ct, c->st, c->mp,
                             c->cosv, c->partials, s);
   mark(c, 4, s);
-  n += launch_row_combine(sz, c->partials, c->Y, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, s);
+  n += launch_row_combine(sz, c->partials, c->Y, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, c->P(), s);
   c->launches += n;
 }
 
 // after all-reduce MAX: red[n] = l_n e^{m_n - gm_n} (non-target columns), red[M + n] = local z_t
-void phase_c(pfc_ctx* c, const float* gmax, cudaStream_t s) {
-  c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->tcol, c->Y, c->ct, c->red, s);
+// (fused collectives: gmax is formed here from the peers' row maxima)
+void phase_c(pfc_ctx* c, float* gmax, cudaStream_t s) {
+  c->launches += launch_prep_sum(c->sz, c->rowmax, gmax, c->rowsum, c->zt, c->tcol, c->Y, c->ct, c->red, c->P(), s);
 }
 
 // after all-reduce SUM: LSE, loss, K8 (prob - onehot), K9 dX_hat partial
 void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
-  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, s);
+  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, c->P(), s);
   mark(c, 5, s);
   if (fused && c->eform) {
     // E-form: no softmax-gradient pass; f, X~ and the target entries, then dW + SGD + dX on E directly
     n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
                            (__nv_bfloat16*)c->cosv, c->dcorr, s);
     mark(c, 6, s);
-    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 0};
+    SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 0};
     EformArgs ef{c->ef_f, c->tcol, c->dcorr, c->xch, c->cnt, c->err_dev, c->mp.s};
-    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, c->split_ws, c->dXh, &ef, s);
+    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, c->split_ws, c->dXh, &ef, c->P(), s);
     c->launches += n;
     return;
   }
@@ -597,10 +669,11 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
     // E-form at M > 256: f, X~, the target entries and the radial dots, then dX_hat = f (E' W_s)
     n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
                            (__nv_bfloat16*)c->cosv, c->dcorr, s);
-    n += launch_eform_dotw(sz, (const __nv_bfloat16*)c->cosv, c->ef_f, c->dcorr, c->st, c->mp, c->dotw, s);
+    if (!dw_sgd_full_enabled(sz, 0))   // else the dW + SGD kernel forms the radial dots from its accumulator
+      n += launch_eform_dotw(sz, (const __nv_bfloat16*)c->cosv, c->ef_f, c->dcorr, c->st, c->mp, c->dotw, s);
     mark(c, 6, s);
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->cosv, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
-                      c->ef_f, s);
+                      c->ef_f, c->P(), s);
     c->launches += n;
     return;
   }
@@ -608,13 +681,15 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
                            fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr, s);
   mark(c, 6, s);
   if (fused && c->use_dwx) {
-    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
-    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, nullptr, s);
+    SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
+    n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, nullptr, c->P(), s);
   } else if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
-                      nullptr, s);
-  else
+                      nullptr, c->P(), s);
+  else {
     n += launch_dx_simt(sz, c->bf16, c->G, c->Ws, c->st, c->dXh, s);
+    if (c->P()) n += launch_push_dx(sz, c->dXh, c->peers, s);   // fused reduce-scatter: the owners' slots
+  }
   c->launches += n;
 }
 
@@ -625,7 +700,7 @@ void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
   if (fused && c->use_dwx) {
     // dW + SGD ran inside the dX kernel (phase_d)
   } else if (c->use_tc && fused) {
-    SgdArgs a{c->W, c->V, c->idx, c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
+    SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
               c->fused_gather ? 1 : 0};
     if (c->eform_pair)   // dW_hat = E'^T X~ (E-form): same contraction, other operands
       n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, s);
@@ -637,15 +712,21 @@ void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
     else
       n += launch_dw_simt(sz, c->bf16, c->G, c->bf16 ? (const void*)c->Xb : (const void*)c->X32, c->st, c->dWh, s);
     if (fused)
-      n += launch_sgd(sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
+      n += launch_sgd(sz, c->Wk(), c->Vk(), c->dWh, c->idxk(), c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
                       c->cfg.weight_decay, c->fused_gather ? 1 : 0, s);
   }
   c->launches += n;
 }
 
+// f4 staging: the updated sampled rows back into the host shard (after the fused train step's update)
+void stage_out(pfc_ctx* c, bool fused, cudaStream_t s) {
+  if (c->stage && fused)
+    c->launches += launch_stage_rows(c->sz, c->W, c->V, c->idx, c->st, c->Wst, c->Vst, /*to_host=*/true, s);
+}
+
 // after reduce-scatter: K10 x-norm backward of this rank's rows, K11 dW_hat (+ K12 when fused)
 void phase_e(pfc_ctx* c, const float* dxh, float* grad_x, bool fused, cudaStream_t s) {
-  c->launches += launch_xnorm_backward(c->sz, dxh, c->xh_local, c->xnorm, grad_x, s);
+  c->launches += launch_xnorm_backward(c->sz, dxh, c->xh_local, c->xnorm, grad_x, c->P(), s);
   mark(c, 8, s);
   phase_e_dw(c, fused, s);
   mark(c, 9, s);
@@ -678,11 +759,46 @@ pfc_status pfc_train_step(pfc_ctx* c, const float* x, const int64_t* labels, flo
   return run_step(c, x, labels, grad_x, loss, true, lr, stream);
 }
 
+// Collectives fused into the kernels (PFC_COMM_NCCL_FUSED, fused_comm.cu): the kernels store into the peers'
+// exchange regions, one LSA barrier after each producer.
+static void enqueue_step_fused(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss_out,
+                               bool fused, cudaStream_t s) {
+  const Sizes& sz = c->sz;
+  mark(c, 0, s);
+  phase_a(c, x, labels, s);                                  // x_hat / labels -> every peer (all-gather)
+  c->launches += launch_lsa_barrier(c->fnccl, s);
+  phase_b(c, fused, s);                                      // ... K7 row maxima -> every peer's xmax slot
+  c->launches += launch_lsa_barrier(c->fnccl, s);
+  phase_c(c, c->gmax, s);                                    // global max (rank order); sums -> peers' xred
+  c->launches += launch_lsa_barrier(c->fnccl, s);
+  phase_d(c, c->gmax, loss_out, fused, s);                   // finalize sums xred; dX rows -> owners' xdx
+  mark(c, 7, s);
+  if (!(fused && c->use_dwx) && !c->prof_cur && c->side) {
+    // barrier + x-norm backward (the reduce-scatter's reduction) on the side stream, overlapping the dW kernel
+    cudaEventRecord(c->ev_fork, s);
+    cudaStreamWaitEvent(c->side, c->ev_fork, 0);
+    c->launches += launch_lsa_barrier(c->fnccl, c->side);
+    c->launches += launch_xnorm_backward(sz, nullptr, c->xh_local, c->xnorm, grad_x, c->P(), c->side);
+    phase_e_dw(c, fused, s);
+    cudaEventRecord(c->ev_join, c->side);
+    cudaStreamWaitEvent(s, c->ev_join, 0);
+  } else {
+    c->launches += launch_lsa_barrier(c->fnccl, s);
+    phase_e(c, nullptr, grad_x, fused, s);
+  }
+  stage_out(c, fused, s);
+  c->launches += launch_advance_step(c->step_dev, c->err_dev, c->err_host_dev, s);
+}
+
 static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, float* grad_x, float* loss_out, bool fused,
                          cudaStream_t s, ncclResult_t* nres) {
   const Sizes& sz = c->sz;
   const bool multi = sz.world > 1 || c->nccl_solo;
   *nres = ncclSuccess;
+  if (c->fused_nccl) {
+    enqueue_step_fused(c, x, labels, grad_x, loss_out, fused, s);
+    return;
+  }
   auto nccl = [&](ncclResult_t r) { if (r != ncclSuccess && *nres == ncclSuccess) *nres = r; };
   mark(c, 0, s);
   phase_a(c, x, labels, s);
@@ -693,7 +809,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     nccl(ncclGroupEnd());
   }
   phase_b(c, fused, s);
-  const float* gmax = c->rowmax;
+  float* gmax = c->rowmax;
   if (multi) {  // Alg.1 L7 (stabilised, R12): global row max, then global sum
     nccl(ncclAllReduce(c->rowmax, c->gmax, sz.M, ncclFloat, ncclMax, c->comm, s));
     gmax = c->gmax;
@@ -709,7 +825,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     cudaEventRecord(c->ev_fork, s);
     cudaStreamWaitEvent(c->side, c->ev_fork, 0);
     nccl(ncclReduceScatter(c->dXh, c->dxh_local, (size_t)sz.B * sz.d, ncclFloat, ncclSum, c->comm, c->side));
-    c->launches += launch_xnorm_backward(sz, c->dxh_local, c->xh_local, c->xnorm, grad_x, c->side);
+    c->launches += launch_xnorm_backward(sz, c->dxh_local, c->xh_local, c->xnorm, grad_x, nullptr, c->side);
     phase_e_dw(c, fused, s);
     cudaEventRecord(c->ev_join, c->side);
     cudaStreamWaitEvent(s, c->ev_join, 0);
@@ -720,6 +836,7 @@ static void enqueue_step(pfc_ctx* c, const float* x, const int64_t* labels, floa
     }
     phase_e(c, dxh, grad_x, fused, s);
   }
+  stage_out(c, fused, s);
   c->launches += launch_advance_step(c->step_dev, c->err_dev, c->err_host_dev, s);
 }
 
@@ -728,7 +845,7 @@ static pfc_status run_step(pfc_ctx* c, const float* x, const int64_t* labels, fl
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   pfc_status a = check_fb_args(c, x, labels, grad_x);
   if (a != PFC_OK) return a;
-  if (c->sz.world > 1 && c->cfg.comm_mode == PFC_COMM_LOOPBACK)
+  if (c->cfg.comm_mode == PFC_COMM_LOOPBACK_FUSED || (c->sz.world > 1 && c->cfg.comm_mode == PFC_COMM_LOOPBACK))
     return set_err(c, PFC_ERR_CONTRACT, "loopback contexts are driven by pfc_group_forward_backward");
   if (pfc_status pe = pending_error(c)) return pe;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -804,7 +921,8 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   for (int r = 0; r < n; ++r) {
     pfc_ctx* c = ctxs[r];
     if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "NULL context in group");
-    if (c->sz.world != n || c->sz.rank != r || (n > 1 && c->cfg.comm_mode != PFC_COMM_LOOPBACK))
+    const bool lb = c->cfg.comm_mode == PFC_COMM_LOOPBACK || c->cfg.comm_mode == PFC_COMM_LOOPBACK_FUSED;
+    if (c->sz.world != n || c->sz.rank != r || (n > 1 && !lb) || c->cfg.comm_mode != ctxs[0]->cfg.comm_mode)
       return set_err(c, PFC_ERR_CONTRACT, "group contexts must be loopback ranks 0..n-1 of a world of size n");
     if (c->sz.B != ctxs[0]->sz.B || c->sz.d != ctxs[0]->sz.d || c->sz.C != ctxs[0]->sz.C || c->step != ctxs[0]->step)
       return set_err(c, PFC_ERR_CONTRACT, "group contexts disagree on B, d, C or step");
@@ -822,6 +940,34 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   const size_t rowbytes = (size_t)sz.B * sz.d * 4;
   pfc_ctx* c0 = ctxs[0];
   PtrPack src{}, dst{};
+  if (c0->cfg.comm_mode == PFC_COMM_LOOPBACK_FUSED) {
+    // collectives fused into the kernels (fused_comm.cu), the ranks' exchange regions being the contexts' own
+    // allocations: each phase runs for every rank before the next one consumes the peers' stores (stream order
+    // stands in for the LSA barriers of PFC_COMM_NCCL_FUSED)
+    for (int r = 0; r < n; ++r) {
+      Peers& P = ctxs[r]->peers;
+      P = Peers{};
+      for (int q = 0; q < n; ++q) P.base[q] = ctxs[q]->sym;
+      P.n = n;
+      P.rank = r;
+      P.lay = sym_layout(ctxs[r]->sz);
+    }
+    for (int r = 0; r < n; ++r) phase_a(ctxs[r], x[r], labels[r], s);
+    for (int r = 0; r < n; ++r) phase_b(ctxs[r], fused, s);
+    for (int r = 0; r < n; ++r) phase_c(ctxs[r], ctxs[r]->gmax, s);
+    for (int r = 0; r < n; ++r) phase_d(ctxs[r], ctxs[r]->gmax, r == 0 && loss ? loss : ctxs[r]->loss_dev, fused, s);
+    for (int r = 0; r < n; ++r) {
+      phase_e(ctxs[r], nullptr, grad_x[r], fused, s);
+      stage_out(ctxs[r], fused, s);
+      ctxs[r]->launches += launch_advance_step(ctxs[r]->step_dev, ctxs[r]->err_dev, ctxs[r]->err_host_dev, s);
+    }
+    if (tmap_error()) return set_err(c0, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed: kernels not launched");
+    for (int r = 0; r < n; ++r) {
+      pfc_status f = finish_fb(ctxs[r], fused, s);
+      if (f != PFC_OK) return f;
+    }
+    return PFC_OK;
+  }
   for (int r = 0; r < n; ++r) phase_a(ctxs[r], x[r], labels[r], s);
   for (int r = 0; r < n; ++r)      // all-gather: copy rank r's slot into every other rank
     for (int q = 0; q < n; ++q) {
@@ -846,6 +992,7 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
   }
   for (int r = 0; r < n; ++r) {
     phase_e(ctxs[r], ctxs[r]->dxh_local, grad_x[r], fused, s);
+    stage_out(ctxs[r], fused, s);
     ctxs[r]->launches += launch_advance_step(ctxs[r]->step_dev, ctxs[r]->err_dev, ctxs[r]->err_host_dev, s);
   }
   if (tmap_error()) return set_err(c0, PFC_ERR_CUDA, "cuTensorMapEncodeTiled failed: kernels not launched");
@@ -892,8 +1039,9 @@ pfc_status pfc_step(pfc_ctx* c, float lr, void* stream) {
     mark(c, 9, s);
   }
   c->launches += launch_set_scalar(c->lr_dev, lr, s);
-  c->launches += launch_sgd(c->sz, c->W, c->V, c->dWh, c->idx, c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
+  c->launches += launch_sgd(c->sz, c->Wk(), c->Vk(), c->dWh, c->idxk(), c->inv_norm, c->st, c->lr_dev, c->cfg.momentum,
                             c->cfg.weight_decay, c->fused_gather ? 1 : 0, s);
+  stage_out(c, true, s);
   if (c->prof) mark(c, 10, s);
   CUDA_TRY(c, cudaGetLastError());
   c->fb_done = false;
@@ -963,7 +1111,7 @@ pfc_status pfc_get_sampled_grad(pfc_ctx* c, float* dW_host, int64_t capacity_row
   float* tmp = nullptr;
   const size_t bytes = (size_t)h.k * c->sz.d * 4;
   CUDA_TRY(c, cudaMalloc(&tmp, std::max<size_t>(bytes, 16)));
-  c->launches += launch_raw_grad(c->sz, c->W, c->dWh, c->idx, c->inv_norm, c->st, tmp, c->fused_gather ? 1 : 0, 0);
+  c->launches += launch_raw_grad(c->sz, c->Wk(), c->dWh, c->idxk(), c->inv_norm, c->st, tmp, c->fused_gather ? 1 : 0, 0);
   cudaError_t e = cudaMemcpy(dW_host, tmp, bytes, cudaMemcpyDeviceToHost);
   cudaFree(tmp);
   CUDA_TRY(c, e);

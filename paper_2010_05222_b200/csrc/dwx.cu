@@ -428,8 +428,9 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
 }
 
 // dX_hat = sum of the split partials (fixed order); E-form: times f_n per batch row (dX_hat_n = f_n sum_j E'_nj w_hat_j)
+// P.n > 0 (fused reduce-scatter): each row goes straight into its owner's xdx slot `rank`
 __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
-                            const float* __restrict__ f, float* __restrict__ out) {
+                            const float* __restrict__ f, float* __restrict__ out, Peers P, int B) {
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
@@ -442,7 +443,7 @@ __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const 
     const float fn = f[i / d];
     acc.x *= fn; acc.y *= fn; acc.z *= fn; acc.w *= fn;
   }
-  *reinterpret_cast<float4*>(out + i) = acc;
+  *reinterpret_cast<float4*>(dx_dst(P, out, i, d, B)) = acc;
 }
 
 int dwx_gper(const Sizes& sz) { return std::max(1, num_sms() / (sz.d / 128)); }
@@ -457,7 +458,7 @@ bool dwx_supported(const Sizes& sz) {
 int64_t dwx_ws_floats(const Sizes& sz) { return (int64_t)dwx_gper(sz) * sz.M * sz.d; }
 
 int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
-                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, cudaStream_t s) {
+                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, const Peers* P, cudaStream_t s) {
   // W / V streamed with an L2 evict-first policy so that the G' tile re-read for dX stays resident (-0.1 to -0.2 GB
   // of DRAM reads per step at C4); PFC_DWX_HINT=0 disables
   static const bool hint = [] { const char* e = std::getenv("PFC_DWX_HINT"); return !e || std::atoi(e) != 0; }();
@@ -501,7 +502,10 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     kern<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
   }
   const int64_t n = (int64_t)sz.M * sz.d;
-  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh);
+  Peers q{};
+  if (P) q = *P;
+  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh, q,
+                                                              sz.B);
   return 2;
 }
 

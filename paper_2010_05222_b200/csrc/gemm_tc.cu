@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------------ MMA issuer (one thread)
-    constexpr uint32_t IDESC = make_idesc(128, C::UMMA_N, C::A_MN, C::B_MN);
+    constexpr uint32_t IDESC = make_idesc(128, C::UMMA_N, C::A_MN, C::B_MN, KIND == LOGITS);   // logits: fp16 (R27)
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int u = blockIdx.x; u < w.n_units; u += gridDim.x) {
@@ -422,11 +422,10 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
             __half2 h2[16];
             float cf[32];
 #pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-              const float2 f = __half22float2(h2[i]);
-              cf[2 * i] = f.x;
-              cf[2 * i + 1] = f.y;
+            for (int i = 0; i < 16; ++i) {   // fp16 cosine stored; the partials use the fp32 value (R27)
+              cf[2 * i] = __uint_as_float(v[2 * i]);
+              cf[2 * i + 1] = __uint_as_float(v[2 * i + 1]);
+              h2[i] = __floats2half2_rn(cf[2 * i], cf[2 * i + 1]);
             }
             if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {     // rare: mask columns >= k_i and the target
 #pragma unroll
@@ -556,8 +555,9 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
 }
 
 // Deterministic split-K reduction: dX[r][c] = sum_s ws[s][r][c] (fixed split order).
+// P.n > 0 (fused reduce-scatter): each row goes straight into its owner's xdx slot `rank`
 __global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
-                                const float* __restrict__ rowscale, float* __restrict__ out) {
+                                const float* __restrict__ rowscale, float* __restrict__ out, Peers P, int B) {
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
@@ -569,7 +569,7 @@ __global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, int d, co
     const float r = rowscale[i / d];
     acc.x *= r; acc.y *= r; acc.z *= r; acc.w *= r;
   }
-  *reinterpret_cast<float4*>(out + i) = acc;
+  *reinterpret_cast<float4*>(dx_dst(P, out, i, d, B)) = acc;
 }
 
 template <int KIND>
@@ -597,11 +597,11 @@ bool tc_available() {
   return major == 10 && minor == 0 && encode_fn() != nullptr;
 }
 
-int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+int launch_logits_tc(const Sizes& sz, const __half* Xh, const __half* Ws, const int32_t* tcol,
                      const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
                      cudaStream_t s) {
   (void)ct;
-  CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 operands (R27)
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
   TC_MAPS_OK();
   TcParams p{};
@@ -629,7 +629,7 @@ int64_t dx_split_ws_floats(const Sizes& sz) {
 }
 
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st, float* dXh,
-                 float* split_ws, const float* rowscale, cudaStream_t s) {
+                 float* split_ws, const float* rowscale, const Peers* P, cudaStream_t s) {
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 64);      // Gc class-major, MN-major A
   CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 64);
   TC_MAPS_OK();
@@ -642,12 +642,16 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
   if (dtile(sz) == 256) launch<DX>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
   else launch<DX128>(a, b, p, std::min(tiles * nsplit, num_sms()), s);
   const int64_t n = (int64_t)sz.M * sz.d;
-  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, sz.d, split_ws, rowscale, dXh);
+  Peers q{};
+  if (P) q = *P;
+  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, sz.d, split_ws, rowscale, dXh, q,
+                                                                  sz.B);
   return 2;
 }
 
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& sa, cudaStream_t s) {
+  if (dw_sgd_full_enabled(sz, sa.gsc)) return launch_dw_sgd_full_tc(sz, G, Xb, st, sa, s);   // dwfull.cu
   if (dw_sgd_pair_enabled(sz)) return launch_dw_sgd_pair_tc(sz, G, Xb, st, sa, s);   // dwpair.cu (CTA pairs)
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);     // Gc class-major, K-major A (= Gc^T)
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);

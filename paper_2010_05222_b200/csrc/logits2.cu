@@ -139,7 +139,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA issuer (leader CTA)
     if (leader) {
-      constexpr uint32_t IDESC = make_idesc(256, 256, false, false);
+      constexpr uint32_t IDESC = make_idesc(256, 256, false, false, true);   // fp16 operands (R27)
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
       if (ARES && n_iter > 0) {
@@ -202,11 +202,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
           for (int j = 0; j < 32; ++j) cf[j] = __uint_as_float(v[j]);
         } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) {
-            h2[i] = __floats2half2_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-            const float2 f = __half22float2(h2[i]);
-            cf[2 * i] = f.x;
-            cf[2 * i + 1] = f.y;
+          for (int i = 0; i < 16; ++i) {   // fp16 cosine stored; the partials use the fp32 value (R27)
+            cf[2 * i] = __uint_as_float(v[2 * i]);
+            cf[2 * i + 1] = __uint_as_float(v[2 * i + 1]);
+            h2[i] = __floats2half2_rn(cf[2 * i], cf[2 * i + 1]);
           }
         }
         if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
@@ -295,7 +294,7 @@ bool logits_pair_enabled(const Sizes& sz) {
   return forced != 0 && sz.M > 256 && sz.k_pad % 256 == 0;
 }
 
-int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, const int32_t* tcol,
                           const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
                           cudaStream_t s) {
   static bool attr = false;
@@ -306,7 +305,7 @@ int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_b
     cudaFuncSetAttribute(k_logits_pair<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2R_SMEM);
     attr = true;
   }
-  const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  const CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 operands (R27)
   const CUtensorMap b = make_map(Ws, sz.k_pad, sz.d, 64, 128);
   TC_MAPS_OK();
   L2Params p{};

@@ -43,6 +43,8 @@ constexpr int LG_AUX = 256 /*barriers*/ + LG_ACC * 128 * 4 /*s_inv*/ + LG_ACC * 
 constexpr int LG_SMEM = LG_STAGES * LG_STAGE + 1024 + LG_AUX;
 static_assert(LG_SMEM <= 232448, "shared memory overflow");
 static_assert(128 * LG_PITCH <= LG_W_BYTES, "W stage too small");
+constexpr int LG_WS_OFF = 128 * LG_BK * 2;              // the bf16 W_s tile after the fp16 operand tile
+static_assert(2 * LG_WS_OFF <= LG_W_BYTES, "W stage too small for both 16-bit tiles");
 
 struct LgParams {
   int M, ldm, d;
@@ -59,6 +61,10 @@ struct LgParams {
   int write_ws;            // store bf16(w) into W_s (the separate dX GEMM needs it; the fused dW/dX kernel does not)
 };
 
+__device__ __forceinline__ uint32_t pack_f16(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
 __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
@@ -157,7 +163,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     }
   } else if (warp == LG_MMA_WARP) {
     // ---------------------------------------------------------------- MMA issuer
-    constexpr uint32_t IDESC = make_idesc(128, 128, false, false);
+    constexpr uint32_t IDESC = make_idesc(128, 128, false, false, true);   // fp16 operands (R27)
     int stage = 0, acc = 0;
     uint32_t phase = 0, acc_phase = 0;
     for (int t = blockIdx.x; t < nt; t += gridDim.x) {
@@ -195,29 +201,43 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     for (int t = blockIdx.x; t < nt; t += gridDim.x) {
       const int n0 = t * 128;
       const bool valid = n0 + r < k;
-      float ss = 0.f;
+      float ss = 0.f, amax = 0.f;
       for (int kb = 0; kb < n_kb; ++kb) {
         mbar_wait(&full[stage], phase);
         uint8_t* sw = smem + stage * LG_STAGE + LG_A_BYTES;
-        uint32_t pk[32];
+        uint32_t pk[32], pb[32];
+        const bool wb = p.write_ws;
         if (valid) {
           const float4* src = reinterpret_cast<const float4*>(sw + r * LG_PITCH);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             const float4 v = src[q];
             ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
-            pk[2 * q] = pack_bf16(v.x, v.y);
-            pk[2 * q + 1] = pack_bf16(v.z, v.w);
+            amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+            pk[2 * q] = pack_f16(v.x, v.y);
+            pk[2 * q + 1] = pack_f16(v.z, v.w);
+            if (wb) {
+              pb[2 * q] = pack_bf16(v.x, v.y);
+              pb[2 * q + 1] = pack_bf16(v.z, v.w);
+            }
           }
         } else {
 #pragma unroll
-          for (int q = 0; q < 32; ++q) pk[q] = 0u;
+          for (int q = 0; q < 32; ++q) pk[q] = pb[q] = 0u;
         }
-        // every row read before the bf16 tile overwrites the head of the fp32 buffer
+        // every row read before the 16-bit tiles overwrite the head of the fp32 buffer
         asm volatile("bar.sync 5, %0;" ::"n"(32 * LG_CONV) : "memory");
-        uint4* dst = reinterpret_cast<uint4*>(sw + r * 128);   // K-major SW128: row r, 16-byte chunk c ^ (r % 8)
+        // K-major SW128: row r, 16-byte chunk c ^ (r % 8); the fp16 tile is the MMA operand (R27), the bf16 tile
+        // (16 KB further) the W_s copy for the separate dX contraction
+        uint4* dst = reinterpret_cast<uint4*>(sw + r * 128);
 #pragma unroll
         for (int c = 0; c < 8; ++c) dst[c ^ (r & 7)] = make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        if (wb) {
+          uint4* dstb = reinterpret_cast<uint4*>(sw + LG_WS_OFF + r * 128);
+#pragma unroll
+          for (int c = 0; c < 8; ++c)
+            dstb[c ^ (r & 7)] = make_uint4(pb[4 * c], pb[4 * c + 1], pb[4 * c + 2], pb[4 * c + 3]);
+        }
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&conv[stage]);
@@ -227,6 +247,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       const float inv = valid ? 1.f / fmaxf(nrm, kNormEps) : 0.f;
       p.inv_norm[n0 + r] = inv;
       if (valid && !(nrm > 0.f)) atomicOr(p.err, ERR_DEGENERATE);
+      if (amax >= 65504.f) atomicOr(p.err, ERR_NUMERIC);   // an element outside the fp16 operand range (R27)
       mbar_wait(&inv_empty[acc], acc_phase ^ 1);
       s_inv[acc * 128 + r] = inv;
       __syncwarp();
@@ -242,7 +263,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
         mbar_wait(&conv[stage], phase);
         if (lane == 0) {
           if (p.write_ws) {
-            tma_store_2d(&tmWs, smem + stage * LG_STAGE + LG_A_BYTES, kb * LG_BK, t * 128);
+            tma_store_2d(&tmWs, smem + stage * LG_STAGE + LG_A_BYTES + LG_WS_OFF, kb * LG_BK, t * 128);
             bulk_commit();
             bulk_wait_read0();                      // smem read back: the stage may be refilled
           }
@@ -296,17 +317,14 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
             }
           } else {
 #pragma unroll
-            for (int q = 0; q < 8; ++q) {
+            for (int q = 0; q < 8; ++q) {   // fp16 cosine stored; the partials use the fp32 value (R27)
               const float4 s4 = iv[q];
-              h2[2 * q] = __floats2half2_rn(__uint_as_float(v[4 * q]) * s4.x, __uint_as_float(v[4 * q + 1]) * s4.y);
-              h2[2 * q + 1] =
-                  __floats2half2_rn(__uint_as_float(v[4 * q + 2]) * s4.z, __uint_as_float(v[4 * q + 3]) * s4.w);
-            }
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              const float2 f = __half22float2(h2[i]);
-              cf[2 * i] = f.x;
-              cf[2 * i + 1] = f.y;
+              cf[4 * q] = __uint_as_float(v[4 * q]) * s4.x;
+              cf[4 * q + 1] = __uint_as_float(v[4 * q + 1]) * s4.y;
+              cf[4 * q + 2] = __uint_as_float(v[4 * q + 2]) * s4.z;
+              cf[4 * q + 3] = __uint_as_float(v[4 * q + 3]) * s4.w;
+              h2[2 * q] = __floats2half2_rn(cf[4 * q], cf[4 * q + 1]);
+              h2[2 * q + 1] = __floats2half2_rn(cf[4 * q + 2], cf[4 * q + 3]);
             }
           }
           if (col0 + 32 > k || (unsigned)(tc - col0) < 32u) {
@@ -402,7 +420,7 @@ bool logits_gather_supported(const Sizes& sz) {
   return forced != 0 && sz.M <= 256 && sz.d % LG_BK == 0 && sz.k_pad % 128 == 0;
 }
 
-int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
+int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __half* Xh,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
                             MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s) {
   static bool attr = false;
@@ -411,7 +429,7 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
     cudaFuncSetAttribute(k_logits_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
     attr = true;
   }
-  const CUtensorMap a = make_map(Xb, sz.M_pad, sz.d, 64, 128);
+  const CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 X_hat (R27)
   const CUtensorMap ws = make_map(Ws, sz.k_pad, sz.d, 64, 128);
   TC_MAPS_OK();
   LgParams p{};

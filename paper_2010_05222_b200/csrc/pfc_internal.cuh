@@ -109,6 +109,27 @@ struct Sizes {
   int ntiles_sel;          // sampler compaction tiles
 };
 
+constexpr int kMaxLoopback = 16;
+// Collectives fused into the kernels (PFC_COMM_NCCL_FUSED / PFC_COMM_LOOPBACK_FUSED): every
+// rank owns one "exchange region" laid out identically on all ranks (an NCCL symmetric window, or a plain
+// allocation of each loopback context), and the producing kernels store straight into the peers' regions:
+//   x32  [M_pad][d] f32   all-gathered x_hat: rank r writes rows [rB, rB + B) of every peer   (Alg.1 L2)
+//   y    [M] i64          all-gathered labels, likewise
+//   xmax [world][M] f32   slot r = rank r's row maxima                                          (Alg.1 L6-7)
+//   xred [world][3M+1]    slot r = rank r's rescaled sums / target logits / CA_pcc numerator
+//   xdx  [world][B][d]    slot r = rank r's dX_hat partial of this owner's rows                  (Alg.1 L12-13)
+// The consumers reduce the slots in rank order (deterministic). Peers.n == 0: plain (non-fused) kernels.
+struct SymLayout {
+  int64_t x32, y, xmax, xred, xdx, bytes;
+};
+struct Peers {
+  char* base[kMaxLoopback];   // every rank's exchange region, indexed by rank (base[rank] = this rank's)
+  int n, rank;
+  SymLayout lay;
+  __host__ __device__ float* f32(int q, int64_t off) const { return reinterpret_cast<float*>(base[q] + off); }
+};
+SymLayout sym_layout(const Sizes& sz);
+
 constexpr int kSelTile = 8192;   // sampler compaction tile (256 threads x 32)
 constexpr int kKPad = 256;       // k_pad granularity (multiple of every GEMM tile width)
 
@@ -119,34 +140,45 @@ int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint6
 
 // rows.cu
 int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
-                       float* X32, int64_t* Y, int* err, cudaStream_t s);
-int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s);
+                       float* X32, int64_t* Y, int* err, const Peers* P, cudaStream_t s);
+// X_hat -> bf16 Xb (dW / dX operand) and, when Xh16 != NULL, fp16 Xh16 (the logits operand, R27)
+int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, __half* Xh16, cudaStream_t s);
+// K5: normalised sampled rows -> W_s (bf16, or fp32 in fp32 mode) and, when Ws16 != NULL, an fp16 copy (R27)
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st,
-                    void* Ws, float* inv_norm, int* err, cudaStream_t s);
+                    void* Ws, __half* Ws16, float* inv_norm, int* err, cudaStream_t s);
 int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
                       const SamplerState* st, const int* tile_cnt /* sampler K4 tile offsets */, int32_t* tcol,
                       float* ct, cudaStream_t s);
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
-                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s);
-int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
-                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, cudaStream_t s);
+                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, const Peers* P,
+                       cudaStream_t s);
+// fused (P): gmax is computed here from the peers' xmax slots (max in rank order) and written
+int launch_prep_sum(const Sizes& sz, const float* rowmax, float* gmax, const float* rowsum, const float* zt,
+                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, const Peers* P, cudaStream_t s);
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    float* metrics, int* err, cudaStream_t s);
+                    float* metrics, int* err, const Peers* P, cudaStream_t s);
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
                         float* dotw /* per-class w_hat . dW_hat, or NULL */,
                         const float* gsc /* R25: per-class 1/||w|| folded into G, or NULL */, cudaStream_t s);
+// fused (P): dxh is ignored, the owner's xdx slots are summed in rank order
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
-                          float* grad_x, cudaStream_t s);
+                          float* grad_x, const Peers* P, cudaStream_t s);
+// fused fallback for the SIMT (fp32) dX: push the local dX_hat rows of every owner into its xdx slot
+int launch_push_dx(const Sizes& sz, const float* dXh, const Peers& P, cudaStream_t s);
 int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int32_t* idx, const float* inv_norm,
                const SamplerState* st, const float* lr_dev, float mu, float lambda, int gsc, cudaStream_t s);
 int launch_set_scalar(float* dst, float v, cudaStream_t s);
+// f4 staging: sampled rows W[idx_p], V[idx_p] <-> Wst[p], Vst[p] (p < k_i)
+int launch_stage_rows(const Sizes& sz, float* W, float* V, const int32_t* idx, const SamplerState* st, float* Wst,
+                      float* Vst, bool to_host, cudaStream_t s);
+int launch_iota(int32_t* out, int64_t n, int32_t base);   // out[i] = base + i (legacy stream)
 int launch_advance_step(uint64_t* step_dev, const int* err_dev, int* err_host_mapped, cudaStream_t s);
 int launch_raw_grad(const Sizes& sz, const float* W, const float* dWh, const int32_t* idx, const float* inv_norm,
                     const SamplerState* st, float* out, int gsc, cudaStream_t s);
 
 // loopback collectives: dst[r][i] = op_{q ascending} src[q][src_off + i] for r < ndst (op 0 = sum, 1 = max)
-constexpr int kMaxLoopback = 16;
+
 struct PtrPack { float* p[kMaxLoopback]; };
 int launch_group_reduce(int64_t n, const PtrPack& src, int64_t src_off, const PtrPack& dst, int nranks, int ndst,
                         int op, cudaStream_t s);
@@ -167,22 +199,23 @@ constexpr int kMaxSplits = 64;   // split-K bound of the dx contraction
 bool tc_available();
 int& tmap_error();   // tc_common.cuh: status of the last failed tensor-map encode (per host thread)
 int64_t dx_split_ws_floats(const Sizes& sz);
-int launch_logits_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+int launch_logits_tc(const Sizes& sz, const __half* Xh, const __half* Ws16, const int32_t* tcol,
                      const float* ct, const SamplerState* st, MarginParams mp, __half* cosv, float2* partials,
                      cudaStream_t s);
 // logits_gather.cu — K5 + K6 fused (M <= 256): sampled fp32 W rows -> norms, bf16 W_s (un-normalised), logits
 bool logits_gather_supported(const Sizes& sz);
-int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __nv_bfloat16* Xb,
+int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __half* Xh16,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
                             MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s);
 // logits2.cu — K6 on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) for M > 256
 bool logits_pair_enabled(const Sizes& sz);
-int launch_logits_pair_tc(const Sizes& sz, const __nv_bfloat16* Xb, const __nv_bfloat16* Ws, const int32_t* tcol,
+int launch_logits_pair_tc(const Sizes& sz, const __half* Xh16, const __half* Ws16, const int32_t* tcol,
                           const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
                           cudaStream_t s);
 // dX_hat = G W_s (split-K + fixed-order reduction); rowscale (E-form f_n, or NULL) multiplies each output row
+// P: the split-K reduction stores each owner's rows straight into its xdx slot (fused reduce-scatter)
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,
-                 float* dXh, float* split_ws, const float* rowscale, cudaStream_t s);
+                 float* dXh, float* split_ws, const float* rowscale, const Peers* P, cudaStream_t s);
 int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                  float* dWh, cudaStream_t s);
 // Fused K11 + K12: dW_hat tile in TMEM -> g = (dw_hat - w_hat dot)/||w||,
@@ -197,6 +230,11 @@ int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat1
 bool dw_sgd_pair_enabled(const Sizes& sz);
 int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                           const SgdArgs& sa, cudaStream_t s);
+// dwfull.cu — K11 + radial dot + K12 on CTA pairs over all d columns of 256-class tiles (M > 256, d in {256, 512},
+// normalised W_s operand); the radial dots come from the accumulator, sa.dotw is not read (PFC_DWFULL=0 disables)
+bool dw_sgd_full_enabled(const Sizes& sz, int gsc);
+int launch_dw_sgd_full_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                          const SgdArgs& sa, cudaStream_t s);
 // dwx.cu — K9 + K11 + K12 fused for the train step (M <= 256, R25 scaling): dW + SGD update + dX_hat partials
 bool dwx_supported(const Sizes& sz);
 int64_t dwx_ws_floats(const Sizes& sz);
@@ -205,7 +243,20 @@ struct EformArgs {
   const float* f; const int32_t* tcol; const float* dcorr; float* xch; int* cnt; int* err; float s;
 };
 int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
-                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, cudaStream_t s);
+                  const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, const Peers* P, cudaStream_t s);
+// fused_comm.cu — NCCL device-API exchange (PFC_COMM_NCCL_FUSED): symmetric window, LSA barrier
+struct FusedNccl;
+pfc_status fused_nccl_create(ncclComm_t comm, const Sizes& sz, FusedNccl** out, char** local_region, Peers* P,
+                             std::string* err);
+void fused_nccl_destroy(ncclComm_t comm, FusedNccl* f);
+int launch_lsa_barrier(const FusedNccl* f, cudaStream_t s);
+// the fused dX_hat push shared by the split-K reductions: row i of the M x d result goes to owner i / B, slot rank
+__device__ __forceinline__ float* dx_dst(const Peers& P, float* local, int64_t i, int d, int B) {
+  if (P.n == 0) return local + i;
+  const int64_t row = i / d, col = i % d;
+  const int q = (int)(row / B);
+  return P.f32(q, P.lay.xdx) + ((int64_t)P.rank * B + (row % B)) * d + col;
+}
 // eform.cu — E-form preparation (f_n, X~, target entries of E) and the radial dots for the unfused-dX path
 int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
                       const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,

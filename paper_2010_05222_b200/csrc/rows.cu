@@ -14,9 +14,12 @@ namespace pfc {
 namespace {
 
 // ---------------------------------------------------------------- K1
+// Fused (P.n > 0): the all-gather of Alg.1 L2 is these stores — row rB + n of x_hat and its
+// label go straight into every rank's exchange region (NVLink peer stores in PFC_COMM_NCCL_FUSED).
 __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __restrict__ x,
                               const int64_t* __restrict__ labels, float* __restrict__ xh_local,
-                              float* __restrict__ xnorm, float* __restrict__ X32, int64_t* __restrict__ Y, int* err) {
+                              float* __restrict__ xnorm, float* __restrict__ X32, int64_t* __restrict__ Y, int* err,
+                              Peers P) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
   const float* xr = x + (int64_t)warp * d;
@@ -27,25 +30,40 @@ __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __
   const float inv = 1.f / fmaxf(nrm, kNormEps);
   float* out_l = xh_local + (int64_t)warp * d;
   float* out_g = X32 + ((int64_t)rank * B + warp) * d;
-  for (int c = lane; c < d; c += 32) { float v = xr[c] * inv; out_l[c] = v; out_g[c] = v; }
+  const int64_t grow = (int64_t)rank * B + warp;
+  for (int c = lane; c < d; c += 32) {
+    float v = xr[c] * inv;
+    out_l[c] = v;
+    if (P.n == 0) out_g[c] = v;
+    for (int q = 0; q < P.n; ++q) P.f32(q, P.lay.x32)[grow * d + c] = v;
+  }
   if (lane == 0) {
     xnorm[warp] = nrm;
     int64_t y = labels[warp];
-    Y[(int64_t)rank * B + warp] = y;
+    if (P.n == 0) Y[grow] = y;
+    for (int q = 0; q < P.n; ++q) reinterpret_cast<int64_t*>(P.base[q] + P.lay.y)[grow] = y;
     if (y < 0 || y >= C) atomicOr(err, ERR_DATA);
     if (!(nrm > 0.f)) atomicOr(err, ERR_DEGENERATE);
   }
 }
 
-__global__ void k_x_to_bf16(int64_t n, const float* __restrict__ X32, __nv_bfloat16* __restrict__ Xb) {
+// X_hat operands: bf16 for the dW / dX contractions, fp16 for the logits contraction (R27: the normalised features
+// sit in [-1, 1], where fp16's 11-bit significand is 8x finer than bf16's)
+__global__ void k_x_to_bf16(int64_t n, const float* __restrict__ X32, __nv_bfloat16* __restrict__ Xb,
+                            __half* __restrict__ Xh16) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) Xb[i] = __float2bfloat16_rn(X32[i]);
+  if (i < n) {
+    const float v = X32[i];
+    Xb[i] = __float2bfloat16_rn(v);
+    if (Xh16) Xh16[i] = __float2half_rn(v);
+  }
 }
 
 // ---------------------------------------------------------------- K5: one warp per sampled row
 template <bool BF16>
 __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, const int32_t* __restrict__ idx,
-                           const SamplerState* st, void* __restrict__ Ws, float* __restrict__ inv_norm, int* err) {
+                           const SamplerState* st, void* __restrict__ Ws, __half* __restrict__ Ws16,
+                           float* __restrict__ inv_norm, int* err) {
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= k_pad) return;
@@ -56,6 +74,7 @@ __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, co
         __nv_bfloat162 z = __floats2bfloat162_rn(0.f, 0.f);
         __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)Ws + p * d + c);
         o[0] = z; o[1] = z;
+        if (Ws16) *reinterpret_cast<uint2*>(Ws16 + p * d + c) = make_uint2(0u, 0u);
       } else {
         *reinterpret_cast<float4*>((float*)Ws + p * d + c) = make_float4(0.f, 0.f, 0.f, 0.f);
       }
@@ -90,6 +109,11 @@ __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, co
       __nv_bfloat162* o = reinterpret_cast<__nv_bfloat162*>((__nv_bfloat16*)Ws + p * d + c);
       o[0] = __floats2bfloat162_rn(u.x * inv, u.y * inv);
       o[1] = __floats2bfloat162_rn(u.z * inv, u.w * inv);
+      if (Ws16) {   // the fp16 copy: B operand of the logits contraction (R27)
+        __half2* h = reinterpret_cast<__half2*>(Ws16 + p * d + c);
+        h[0] = __floats2half2_rn(u.x * inv, u.y * inv);
+        h[1] = __floats2half2_rn(u.z * inv, u.w * inv);
+      }
     } else {
       *reinterpret_cast<float4*>((float*)Ws + p * d + c) = make_float4(u.x * inv, u.y * inv, u.z * inv, u.w * inv);
     }
@@ -145,7 +169,7 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
                                                      const int64_t* __restrict__ Y, const float* __restrict__ ct,
                                                      const SamplerState* st, MarginParams mp,
                                                      float* __restrict__ rowmax, float* __restrict__ rowsum,
-                                                     float* __restrict__ zt) {
+                                                     float* __restrict__ zt, Peers P) {
   __shared__ float sm[8], ss[8];
   const int n = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -179,6 +203,7 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
       for (int i = 0; i < 8; ++i) L += sm[i] > -INFINITY ? ss[i] * __expf(sm[i] - M_) : 0.f;
     rowmax[n] = M_;
     rowsum[n] = L;
+    for (int q = 0; q < P.n; ++q) P.f32(q, P.lay.xmax)[(int64_t)P.rank * M + n] = M_;   // fused MAX all-reduce: push
     const int64_t j = Y[n] - a;
     zt[n] = (j >= 0 && j < C_local) ? mp.s * margin_phi(mp, ct[n]) : 0.f;   // owner rank of the positive
   }
@@ -192,18 +217,34 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
 //   red[M + n]  = z_t of row n on the rank owning its class (0 elsewhere)
 //   red[2M + n] = 1 if the rank sampled row n's class (the sum is 1 iff the positive is in S; R24)
 //   red[3M]     = sum of c_t over the rows whose class is on this rank (CA_pcc numerator, Eq.7)
+// Fused (P.n > 0): gm_n = max over the peers' xmax slots (the MAX all-reduce, read in rank order) is formed here and
+// stored to gmax; the 3M + 1 values are pushed into slot `rank` of every peer's xred (the SUM all-reduce's send).
 __global__ void __launch_bounds__(1024) k_prep_sum(int M, int64_t a, int64_t C_local, const float* __restrict__ rowmax,
-                                                   const float* __restrict__ gmax, const float* __restrict__ rowsum,
+                                                   float* __restrict__ gmax, const float* __restrict__ rowsum,
                                                    const float* __restrict__ zt, const int32_t* __restrict__ tcol,
                                                    const int64_t* __restrict__ Y, const float* __restrict__ ct,
-                                                   float* __restrict__ red) {
+                                                   float* __restrict__ red, Peers P) {
   __shared__ float sh[32];
   float acc = 0.f;
+  const int64_t ld = 3 * (int64_t)M + 1;
+  auto put = [&](int64_t i, float v) {
+    if (P.n == 0) red[i] = v;
+    for (int q = 0; q < P.n; ++q) P.f32(q, P.lay.xred)[(int64_t)P.rank * ld + i] = v;
+  };
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
     const float rm = rowmax[n];
-    red[n] = rm > -INFINITY ? rowsum[n] * __expf(rm - gmax[n]) : 0.f;
-    red[M + n] = zt[n];
-    red[2 * M + n] = tcol[n] >= 0 ? 1.f : 0.f;
+    float gm;
+    if (P.n) {
+      const float* xm = P.f32(P.rank, P.lay.xmax);
+      gm = xm[n];
+      for (int q = 1; q < P.n; ++q) gm = fmaxf(gm, xm[(int64_t)q * M + n]);
+      gmax[n] = gm;
+    } else {
+      gm = gmax[n];
+    }
+    put(n, rm > -INFINITY ? rowsum[n] * __expf(rm - gm) : 0.f);
+    put(M + n, zt[n]);
+    put(2 * M + n, tcol[n] >= 0 ? 1.f : 0.f);
     const int64_t j = Y[n] - a;
     if (j >= 0 && j < C_local) acc += ct[n];
   }
@@ -213,19 +254,29 @@ __global__ void __launch_bounds__(1024) k_prep_sum(int M, int64_t a, int64_t C_l
   if (threadIdx.x < 32) {
     float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
     v = warp_sum(v);
-    if (threadIdx.x == 0) red[3 * M] = v;
+    if (threadIdx.x == 0) put(3 * M, v);
   }
 }
 
 // Global LSE_n, loss (Eq.5 over the global batch, R13), g_t[n] = p_t - 1 for K8, CA_pcc (Eq.7).
+// Fused (P.n > 0): the SUM all-reduce is completed here — each value is the rank-ordered sum of the xred slots.
 __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restrict__ gmax, const float* __restrict__ red,
                                                    float* __restrict__ lse, float* __restrict__ gt,
-                                                   float* __restrict__ loss_out, float* __restrict__ metrics, int* err) {
+                                                   float* __restrict__ loss_out, float* __restrict__ metrics, int* err,
+                                                   Peers P) {
   __shared__ float sh[32];
   float acc = 0.f;
+  const int64_t ld = 3 * (int64_t)M + 1;
+  auto R = [&](int64_t i) {
+    if (P.n == 0) return red[i];
+    const float* xr = P.f32(P.rank, P.lay.xred);
+    float v = xr[i];
+    for (int q = 1; q < P.n; ++q) v += xr[(int64_t)q * ld + i];
+    return v;
+  };
   for (int n = threadIdx.x; n < M; n += blockDim.x) {
-    const float gm = gmax[n], S = red[n], z = red[M + n];
-    const bool sampled = red[2 * M + n] > 0.5f;
+    const float gm = gmax[n], S = R(n), z = R(M + n);
+    const bool sampled = R(2 * M + n) > 0.5f;
     float L, g, ls;
     if (!sampled) {                               // positive not in S (fully random): Eq.9 over S, no pull
       ls = (gm > -INFINITY && S > 0.f) ? gm + __logf(S) : -INFINITY;
@@ -264,7 +315,7 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
       const float Lm = v / (float)M;
       if (loss_out) *loss_out = Lm;
       metrics[0] = Lm;
-      metrics[1] = red[3 * M] / (float)M;
+      metrics[1] = R(3 * M) / (float)M;
       if (!isfinite(Lm)) atomicOr(err, ERR_NUMERIC);
     }
   }
@@ -435,17 +486,30 @@ __global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ 
 }
 
 // ---------------------------------------------------------------- K10
+// Fused (P.n > 0): dX_hat row n of this owner = the rank-ordered sum of its xdx slots (the reduce-scatter's
+// reduction, Alg.1 L12-13).
 __global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, const float* __restrict__ xh,
-                                 const float* __restrict__ xnorm, float* __restrict__ gx) {
+                                 const float* __restrict__ xnorm, float* __restrict__ gx, Peers P) {
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= B) return;
-  const float* g = dxh + (int64_t)n * d;
   const float* xr = xh + (int64_t)n * d;
+  const float* xd = P.n ? P.f32(P.rank, P.lay.xdx) : nullptr;
+  auto G = [&](int c) {
+    if (P.n == 0) return dxh[(int64_t)n * d + c];
+    float v = xd[(int64_t)n * d + c];
+    for (int q = 1; q < P.n; ++q) v += xd[((int64_t)q * B + n) * d + c];
+    return v;
+  };
   float dot = 0.f;
-  for (int c = lane; c < d; c += 32) dot += xr[c] * g[c];
+  for (int c = lane; c < d; c += 32) dot += xr[c] * G(c);
   dot = warp_sum(dot);
   const float inv = 1.f / fmaxf(xnorm[n], kNormEps);
-  for (int c = lane; c < d; c += 32) gx[(int64_t)n * d + c] = (g[c] - xr[c] * dot) * inv;
+  for (int c = lane; c < d; c += 32) gx[(int64_t)n * d + c] = (G(c) - xr[c] * dot) * inv;
+}
+
+__global__ void k_push_dx(int64_t n, int d, int B, const float* __restrict__ dXh, Peers P) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) *dx_dst(P, nullptr, i, d, B) = dXh[i];
 }
 
 // ---------------------------------------------------------------- K12 (+ raw-gradient introspection)
@@ -495,24 +559,42 @@ __global__ void k_sgd(int64_t k_pad, int d, float* __restrict__ W, float* __rest
 
 }  // namespace
 
+static Peers none_or(const Peers* P) {
+  Peers q{};
+  if (P) q = *P;
+  return q;
+}
+
+SymLayout sym_layout(const Sizes& sz) {
+  auto up = [](int64_t v) { return (v + 255) / 256 * 256; };
+  SymLayout L{};
+  L.x32 = 0;
+  L.y = up((int64_t)sz.M_pad * sz.d * 4);
+  L.xmax = L.y + up((int64_t)sz.M * 8);
+  L.xred = L.xmax + up((int64_t)sz.world * sz.M * 4);
+  L.xdx = L.xred + up((int64_t)sz.world * (3 * (int64_t)sz.M + 1) * 4);
+  L.bytes = L.xdx + up((int64_t)sz.world * sz.B * sz.d * 4);
+  return L;
+}
+
 int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
-                       float* X32, int64_t* Y, int* err, cudaStream_t s) {
+                       float* X32, int64_t* Y, int* err, const Peers* P, cudaStream_t s) {
   k_normalize_x<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, sz.rank, sz.C, x, labels, xh_local, xnorm, X32, Y,
-                                                        err);
+                                                        err, none_or(P));
   return 1;
 }
 
-int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, cudaStream_t s) {
+int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, __half* Xh16, cudaStream_t s) {
   int64_t n = (int64_t)sz.M * sz.d;
-  k_x_to_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, X32, Xb);
+  k_x_to_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, X32, Xb, Xh16);
   return 1;
 }
 
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st, void* Ws,
-                    float* inv_norm, int* err, cudaStream_t s) {
+                    __half* Ws16, float* inv_norm, int* err, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
-  if (bf16) k_gather_w<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, inv_norm, err);
-  else k_gather_w<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, inv_norm, err);
+  if (bf16) k_gather_w<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, Ws16, inv_norm, err);
+  else k_gather_w<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, nullptr, inv_norm, err);
   return 1;
 }
 
@@ -524,21 +606,22 @@ int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const i
 }
 
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
-                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, cudaStream_t s) {
+                       const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, const Peers* P,
+                       cudaStream_t s) {
   k_row_combine<<<sz.M, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
-                                     rowsum, zt);
+                                     rowsum, zt, none_or(P));
   return 1;
 }
 
-int launch_prep_sum(const Sizes& sz, const float* rowmax, const float* gmax, const float* rowsum, const float* zt,
-                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, cudaStream_t s) {
-  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, sz.a, sz.C_local, rowmax, gmax, rowsum, zt, tcol, Y, ct, red);
+int launch_prep_sum(const Sizes& sz, const float* rowmax, float* gmax, const float* rowsum, const float* zt,
+                    const int32_t* tcol, const int64_t* Y, const float* ct, float* red, const Peers* P, cudaStream_t s) {
+  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, sz.a, sz.C_local, rowmax, gmax, rowsum, zt, tcol, Y, ct, red, none_or(P));
   return 1;
 }
 
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    float* metrics, int* err, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err);
+                    float* metrics, int* err, const Peers* P, cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err, none_or(P));
   return 1;
 }
 
@@ -590,8 +673,14 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
 }
 
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm, float* grad_x,
-                          cudaStream_t s) {
-  k_xnorm_backward<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, dxh, xh_local, xnorm, grad_x);
+                          const Peers* P, cudaStream_t s) {
+  k_xnorm_backward<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, dxh, xh_local, xnorm, grad_x, none_or(P));
+  return 1;
+}
+
+int launch_push_dx(const Sizes& sz, const float* dXh, const Peers& P, cudaStream_t s) {
+  const int64_t n = (int64_t)sz.M * sz.d;
+  k_push_dx<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, sz.d, sz.B, dXh, P);
   return 1;
 }
 
@@ -603,6 +692,33 @@ int launch_sgd(const Sizes& sz, float* W, float* V, const float* dWh, const int3
 }
 
 namespace {
+// f4 staging: one warp per sampled position p moves the d-float rows
+// W[idx_p], V[idx_p] of the (host-mapped) shard to / from the compact HBM rows Wst[p], Vst[p]. Many rows in
+// flight per SM so that the PCIe / C2C reads stream.
+template <bool TO_HOST>
+__global__ void k_stage_rows(int64_t k_pad, int d, float* __restrict__ W, float* __restrict__ V,
+                             const int32_t* __restrict__ idx, const SamplerState* st, float* __restrict__ Wst,
+                             float* __restrict__ Vst) {
+  const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= st->k) return;
+  const int64_t j = idx[p];
+  for (int c = lane * 4; c < d; c += 128) {
+    if (TO_HOST) {
+      *reinterpret_cast<float4*>(W + j * d + c) = *reinterpret_cast<const float4*>(Wst + p * d + c);
+      *reinterpret_cast<float4*>(V + j * d + c) = *reinterpret_cast<const float4*>(Vst + p * d + c);
+    } else {
+      const float4 w = *reinterpret_cast<const float4*>(W + j * d + c);
+      const float4 v = *reinterpret_cast<const float4*>(V + j * d + c);
+      *reinterpret_cast<float4*>(Wst + p * d + c) = w;
+      *reinterpret_cast<float4*>(Vst + p * d + c) = v;
+    }
+  }
+}
+__global__ void k_iota(int32_t* out, int64_t n, int32_t base) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = base + (int32_t)i;
+}
 __global__ void k_set_f32(float* dst, float v) { *dst = v; }
 // end of a step: advance the device step counter and publish the sticky device error word to the host-mapped word
 // (plain store into page-locked memory; the host reads it at the next hot-path call without synchronising)
@@ -611,6 +727,19 @@ __global__ void k_end_step(uint64_t* dst, uint64_t v, const int* err, volatile i
   if (err_host) *err_host = *err;
 }
 }  // namespace
+
+int launch_stage_rows(const Sizes& sz, float* W, float* V, const int32_t* idx, const SamplerState* st, float* Wst,
+                      float* Vst, bool to_host, cudaStream_t s) {
+  const unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
+  if (to_host) k_stage_rows<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, idx, st, Wst, Vst);
+  else k_stage_rows<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, V, idx, st, Wst, Vst);
+  return 1;
+}
+
+int launch_iota(int32_t* out, int64_t n, int32_t base) {
+  k_iota<<<(unsigned)((n + 255) / 256), 256>>>(out, n, base);
+  return 1;
+}
 
 int launch_set_scalar(float* dst, float v, cudaStream_t s) {
   k_set_f32<<<1, 1, 0, s>>>(dst, v);

@@ -127,11 +127,11 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
-// Instruction descriptor, kind::f16: D fp32, A/B bf16, majors, N >> 3, M >> 4.
-__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn) {
+// Instruction descriptor, kind::f16: D fp32, A/B bf16 (or both fp16: f16 = true), majors, N >> 3, M >> 4.
+__host__ __device__ constexpr uint32_t make_idesc(int M, int N, bool a_mn, bool b_mn, bool f16 = false) {
   return (1u << 4)                       // c_format = F32
-         | (1u << 7)                     // a_format = BF16
-         | (1u << 10)                    // b_format = BF16
+         | ((f16 ? 0u : 1u) << 7)        // a_format = BF16 (1) / F16 (0)
+         | ((f16 ? 0u : 1u) << 10)       // b_format = BF16 (1) / F16 (0)
          | ((a_mn ? 1u : 0u) << 15)      // a_major
          | ((b_mn ? 1u : 0u) << 16)      // b_major
          | ((uint32_t)(N >> 3) << 17)    // n_dim

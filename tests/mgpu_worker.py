@@ -25,13 +25,14 @@ def maxrel(a, b):
 
 def main():
     C, d, B, r, lr, steps = int(sys.argv[1]), 512, int(sys.argv[2]), 0.1, 0.1, 3
+    comm = sys.argv[3] if len(sys.argv) > 3 else "nccl"
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     kw = dict(num_classes=C, dim=d, batch=B, sample_rate=r, margin_type="arcface", margin=0.5, momentum=0.9,
               weight_decay=5e-4, precision="bf16", seed=21)
-    L = pfc.PartialFC.from_process_group(device=local, **kw)
+    L = pfc.PartialFC.from_process_group(device=local, comm_mode=comm, **kw)
     W, V = L.params()
     synth.fill_w_shard(W, 3, L.shard_start)
     V.zero_()
@@ -57,21 +58,25 @@ def main():
     dist.gather_object(mine, allr if rank == 0 else None, dst=0)
     L.close()
     if rank == 0:
-        report = check(allr, C, d, B, r, lr, steps, world, kw)
+        report = check(allr, C, d, B, r, lr, steps, world, kw, comm)
         print("MGPU_REPORT " + json.dumps(report), flush=True)
     dist.barrier()
     dist.destroy_process_group()
 
 
-def check(allr, C, d, B, r, lr, steps, world, kw):
-    # (a) the loopback group on this GPU: the same N ranks, same inputs, collectives as device copies / sums
-    layers = [pfc.PartialFC(rank=i, world_size=world, comm_mode="loopback", device=0, **kw) for i in range(world)]
+def check(allr, C, d, B, r, lr, steps, world, kw, comm):
+    # (a) the loopback group on this GPU: the same N ranks, same inputs, collectives as device copies / sums (or, for
+    # the fused NCCL path, the same fused kernels storing into the other contexts' regions)
+    lb = "loopback_fused" if comm == "nccl_fused" else "loopback"
+    layers = [pfc.PartialFC(rank=i, world_size=world, comm_mode=lb, device=0, **kw) for i in range(world)]
     for Lq in layers:
         Wq, Vq = Lq.params()
         synth.fill_w_shard(Wq, 3, Lq.shard_start)
         Vq.zero_()
-    exact = world == 2     # a + b is order-free: NCCL and the loopback sums agree bit for bit at N = 2
-    rep = {"world": world, "exact_expected": exact, "steps": []}
+    # a + b is order-free: NCCL and the loopback sums agree bit for bit at N = 2; the fused path reduces in rank
+    # order on every rank, exactly like its loopback group, at any N
+    exact = world == 2 or comm == "nccl_fused"
+    rep = {"world": world, "comm": comm, "exact_expected": exact, "steps": []}
     for i in range(steps):
         xs = synth.make_features(30, i, world, B, d)
         ys = synth.make_labels(30, i, world, B, C)

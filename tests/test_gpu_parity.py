@@ -212,7 +212,7 @@ def test_forward_backward_step_parity(case, precision):
         assert maxrel(Wn, Wnr) <= bound
 
 
-@pytest.mark.parametrize("case", [FB_CASES[0], FB_CASES[2], FB_CASES[4], FB_CASES[5]], ids=_case_id)
+@pytest.mark.parametrize("case", FB_CASES, ids=_case_id)
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_fused_train_step_parity(case, precision):
     """pfc_train_step (SGD inside the dW epilogue) against the oracle's forward_backward + SGD."""

@@ -24,9 +24,10 @@ def _free_port():
     return p
 
 
+@pytest.mark.parametrize("comm", ["nccl", "nccl_fused"])
 @pytest.mark.parametrize("nproc", ["2", "all"])
 @pytest.mark.parametrize("C,B", [(40_000, 64), (200_000, 256)], ids=["fused-M", "pair-M"])
-def test_nccl_ranks_match_loopback_and_oracle(nproc, C, B):
+def test_nccl_ranks_match_loopback_and_oracle(nproc, C, B, comm):
     n = torch.cuda.device_count() if torch.cuda.is_available() else 0
     if n < 2:
         pytest.skip(f"needs >= 2 GPUs (found {n})")
@@ -35,7 +36,7 @@ def test_nccl_ranks_match_loopback_and_oracle(nproc, C, B):
         pytest.skip("same as nproc=2")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "tests", "mgpu_worker.py"),
-           str(C), str(B)]
+           str(C), str(B), comm]
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-3000:])
     lines = [l for l in r.stdout.splitlines() if l.startswith("MGPU_REPORT ")]
