@@ -109,6 +109,10 @@ typedef struct {
   int32_t comm_mode;     /* pfc_comm_mode                                                                */
   int32_t sample_mode;   /* pfc_sample_mode                                                              */
   int32_t param_location; /* pfc_param_location                                                         */
+  int32_t ignore_index;  /* 0: every label must be in [0, C) (else PFC_ERR_DATA). 1: a label of -1 marks an
+                            ignored row (PyTorch ignore_index = -1, R28): it
+                            contributes no loss and receives zero grad_x; the mean of Eq.5 and the gradients
+                            divide by the number of rows not ignored (global over the ranks; 1 if all are)     */
 } pfc_config;
 
 typedef struct pfc_ctx pfc_ctx;

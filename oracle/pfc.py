@@ -57,6 +57,7 @@ class OracleConfig:
     weight_decay: float = 0.0 # lambda (R15, explicit)
     seed: int = 0
     sample_mode: int = SAMPLE_PPRN
+    ignore_index: bool = False  # R28: a label of -1 marks an ignored row (PyTorch ignore_index = -1)
 
 
 # ----------------------------------------------------------------------------------------------
@@ -170,8 +171,12 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     X = np.concatenate([np.asarray(x, dtype=np.float64).reshape(B, d) for x in xs], axis=0)
     Y = np.concatenate([np.asarray(y, dtype=np.int64).reshape(B) for y in ys], axis=0)
     M = k * B
-    if np.any(Y < 0) or np.any(Y >= C):
+    # R28: with ignore_index, rows labelled -1 take no part in Eq.5 — no loss term, no
+    # gradient, no positive class — and the mean runs over the M_valid other rows
+    ign = (Y == -1) if cfg.ignore_index else np.zeros(M, dtype=bool)
+    if np.any(((Y < 0) | (Y >= C)) & ~ign):
         raise ValueError("label outside [0, C) (R7)")
+    M_valid = max(int(np.sum(~ign)), 1)
     Xh, xnorm = normalize_rows(X)                                    # Eq.6: fix ||x|| by l2 normalisation
 
     # PPRN steps 1-3 on every shard, then W^s = [w_1^s, ..., w_k^s] (Eq.10) in rank order.
@@ -191,8 +196,8 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     rows = np.arange(M)
     hit = tcol >= 0
     # cos(theta) between each row and its own class centre (sampled or not): Eq.7's CA_pcc and z_t
-    Wy, _ = normalize_rows(np.asarray(w_rows(Y), dtype=np.float64).reshape(M, d))
-    ct = np.sum(Xh * Wy, axis=1)
+    Wy, _ = normalize_rows(np.asarray(w_rows(np.where(ign, 0, Y)), dtype=np.float64).reshape(M, d))
+    ct = np.where(ign, 0.0, np.sum(Xh * Wy, axis=1))
     zt = s * margin_phi(ct, mt, m)
     Z = s * cos
     Z[rows[hit], tcol[hit]] = zt[hit]
@@ -204,15 +209,17 @@ def forward_backward(cfg, xs, ys, w_rows, step=0, keep_intermediates=False):
     prob = np.exp(Z - lse[:, None])
     # Eq.5 (R13: mean over the global batch M = N k). A row whose positive is not in S (fully random, R24)
     # keeps Eq.9's denominator over S and its own positive logit as numerator.
-    loss = float(np.mean(lse - zt))
-    ca_pcc = float(np.mean(ct))                                      # Eq.7
+    # R28: ignored rows are left out of the mean (M_valid = M without ignore_index)
+    loss = float(np.sum(np.where(ign, 0.0, lse - zt)) / M_valid)
+    ca_pcc = float(np.sum(ct) / M_valid)                             # Eq.7 (ct = 0 on ignored rows)
 
     # Alg.1 L9: grad logits = prob - onehot, times dL/dlogits scale 1/M, chained through
     # z = s * phi(c) at the target and z = s * c elsewhere. R24: no onehot term (no positive pull) when the
     # positive is not sampled.
     onehot = np.zeros_like(prob)
     onehot[rows[hit], tcol[hit]] = 1.0
-    G = (prob - onehot) / M                                          # dL/dZ
+    G = (prob - onehot) / M_valid                                    # dL/dZ
+    G[ign] = 0.0                                                     # R28: an ignored row has no gradient
     Gc = s * G                                                       # dL/dcos, non-target columns
     Gc[rows[hit], tcol[hit]] *= margin_dphi(ct[hit], mt, m)
 

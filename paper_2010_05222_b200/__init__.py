@@ -52,7 +52,8 @@ class _Config(ctypes.Structure):
                 ("margin", ctypes.c_float), ("momentum", ctypes.c_float), ("weight_decay", ctypes.c_float),
                 ("precision", ctypes.c_int32), ("seed", ctypes.c_uint64), ("rank", ctypes.c_int32),
                 ("world_size", ctypes.c_int32), ("device", ctypes.c_int32), ("nccl_unique_id", ctypes.c_void_p),
-                ("comm_mode", ctypes.c_int32), ("sample_mode", ctypes.c_int32), ("param_location", ctypes.c_int32)]
+                ("comm_mode", ctypes.c_int32), ("sample_mode", ctypes.c_int32), ("param_location", ctypes.c_int32),
+                ("ignore_index", ctypes.c_int32)]
 
 
 _lib = None
@@ -136,7 +137,8 @@ class PartialFC:
 
     def __init__(self, num_classes, dim, batch, sample_rate=0.1, scale=64.0, margin_type="arcface", margin=0.5,
                  momentum=0.9, weight_decay=0.0, precision="bf16", seed=0, rank=0, world_size=1, device=0,
-                 nccl_unique_id=None, comm_mode="nccl", sample_mode="pprn", param_location="device"):
+                 nccl_unique_id=None, comm_mode="nccl", sample_mode="pprn", param_location="device",
+                 ignore_index=False):
         self._lib = load_library()
         self.param_location = param_location
         self.rank, self.world_size, self.device = rank, world_size, device
@@ -149,7 +151,7 @@ class PartialFC:
                       world_size, device, ctypes.cast(self._id_buf, ctypes.c_void_p) if self._id_buf else None,
                       COMM_MODES[comm_mode] if isinstance(comm_mode, str) else int(comm_mode),
                       SAMPLE_MODES[sample_mode] if isinstance(sample_mode, str) else int(sample_mode),
-                      PARAM_LOCATIONS[param_location])
+                      PARAM_LOCATIONS[param_location], 1 if ignore_index else 0)
         h = ctypes.c_void_p()
         s = self._lib.pfc_init(ctypes.byref(cfg), ctypes.byref(h))
         if s:

@@ -255,6 +255,7 @@ pfc_status validate(const pfc_config* c) {
   if (!(c->weight_decay >= 0.f)) return set_err(nullptr, PFC_ERR_CONFIG, "weight_decay must be >= 0");
   if (c->sample_mode < PFC_SAMPLE_PPRN || c->sample_mode > PFC_SAMPLE_RANDOM)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown sample_mode");
+  if (c->ignore_index != 0 && c->ignore_index != 1) return set_err(nullptr, PFC_ERR_CONFIG, "ignore_index must be 0 or 1");
   if (c->param_location != PFC_PARAMS_DEVICE && c->param_location != PFC_PARAMS_HOST)
     return set_err(nullptr, PFC_ERR_CONFIG, "unknown param_location");
   if (c->comm_mode < PFC_COMM_NCCL || c->comm_mode > PFC_COMM_LOOPBACK_FUSED)
@@ -605,7 +606,8 @@ void prof_begin_step(pfc_ctx* c) {
 
 // K1: normalise this rank's features into its all-gather slot; copy labels into theirs.
 void phase_a(pfc_ctx* c, const float* x, const int64_t* labels, cudaStream_t s) {
-  c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, c->P(), s);
+  c->launches += launch_normalize_x(c->sz, x, labels, c->xh_local, c->xnorm, c->X32, c->Y, c->err_dev, c->P(),
+                                    c->cfg.ignore_index, s);
 }
 
 // K1b, sampler K2-K4, K5, K5b, K6 logits + partial den_i, K7 local row (max, sum).
@@ -652,12 +654,13 @@ void phase_c(pfc_ctx* c, float* gmax, cudaStream_t s) {
 void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStream_t s) {
   const Sizes& sz = c->sz;
   int n = 0;
-  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, c->P(), s);
+  n += launch_finalize(sz, gmax, c->red, c->lse, c->gt, loss_out, c->metrics, c->err_dev, c->P(), c->Y,
+                       c->cfg.ignore_index, s);
   mark(c, 5, s);
   if (fused && c->eform) {
     // E-form: no softmax-gradient pass; f, X~ and the target entries, then dW + SGD + dX on E directly
     n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
-                           (__nv_bfloat16*)c->cosv, c->dcorr, s);
+                           (__nv_bfloat16*)c->cosv, c->dcorr, c->metrics + 2, s);
     mark(c, 6, s);
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 0};
     EformArgs ef{c->ef_f, c->tcol, c->dcorr, c->xch, c->cnt, c->err_dev, c->mp.s};
@@ -668,7 +671,7 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
   if (fused && c->eform_pair) {
     // E-form at M > 256: f, X~, the target entries and the radial dots, then dX_hat = f (E' W_s)
     n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
-                           (__nv_bfloat16*)c->cosv, c->dcorr, s);
+                           (__nv_bfloat16*)c->cosv, c->dcorr, c->metrics + 2, s);
     if (!dw_sgd_full_enabled(sz, 0))   // else the dW + SGD kernel forms the radial dots from its accumulator
       n += launch_eform_dotw(sz, (const __nv_bfloat16*)c->cosv, c->ef_f, c->dcorr, c->st, c->mp, c->dotw, s);
     mark(c, 6, s);
@@ -678,7 +681,8 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
     return;
   }
   n += launch_softmax_grad(sz, c->bf16, c->cosv, c->lse, c->gt, c->tcol, c->ct, c->st, c->mp, c->G,
-                           fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr, s);
+                           fused && c->use_tc ? c->dotw : nullptr, c->fused_gather ? c->inv_norm : nullptr,
+                           c->metrics + 2, s);
   mark(c, 6, s);
   if (fused && c->use_dwx) {
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};

@@ -19,10 +19,11 @@ namespace {
 __global__ void k_eform_prep(int M, int ldm, int d, const float* __restrict__ X32, const float* __restrict__ lse,
                              const float* __restrict__ gt, const int32_t* __restrict__ tcol,
                              const float* __restrict__ ct, MarginParams mp, float* __restrict__ f,
-                             __nv_bfloat16* __restrict__ Xt, __nv_bfloat16* __restrict__ E, float* __restrict__ dcorr) {
+                             __nv_bfloat16* __restrict__ Xt, __nv_bfloat16* __restrict__ E, float* __restrict__ dcorr,
+                             const float* __restrict__ mvalid) {
   const int n = blockIdx.x;
   if (n >= M) return;
-  const float gs = mp.s / (float)M;
+  const float gs = mp.s / *mvalid;   // the mean runs over the rows not ignored (finalize; = M without ignore_index)
   const float fn = gs * expf(-lse[n]);
   for (int c = threadIdx.x * 2; c < d; c += blockDim.x * 2) {
     const float2 v = *reinterpret_cast<const float2*>(X32 + (int64_t)n * d + c);
@@ -93,9 +94,9 @@ __global__ void __launch_bounds__(256) k_eform_dotw(int64_t k_pad, int ldm, floa
 
 int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
                       const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
-                      cudaStream_t s) {
+                      const float* mvalid, cudaStream_t s) {
   cudaMemsetAsync(dcorr, 0, (size_t)sz.k_pad * sizeof(float), s);
-  k_eform_prep<<<sz.M, 128, 0, s>>>(sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr);
+  k_eform_prep<<<sz.M, 128, 0, s>>>(sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr, mvalid);
   return 1;
 }
 

@@ -139,8 +139,9 @@ int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint6
                    int* err, cudaStream_t s);
 
 // rows.cu
+// ignore != 0: label -1 marks an ignored row (f3, R28) instead of a DATA error
 int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
-                       float* X32, int64_t* Y, int* err, const Peers* P, cudaStream_t s);
+                       float* X32, int64_t* Y, int* err, const Peers* P, int ignore, cudaStream_t s);
 // X_hat -> bf16 Xb (dW / dX operand) and, when Xh16 != NULL, fp16 Xh16 (the logits operand, R27)
 int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, __half* Xh16, cudaStream_t s);
 // K5: normalised sampled rows -> W_s (bf16, or fp32 in fp32 mode) and, when Ws16 != NULL, an fp16 copy (R27)
@@ -155,12 +156,14 @@ int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y
 // fused (P): gmax is computed here from the peers' xmax slots (max in rank order) and written
 int launch_prep_sum(const Sizes& sz, const float* rowmax, float* gmax, const float* rowsum, const float* zt,
                     const int32_t* tcol, const int64_t* Y, const float* ct, float* red, const Peers* P, cudaStream_t s);
+// metrics[0] = loss, [1] = CA_pcc, [2] = M_valid (rows not ignored, >= 1): the mean's and gradients' divisor
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    float* metrics, int* err, const Peers* P, cudaStream_t s);
+                    float* metrics, int* err, const Peers* P, const int64_t* Y, int ignore, cudaStream_t s);
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
                         float* dotw /* per-class w_hat . dW_hat, or NULL */,
-                        const float* gsc /* R25: per-class 1/||w|| folded into G, or NULL */, cudaStream_t s);
+                        const float* gsc /* R25: per-class 1/||w|| folded into G, or NULL */,
+                        const float* mvalid /* device: rows not ignored (finalize) */, cudaStream_t s);
 // fused (P): dxh is ignored, the owner's xdx slots are summed in rank order
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm,
                           float* grad_x, const Peers* P, cudaStream_t s);
@@ -260,7 +263,7 @@ __device__ __forceinline__ float* dx_dst(const Peers& P, float* local, int64_t i
 // eform.cu — E-form preparation (f_n, X~, target entries of E) and the radial dots for the unfused-dX path
 int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const float* gt, const int32_t* tcol,
                       const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
-                      cudaStream_t s);
+                      const float* mvalid /* device: rows not ignored (finalize) */, cudaStream_t s);
 int launch_eform_dotw(const Sizes& sz, const __nv_bfloat16* E, const float* f, const float* dcorr,
                       const SamplerState* st, MarginParams mp, float* dotw, cudaStream_t s);
 

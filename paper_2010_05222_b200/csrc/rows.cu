@@ -19,7 +19,7 @@ namespace {
 __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __restrict__ x,
                               const int64_t* __restrict__ labels, float* __restrict__ xh_local,
                               float* __restrict__ xnorm, float* __restrict__ X32, int64_t* __restrict__ Y, int* err,
-                              Peers P) {
+                              Peers P, int ignore) {
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
   const float* xr = x + (int64_t)warp * d;
@@ -42,7 +42,7 @@ __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __
     int64_t y = labels[warp];
     if (P.n == 0) Y[grow] = y;
     for (int q = 0; q < P.n; ++q) reinterpret_cast<int64_t*>(P.base[q] + P.lay.y)[grow] = y;
-    if (y < 0 || y >= C) atomicOr(err, ERR_DATA);
+    if ((y < 0 || y >= C) && !(ignore && y == -1)) atomicOr(err, ERR_DATA);
     if (!(nrm > 0.f)) atomicOr(err, ERR_DEGENERATE);
   }
 }
@@ -263,9 +263,11 @@ __global__ void __launch_bounds__(1024) k_prep_sum(int M, int64_t a, int64_t C_l
 __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restrict__ gmax, const float* __restrict__ red,
                                                    float* __restrict__ lse, float* __restrict__ gt,
                                                    float* __restrict__ loss_out, float* __restrict__ metrics, int* err,
-                                                   Peers P) {
+                                                   Peers P, const int64_t* __restrict__ Y, int ignore) {
   __shared__ float sh[32];
+  __shared__ int shn[32];
   float acc = 0.f;
+  int nvalid = 0;
   const int64_t ld = 3 * (int64_t)M + 1;
   auto R = [&](int64_t i) {
     if (P.n == 0) return red[i];
@@ -278,6 +280,12 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
     const float gm = gmax[n], S = R(n), z = R(M + n);
     const bool sampled = R(2 * M + n) > 0.5f;
     float L, g, ls;
+    if (ignore && Y[n] == -1) {                   // ignored row (f3, R28): no loss term, no gradient (p = 0)
+      lse[n] = INFINITY;
+      gt[n] = 0.f;
+      continue;
+    }
+    ++nvalid;
     if (!sampled) {                               // positive not in S (fully random): Eq.9 over S, no pull
       ls = (gm > -INFINITY && S > 0.f) ? gm + __logf(S) : -INFINITY;
       L = ls - z;
@@ -306,16 +314,21 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
     acc += L;
   }
   acc = warp_sum(acc);
-  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = acc;
+  for (int o = 16; o; o >>= 1) nvalid += __shfl_xor_sync(0xffffffffu, nvalid, o);
+  if ((threadIdx.x & 31) == 0) { sh[threadIdx.x >> 5] = acc; shn[threadIdx.x >> 5] = nvalid; }
   __syncthreads();
   if (threadIdx.x < 32) {
     float v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : 0.f;
+    int nv = threadIdx.x < (blockDim.x >> 5) ? shn[threadIdx.x] : 0;
     v = warp_sum(v);
+    for (int o = 16; o; o >>= 1) nv += __shfl_xor_sync(0xffffffffu, nv, o);
     if (threadIdx.x == 0) {
-      const float Lm = v / (float)M;
+      const float Mv = (float)max(nv, 1);          // every row ignored: loss 0, no gradient
+      const float Lm = v / Mv;
       if (loss_out) *loss_out = Lm;
       metrics[0] = Lm;
-      metrics[1] = R(3 * M) / (float)M;
+      metrics[1] = R(3 * M) / Mv;
+      metrics[2] = Mv;
       if (!isfinite(Lm)) atomicOr(err, ERR_NUMERIC);
     }
   }
@@ -365,10 +378,11 @@ template <bool BF16, bool DOT>
 __global__ void __launch_bounds__(256) k_softmax_grad(int64_t k_pad, int M, int ldm, const void* __restrict__ cosv,
                                                       const float* __restrict__ lse, const SamplerState* st,
                                                       MarginParams mp, void* __restrict__ G,
-                                                      float* __restrict__ dotw, const float* __restrict__ gsc) {
+                                                      float* __restrict__ dotw, const float* __restrict__ gsc,
+                                                      const float* __restrict__ mvalid) {
   extern __shared__ float s_off[];            // transposed: pos(n) = (n % 8) * (ldm / 8) + n / 8
   const float L2E = 1.4426950408889634f;
-  const float lgs = log2f(mp.s / (float)M);
+  const float lgs = log2f(mp.s / *mvalid);    // (s / M_valid): the mean over the rows not ignored
   const int l8 = ldm >> 3;
   for (int n = threadIdx.x; n < ldm; n += blockDim.x) s_off[(n & 7) * l8 + (n >> 3)] = n < M ? lse[n] * L2E - lgs : INFINITY;
   __syncthreads();
@@ -466,13 +480,14 @@ template <bool BF16, bool DOT>
 __global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ cosv, const float* __restrict__ lse,
                                        const float* __restrict__ gt, const int32_t* __restrict__ tcol,
                                        const float* __restrict__ ct, MarginParams mp, void* __restrict__ G,
-                                       float* __restrict__ dotw, const float* __restrict__ gsc) {
+                                       float* __restrict__ dotw, const float* __restrict__ gsc,
+                                       const float* __restrict__ mvalid) {
   const int n = blockIdx.x * blockDim.x + threadIdx.x;
   if (n >= M) return;
   const int j = tcol[n];
   if (j < 0) return;
   const float L2E = 1.4426950408889634f;
-  const float gs = mp.s / (float)M;
+  const float gs = mp.s / *mvalid;
   const int64_t e = (int64_t)j * ldm + n;
   const float cst = BF16 ? __half2float(((const __half*)cosv)[e]) : ((const float*)cosv)[e];
   const float lgs = log2f(gs);
@@ -578,9 +593,9 @@ SymLayout sym_layout(const Sizes& sz) {
 }
 
 int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
-                       float* X32, int64_t* Y, int* err, const Peers* P, cudaStream_t s) {
+                       float* X32, int64_t* Y, int* err, const Peers* P, int ignore, cudaStream_t s) {
   k_normalize_x<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, sz.rank, sz.C, x, labels, xh_local, xnorm, X32, Y,
-                                                        err, none_or(P));
+                                                        err, none_or(P), ignore);
   return 1;
 }
 
@@ -620,14 +635,14 @@ int launch_prep_sum(const Sizes& sz, const float* rowmax, float* gmax, const flo
 }
 
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
-                    float* metrics, int* err, const Peers* P, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err, none_or(P));
+                    float* metrics, int* err, const Peers* P, const int64_t* Y, int ignore, cudaStream_t s) {
+  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err, none_or(P), Y, ignore);
   return 1;
 }
 
 int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const float* lse, const float* gt,
                         const int32_t* tcol, const float* ct, const SamplerState* st, MarginParams mp, void* G,
-                        float* dotw, const float* gsc, cudaStream_t s) {
+                        float* dotw, const float* gsc, const float* mvalid, cudaStream_t s) {
   const size_t smem = (size_t)sz.M_pad * sizeof(float);
   static bool attr = false;
   if (!attr) {
@@ -654,19 +669,19 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
   const unsigned tg = (unsigned)((sz.M + 255) / 256);
   if (bf16) {
     if (dotw) {
-      k_softmax_grad<true, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
-      k_softmax_grad_targets<true, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
+      k_softmax_grad<true, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc, mvalid);
+      k_softmax_grad_targets<true, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc, mvalid);
     } else {
-      k_softmax_grad<true, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
-      k_softmax_grad_targets<true, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
+      k_softmax_grad<true, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc, mvalid);
+      k_softmax_grad_targets<true, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc, mvalid);
     }
   } else {
     if (dotw) {
-      k_softmax_grad<false, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
-      k_softmax_grad_targets<false, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
+      k_softmax_grad<false, true><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc, mvalid);
+      k_softmax_grad_targets<false, true><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc, mvalid);
     } else {
-      k_softmax_grad<false, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc);
-      k_softmax_grad_targets<false, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc);
+      k_softmax_grad<false, false><<<grid, 256, smem, s>>>(sz.k_pad, sz.M, ldm, cosv, lse, st, mp, G, dotw, gsc, mvalid);
+      k_softmax_grad_targets<false, false><<<tg, 256, 0, s>>>(sz.M, ldm, cosv, lse, gt, tcol, ct, mp, G, dotw, gsc, mvalid);
     }
   }
   return 2;

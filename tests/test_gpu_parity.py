@@ -734,3 +734,56 @@ def test_update_touches_exactly_the_sampled_rows(C, d, B, precision, fused):
     assert torch.isfinite(W[idx]).all() and torch.isfinite(V[idx]).all()
     assert (V[idx] != V0[idx]).any(dim=1).all()
     L.close()
+
+
+@pytest.mark.parametrize("B,world", [(48, 1), (320, 1), (24, 2)], ids=["fusedM48", "pairM320", "loopback2"])
+@pytest.mark.parametrize("precision", ["bf16", "fp32"])
+@pytest.mark.parametrize("train", [True, False], ids=["train_step", "fwd_bwd"])
+def test_ignore_index_parity(B, world, precision, train):
+    """SURVEY.md §8(f) f3 / DESIGN.md R28: rows labelled -1 with ignore_index — no loss term, zero grad_x, no positive;
+    the mean over the other rows. Against the oracle (ids bit-exact, north-star bars); ignored rows' grad_x exactly 0."""
+    C, d = 20000, 256
+    layers = [pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=0.1, margin_type="arcface", margin=0.5,
+                            momentum=0.9, weight_decay=5e-4, precision=precision, seed=4, rank=i, world_size=world,
+                            comm_mode="loopback" if world > 1 else "nccl", ignore_index=True) for i in range(world)]
+    for L in layers:
+        W, V = L.params()
+        synth.fill_w_shard(W, 2, L.shard_start)
+        V.zero_()
+    ys = synth.make_labels(14, 0, world, B, C)
+    for i, y in enumerate(ys):
+        y[(np.arange(B) * 7 + i) % 5 == 0] = -1          # ~1/5 of the rows ignored, on every rank
+    xs = synth.make_features(14, 0, world, B, d)
+    xt = [torch.from_numpy(x).cuda() for x in xs]
+    yt = [torch.from_numpy(y).cuda() for y in ys]
+    gt = [torch.empty_like(x) for x in xt]
+    loss = torch.zeros(1, device="cuda")
+    lr = 0.1
+    if world == 1:
+        (layers[0].train_step if train else layers[0].forward_backward)(xt[0], yt[0], gt[0], loss,
+                                                                        **({"lr": lr} if train else {}))
+    else:
+        pfc.group_forward_backward(layers, xt, yt, gt, loss, lr=lr if train else None)
+    torch.cuda.synchronize()
+    for L in layers:
+        L.check()
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, world_size=world, sample_rate=0.1, margin_type=1, margin=0.5,
+                       momentum=0.9, weight_decay=5e-4, seed=4, ignore_index=True)
+    ref = oracle.forward_backward(cfg, xs, ys, lambda ids: synth.w_rows_np(2, ids, d), step=0)
+    for i, L in enumerate(layers):
+        idx = L.sampled()
+        assert np.array_equal(idx, ref["idx"][i])
+        g = gt[i].cpu().numpy()
+        assert not np.any(g[ys[i] == -1])
+        W, V = L.params()
+        if train:
+            w0 = synth.w_rows_np(2, idx, d)
+            _, Vr = oracle.sgd_momentum_rows(w0, np.zeros_like(w0), ref["dW"][i], lr, 0.9, 5e-4)
+            check(precision, loss.item(), ref["loss"], g, ref["grad_x"][i],
+                  Vn=V[torch.from_numpy(idx - L.shard_start).cuda()].cpu().numpy(), Vnr=Vr)
+        else:
+            check(precision, loss.item(), ref["loss"], g, ref["grad_x"][i], L.sampled_grad(), ref["dW"][i])
+    L0, ca = layers[0].metrics()
+    assert abs(ca - ref["ca_pcc"]) <= 1e-5
+    for L in layers:
+        L.close()

@@ -255,13 +255,13 @@ def test_perfect_prediction_loss_zero_and_fixed_point():
 
 
 # ---------------------------------------------------------------- library special case (r = 1)
-def _torch_dense(x, y, W, s, mt, m, mask=None):
+def _torch_dense(x, y, W, s, mt, m, mask=None, ignore_index=None):
     """F.normalize + margin + F.cross_entropy + autograd (library routines) on the dense problem."""
     xt = torch.tensor(x, dtype=torch.float64, requires_grad=True)
     Wt = torch.tensor(W, dtype=torch.float64, requires_grad=True)
     cos = torch.nn.functional.normalize(xt, dim=1, eps=1e-12) @ torch.nn.functional.normalize(Wt, dim=1, eps=1e-12).T
     yt = torch.tensor(y)
-    oh = torch.nn.functional.one_hot(yt, W.shape[0]).bool()
+    oh = torch.nn.functional.one_hot(yt.clamp_min(0), W.shape[0]).bool() & (yt[:, None] >= 0)
     if mt == MARGIN_COSFACE:
         tgt = cos - m
     elif mt == MARGIN_ARCFACE:
@@ -272,7 +272,10 @@ def _torch_dense(x, y, W, s, mt, m, mask=None):
     logits = s * torch.where(oh, tgt, cos)
     if mask is not None:
         logits = logits.masked_fill(~torch.tensor(mask)[None, :], float("-inf"))
-    loss = torch.nn.functional.cross_entropy(logits, yt)
+    if ignore_index is None:
+        loss = torch.nn.functional.cross_entropy(logits, yt)
+    else:
+        loss = torch.nn.functional.cross_entropy(logits, yt, ignore_index=ignore_index)
     loss.backward()
     return loss.item(), xt.grad.numpy(), Wt.grad.numpy()
 
@@ -530,3 +533,50 @@ def test_variants_equal_masked_torch_autograd(mode):
     assert out["loss"] == pytest.approx(L.item(), rel=1e-12)
     assert np.allclose(np.concatenate(out["grad_x"]), xt.grad.numpy(), rtol=1e-9, atol=1e-15)
     assert np.allclose(np.concatenate(out["dW"]), Wt.grad.numpy()[S], rtol=1e-9, atol=1e-15)
+
+
+# ---------------------------------------------------------------- ignore_index = -1 (R28)
+@pytest.mark.parametrize("mt,m", [(MARGIN_ARCFACE, 0.5), (MARGIN_COSFACE, 0.4)])
+@pytest.mark.parametrize("k", [1, 2])
+def test_ignore_index_r1_equals_torch_cross_entropy_ignore_index(mt, m, k):
+    """At r = 1 the method is the dense margin softmax: with rows labelled -1 it must equal the library routine
+    F.cross_entropy(..., ignore_index=-1) (mean over the other rows) under autograd — loss, grad x and grad W."""
+    C, d, B = 41, 16, 6
+    W = w_rows_np(4, np.arange(C), d)
+    ys = make_labels(5, 0, k, B, C)
+    xs = [x.astype(np.float64) for x in make_features(5, 0, k, B, d, labels=ys, dist="trained", sigma=0.3, w_seed=4)]
+    ys[0][1] = -1
+    ys[-1][4] = -1
+    cfg = OracleConfig(num_classes=C, dim=d, batch=B, world_size=k, sample_rate=1.0, scale=64.0, margin_type=mt,
+                       margin=m, ignore_index=True)
+    out = oracle.forward_backward(cfg, xs, ys, lambda ids: W[np.asarray(ids)])
+    L, gx, gW = _torch_dense(np.concatenate(xs), np.concatenate(ys), W, 64.0, mt, m, ignore_index=-1)
+    assert out["loss"] == pytest.approx(L, rel=1e-12)
+    assert np.allclose(np.concatenate(out["grad_x"]), gx, rtol=1e-9, atol=1e-15)
+    assert np.allclose(np.concatenate(out["dW"]), gW, rtol=1e-9, atol=1e-15)
+    assert not np.any(np.concatenate(out["grad_x"])[[1, k * B - 2]])
+
+
+def test_ignore_index_equals_dropping_the_rows():
+    """Sampled (r < 1): ignoring rows is the same computation as leaving them out of the batch — same sampled ids
+    (ignored labels are no positives; the negatives' keys depend only on class ids and the step), same loss,
+    same grad_x on the kept rows, zero grad_x on the ignored ones, same class-centre gradients."""
+    C, d, B = 3000, 32, 12
+    ys = make_labels(7, 0, 1, B, C)
+    xs = [x.astype(np.float64) for x in make_features(7, 0, 1, B, d)]
+    drop = [2, 3, 9]
+    keep = [n for n in range(B) if n not in drop]
+    y_ign = ys[0].copy()
+    y_ign[drop] = -1
+    w = lambda ids: w_rows_np(1, ids, d)
+    a = oracle.forward_backward(OracleConfig(num_classes=C, dim=d, batch=B, sample_rate=0.05, seed=3, ignore_index=True),
+                                xs, [y_ign], w, step=2)
+    b = oracle.forward_backward(OracleConfig(num_classes=C, dim=d, batch=len(keep), sample_rate=0.05, seed=3),
+                                [xs[0][keep]], [ys[0][keep]], w, step=2)
+    assert np.array_equal(a["idx"][0], b["idx"][0])
+    assert a["loss"] == pytest.approx(b["loss"], rel=1e-13)
+    assert np.allclose(a["grad_x"][0][keep], b["grad_x"][0], rtol=1e-12, atol=1e-18)
+    assert not np.any(a["grad_x"][0][drop])
+    assert np.allclose(a["dW"][0], b["dW"][0], rtol=1e-12, atol=1e-18)
+    with pytest.raises(ValueError):     # without ignore_index a -1 label is a data error (R7)
+        oracle.forward_backward(OracleConfig(num_classes=C, dim=d, batch=B, sample_rate=0.05), xs, [y_ign], w)
