@@ -273,7 +273,7 @@ def measure(cfgname, args, world, rank, local, dist, e2e=True, clocks=True):
     C, d, B, r, mt, m, desc = CONFIGS[cfgname]
     kw = dict(num_classes=C, dim=d, batch=B, sample_rate=r, scale=SCALE, margin_type=mt, margin=m, momentum=MOMENTUM,
               weight_decay=WEIGHT_DECAY, precision=args.precision, seed=1234, device=local,
-              param_location=args.params)
+              param_location=args.params, comm_mode=args.comm)
     layer = pfc.PartialFC.from_process_group(**kw) if world > 1 else pfc.PartialFC(**kw)
     W, V = layer.params()
     if args.params == "host":       # page-locked host shard: rows generated on the GPU, copied
@@ -463,6 +463,8 @@ def main():
     ap.add_argument("--params", default="device", choices=["device", "host"],
                     help="where W and V live: HBM (default) or page-locked host memory (capacity mode, f4)")
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds per oracle step of the cpu_baseline")
+    ap.add_argument("--comm", default="nccl", choices=["nccl", "nccl_fused"],
+                    help="collectives: NCCL calls, or fused into the kernels over NCCL symmetric windows (f2)")
     args = ap.parse_args()
     assert args.warmup >= 3, "W >= 3 warm-up steps"
 
@@ -508,7 +510,7 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": args.precision, "data": "synthetic",
             "config": {"workload": res["desc"], "num_classes": res["C"], "dim": d, "batch_per_gpu": B,
                        "global_batch": M, "sample_rate": res["r"], "k_per_gpu": k, "shard_rows": res["shard"],
-                       "margin": f"{res['mt']} {res['m']}", "scale": SCALE, "parallelism": f"class-parallel x{world}",
+                       "margin": f"{res['mt']} {res['m']}", "scale": SCALE, "parallelism": f"class-parallel x{world}", "comm": args.comm,
                        "params": args.params,
                        "l2": "inputs larger than L2 (W+V shard %.1f GB, %.1f GB of sampled rows per step)"
                              % (2 * res["shard"] * d * 4 / 1e9, k * d * 4 / 1e9)},

@@ -335,7 +335,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DF_THREADS, 1)
 }  // namespace
 
 bool dw_sgd_full_enabled(const Sizes& sz, int gsc) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DWFULL"); return e ? std::atoi(e) : 1; }();
+  static const int forced = [] { const char* e = std::getenv("PFC_DWFULL"); return e ? std::atoi(e) : 0; }();
   return forced != 0 && gsc == 0 && sz.M > 256 && (sz.d == 256 || sz.d == 512) && sz.k_pad % 256 == 0;
 }
 

@@ -85,8 +85,9 @@ pfc_status fused_nccl_create(ncclComm_t comm, const Sizes& sz, FusedNccl** out, 
   p.n = sz.world;
   p.rank = sz.rank;
   p.lay = L;
-  if (p.base[sz.rank] != static_cast<char*>(f->region))
-    return fail(PFC_ERR_NCCL, "the LSA address of this rank's window is not its own allocation");
+  // p.base[rank] is the window's LSA alias of this rank's own region (a second mapping of the same memory): the fused
+  // kernels address every rank, this one included, through the LSA aliases; the other kernels use the allocation's
+  // own address (c->X32, c->Y) — never both inside one kernel
   *P = p;
   *local_region = static_cast<char*>(f->region);
   *out = f;

@@ -379,12 +379,14 @@ def test_path_flags():
 @pytest.mark.parametrize("case", TINY_CASES, ids=_case_id)
 @pytest.mark.parametrize("precision", ["fp32", "bf16"])
 def test_tiny_loss_regime(case, precision):
-    """fp32 mode: the north-star bars. bf16 mode (R21): bf16 operand rounding perturbs every logit by
-    ~ s u sqrt(2/d) (u = 2^-9), independent of L, so relative errors do not shrink with L: the loss must be
-    within 1e-3 * max(L, 0.05) absolute and the gradients within 4 s u sqrt(2/d) max-relative."""
+    """Features almost on their centres (L ~ 3e-8 .. 8e-3). fp32 mode: the north-star bars. bf16 mode: operand
+    rounding perturbs every logit by ~ s u sqrt(2/d) independently of L, so the relative loss error grows like
+    1/L; with fp16 logits operands (R27) the north-star bars hold down to L ~ 8e-3 (measured 1.5e-4 / 9.3e-5), and
+    only the L < 1e-6 steps (measured 3.3e-4 / 8.4e-4) are held to R21's derived 4 sigma_z instead."""
     d = case[1]
     for (L, Lr, gx, gxr, dW, dWr, Wn, Wnr, Vn, Vnr) in _run_single(case, precision):
-        check(precision, L, Lr, gx, gxr, dW, dWr, tiny_d=d)
+        # R21's derived bound only where L < 1e-6 (six orders below 0.05); at L ~ 8e-3 the north-star bars hold
+        check(precision, L, Lr, gx, gxr, dW, dWr, tiny_d=d if Lr < 1e-6 else None)
 
 
 @pytest.mark.parametrize("world", [2, 4])
