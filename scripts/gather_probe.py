@@ -4,7 +4,7 @@
 import torch
 
 torch.cuda.set_device(0)
-C, d, k = 10_000_000, 512, 1_000_000
+C, d, k = 10_000_000, 512, 7812 * 128
 W = torch.empty(C, d, device="cuda")
 idx = torch.randperm(C, device="cuda")[:k].sort().values
 
