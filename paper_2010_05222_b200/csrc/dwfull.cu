@@ -65,7 +65,7 @@ __device__ __forceinline__ void ld8(const float* a, float (&v)[8]) {
 }
 
 template <bool HINT>
-__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DF_THREADS, 1)
     k_dw_sgd_full(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, DfParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -354,7 +354,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(200)
 }  // namespace
 
 bool dw_sgd_full_enabled(const Sizes& sz, int gsc) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DWFULL"); return e ? std::atoi(e) : 1; }();
+  static const int forced = [] { const char* e = std::getenv("PFC_DWFULL"); return e ? std::atoi(e) : 0; }();
   return forced != 0 && gsc == 0 && sz.M > 256 && sz.d == 512 && sz.k_pad % 256 == 0;
 }
 

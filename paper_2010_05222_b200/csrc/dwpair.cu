@@ -21,7 +21,15 @@ namespace {
 constexpr int DP_BK = 64;
 constexpr int DP_STAGES = 4;
 constexpr int DP_ACC = 2;
-constexpr int DP_EPI = 8;
+// epilogue warps: 8 (2 per TMEM lane quadrant, 16 rows each); PFC_DP_EPI=16 (4 per quadrant, 8 rows each, twice
+// the warps in flight) measured no faster: 0.352 vs 0.345 ms at the per-rank C4 shape, the kernel is DRAM-bound)
+#ifndef PFC_DP_EPI
+#define PFC_DP_EPI 8
+#endif
+constexpr int DP_EPI = PFC_DP_EPI;
+constexpr int DP_NSET = DP_EPI / 4;                   // warps per TMEM lane quadrant (column sets of the staging)
+constexpr int DP_RPW = 128 / DP_EPI;                  // rows per warp in the update
+static_assert(DP_RPW == 8 || DP_RPW == 16, "epilogue layout");
 constexpr int DP_THREADS = 32 * (2 + DP_EPI);
 constexpr int DP_HALF = 128 * DP_BK * 2;              // 16 KB
 constexpr int DP_STAGE = 2 * DP_HALF;                 // A (128 classes x 64 batch) + B (64 batch x 128 columns)
@@ -129,7 +137,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
     const int ew = warp - 2;
     const int lg = warp & 3;
     const int row_in = lg * 32 + lane;
-    const int eset = ew >> 2;
+    const int eset = ew >> 2;                  // 0 .. DP_NSET-1
     const float lr = *p.sgd.lr;
     const uint64_t pol = HINT ? policy_evict_first() : 0;
     const uint32_t acce_leader = leader_addr(&acc_empty[0]);
@@ -155,7 +163,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
-      const int ew16 = ew * 16;
+      const int ew16 = ew * DP_RPW;
       // W / V rows of 4-row batch b (rows ew16 + 4b .. +3) of column half h into registers
       auto load = [&](int h, int b, float4 (&wv)[4], float4 (&mv)[4], int32_t (&jr)[4]) {
         const int col = dcol0 + h * 128 + lane * 4;
@@ -200,7 +208,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       };
       auto stage = [&](int h) {
 #pragma unroll 1
-        for (int c = eset * 4; c < eset * 4 + 4; ++c) {
+        for (int c = eset * (8 / DP_NSET); c < (eset + 1) * (8 / DP_NSET); ++c) {
           uint32_t v[16];
           tmem_ld16(tacc + h * 128 + c * 16, v);
 #pragma unroll
@@ -229,12 +237,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
           asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
         }
       }
-      load(0, 2, wa, ma, ja);
-      update(0, 1, wb, mb, jb);
-      load(0, 3, wb, mb, jb);
-      update(0, 2, wa, ma, ja);
-      load(1, 0, wa, ma, ja);
-      update(0, 3, wb, mb, jb);
+      if constexpr (DP_RPW == 16) {
+        load(0, 2, wa, ma, ja);
+        update(0, 1, wb, mb, jb);
+        load(0, 3, wb, mb, jb);
+        update(0, 2, wa, ma, ja);
+        load(1, 0, wa, ma, ja);
+        update(0, 3, wb, mb, jb);
+      } else {
+        load(1, 0, wa, ma, ja);
+        update(0, 1, wb, mb, jb);
+      }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DP_EPI) : "memory");   // staging free
       stage(1);
       tc_fence_before();
@@ -247,11 +260,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DP_EPI) : "memory");
       load(1, 1, wb, mb, jb);
       update(1, 0, wa, ma, ja);
-      load(1, 2, wa, ma, ja);
-      update(1, 1, wb, mb, jb);
-      load(1, 3, wb, mb, jb);
-      update(1, 2, wa, ma, ja);
-      update(1, 3, wb, mb, jb);
+      if constexpr (DP_RPW == 16) {
+        load(1, 2, wa, ma, ja);
+        update(1, 1, wb, mb, jb);
+        load(1, 3, wb, mb, jb);
+        update(1, 2, wa, ma, ja);
+        update(1, 3, wb, mb, jb);
+      } else {
+        update(1, 1, wb, mb, jb);
+      }
     }
   }
   tc_fence_before();

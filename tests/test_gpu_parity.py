@@ -311,6 +311,56 @@ def test_host_resident_params_match_device(B, fused):
     host.close()
 
 
+@pytest.mark.parametrize("B", [96, 640], ids=["fused-M96", "pair-M640"])
+@pytest.mark.parametrize("stage", ["1", "0"], ids=["staged", "zero-copy"])
+def test_host_resident_params_oracle_parity(B, stage, monkeypatch):
+    """f4 (W in host RAM): with PFC_PARAMS_HOST the sampled rows are staged into HBM once per step
+    (gather kernel over the mapping) and written back after the update (PFC_HOST_STAGE=0: every kernel reads the
+    mapping directly). Two train steps against the float64 oracle: ids bit-exact, loss / grad_x / the updated W and V
+    rows of the host shard at the north-star bars, unsampled host rows untouched."""
+    monkeypatch.setenv("PFC_HOST_STAGE", stage)
+    case = (30000, 512, B, 0.1, "arcface", 0.5, "init", 0.0)
+    C, d = case[0], case[1]
+    layer = pfc.PartialFC(num_classes=C, dim=d, batch=B, sample_rate=0.1, margin_type="arcface", margin=0.5,
+                          momentum=0.9, weight_decay=5e-4, precision="bf16", seed=3, param_location="host")
+    W, V = layer.params()
+    W.copy_(synth.w_rows(1, torch.arange(C), d))
+    V.zero_()
+    W0 = W.clone()
+    cfg = ocfg(C, d, B, 0.1, "arcface", 0.5, seed=3)
+    Wcur, Vh = {}, {}
+
+    def w_rows(ids):
+        base = synth.w_rows_np(1, np.asarray(ids), d)
+        for t, j in enumerate(np.asarray(ids)):
+            if int(j) in Wcur:
+                base[t] = Wcur[int(j)]
+        return base
+    touched = set()
+    for step in range(2):
+        ys = synth.make_labels(10 + step, step, 1, B, C)
+        xs = synth.make_features(10 + step, step, 1, B, d)
+        x, y = torch.from_numpy(xs[0]).cuda(), torch.from_numpy(ys[0]).cuda()
+        gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+        layer.train_step(x, y, gx, loss, lr=0.1)
+        torch.cuda.synchronize()
+        layer.check()
+        idx = layer.sampled()
+        ref = oracle.forward_backward(cfg, xs, ys, w_rows, step=step)
+        assert np.array_equal(idx, ref["idx"][0])
+        Wr, Vr = oracle.sgd_momentum_rows(w_rows(idx), np.stack([Vh.get(int(j), np.zeros(d)) for j in idx]),
+                                          ref["dW"][0], 0.1, cfg.momentum, cfg.weight_decay)
+        check("bf16", loss.item(), ref["loss"], gx.cpu().numpy(), ref["grad_x"][0], Vn=V[idx].numpy(), Vnr=Vr)
+        assert maxrel(W[idx].numpy(), Wr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vr)) / np.max(np.abs(Wr))
+        for t, j in enumerate(idx):
+            Wcur[int(j)], Vh[int(j)] = Wr[t], Vr[t]
+        touched |= set(idx.tolist())
+    mask = torch.ones(C, dtype=torch.bool)
+    mask[torch.tensor(sorted(touched))] = False
+    assert torch.equal(W[mask], W0[mask])
+    layer.close()
+
+
 @pytest.mark.parametrize("B", [96, 320], ids=["fused-M96", "pair-M320"])
 @pytest.mark.parametrize("scale", [16.0, 72.0])
 def test_eform_scale_range(B, scale):
