@@ -39,6 +39,7 @@ static_assert(DP_SMEM <= 232448, "shared memory overflow");
 
 struct DpParams {
   int M, d;
+  int tile_major;
   const SamplerState* st;
   SgdArgs sgd;
 };
@@ -67,6 +68,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
   const int n_units = nct * ndq, n_kb = (p.M + DP_BK - 1) / DP_BK;
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   auto dtile = [&](int u) { return (u % ndq) * 256; };
+  // unit order: unit u = pair + i * npairs (the two column halves of a tile go to neighbouring pairs at the same
+  // time); PFC_DW_ORDER=1: pair p takes the class tiles p, p + npairs, ... and, for each, its column halves back to
+  // back (the tile's E' block re-read right after the first half) — measured slower (0.40 vs 0.346 ms, c4rank)
+  const bool tile_major = p.tile_major;
+  const int u_first = tile_major ? pair * ndq : pair;
+  auto u_next = [&](int u) {
+    if (!tile_major) return u + npairs;
+    return (u % ndq + 1 < ndq) ? u + 1 : (u / ndq + npairs) * ndq;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < DP_STAGES; ++i) { mbar_init(&full[i], 1); mbar_init(&empty[i], 1); }
@@ -90,7 +100,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
-      for (int u = pair; u < n_units; u += npairs) {
+      for (int u = u_first; u < n_units; u = u_next(u)) {
         const int c0 = (u / ndq) * 256 + 128 * pr, d0 = dtile(u) + 128 * pr;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
@@ -109,7 +119,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       constexpr uint32_t IDESC = make_idesc(256, 256, false, true);
       int stage = 0, acc = 0;
       uint32_t phase = 0, acc_phase = 0;
-      for (int u = pair; u < n_units; u += npairs) {
+      for (int u = u_first; u < n_units; u = u_next(u)) {
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
         tc_fence_after();
         const uint32_t tacc = tmem_base + acc * 256;
@@ -148,16 +158,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
       if (u < n_units && prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = p.sgd.dotw[prow]; }
     };
-    if (eset == 0) scalars(pair);
+    if (eset == 0) scalars(u_first);
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = pair; u < n_units; u += npairs) {
+    for (int u = u_first; u < n_units; u = u_next(u)) {
       const int dcol0 = dtile(u);
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DP_EPI) : "memory");   // previous tile consumed
       int32_t pf_j = -1;
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
-        scalars(u + npairs);
+        scalars(u_next(u));
         pf_j = nx_j;
       }
       mbar_wait(&acc_full[acc], acc_phase);
@@ -228,7 +238,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
       load(0, 1, wb, mb, jb);
       update(0, 0, wa, ma, ja);
       if (pf_j >= 0) {   // the next tile's W / V row segments (256 columns) into L2
-        const int ndc = dtile(u + npairs);
+        const int ndc = dtile(u_next(u));
         const float* wp = p.sgd.W + (int64_t)pf_j * p.d + ndc;
         const float* vp = p.sgd.V + (int64_t)pf_j * p.d + ndc;
 #pragma unroll
@@ -301,8 +311,10 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
   const CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);    // G class-major: 128 classes x 64 batch
   const CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);        // X_hat: 64 batch rows x 64 columns
   TC_MAPS_OK();
+  // tile-major order measured slower at the per-rank C4 shape (0.40 vs 0.346 ms): the interleaved order is the default
+  static const int order = [] { const char* e = std::getenv("PFC_DW_ORDER"); return e ? std::atoi(e) : 0; }();
   DpParams p{};
-  p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa;
+  p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa; p.tile_major = order;
   const int64_t units = (sz.k_pad / 256) * (sz.d / 256);
   const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, num_sms() / 2));   // 74 co-resident
   kern<<<2 * pairs, DP_THREADS, DP_SMEM, s>>>(a, b, p);
