@@ -426,6 +426,25 @@ def test_sgd_reduces_to_vanilla_and_two_step_unroll():
     assert np.array_equal(w0, W)                                           # zero-gradient fixed point
 
 
+def test_sgd_matches_torch_optim_sgd():
+    """R15 against the library routine: torch.optim.SGD(momentum=mu, weight_decay=lam, dampening=0, nesterov=False)
+    over three steps with fresh gradients (its first step sets the buffer to g + lam w, as the oracle's v = 0
+    start does)."""
+    rng = np.random.default_rng(3)
+    W = rng.standard_normal((5, 7))
+    grads = [rng.standard_normal((5, 7)) for _ in range(3)]
+    mu, lam, lr = 0.9, 5e-4, 0.07
+    p = torch.nn.Parameter(torch.tensor(W, dtype=torch.float64))
+    opt = torch.optim.SGD([p], lr=lr, momentum=mu, weight_decay=lam)
+    w, v = W.copy(), np.zeros_like(W)
+    for g in grads:
+        p.grad = torch.tensor(g, dtype=torch.float64)
+        opt.step()
+        w, v = oracle.sgd_momentum_rows(w, v, g, lr, mu, lam)
+        assert np.allclose(w, p.detach().numpy(), rtol=1e-14, atol=1e-15)
+        assert np.allclose(v, opt.state[p]["momentum_buffer"].numpy(), rtol=1e-14, atol=1e-15)
+
+
 def test_label_out_of_range_is_rejected():
     cfg = OracleConfig(num_classes=10, dim=4, batch=1)
     with pytest.raises(ValueError):
