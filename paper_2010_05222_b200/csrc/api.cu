@@ -113,6 +113,7 @@ struct pfc_ctx {
   __nv_bfloat16* Xt = nullptr;       // M_pad x d: bf16(f_n x_hat_n)
   float* dcorr = nullptr;            // k_pad: sum of G_t c_t over each class's target entries
   float* xch = nullptr;              // k_pad x (d/128): radial-dot partials
+  float* xws = nullptr;              // dwxdot.cu: half-dots + flags of the partner pairs (M >= 2048, d = 512)
   int* cnt = nullptr;                // k_pad/128
   int* err_dev = nullptr;
   int* err_host = nullptr;           // page-locked mirror of err_dev written by the step's last kernel
@@ -466,6 +467,8 @@ pfc_status pfc_init(const pfc_config* cfg, pfc_ctx** out) {
     ALLOC(c->Xt, Mp * d * 2);
     ALLOC(c->dcorr, kp * 4);
   }
+  if (c->eform_pair && dw_sgd_pairx_enabled(sz, 0) && !dw_sgd_full_enabled(sz, 0))
+    ALLOC(c->xws, (size_t)dw_sgd_pairx_ws_floats(sz) * 4);
   if (c->eform) {
     ALLOC(c->xch, kp * (size_t)(d / 128) * 4);
     ALLOC(c->cnt, (kp / 128) * 4);
@@ -672,7 +675,7 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
     // E-form at M > 256: f, X~, the target entries and the radial dots, then dX_hat = f (E' W_s)
     n += launch_eform_prep(sz, c->X32, c->lse, c->gt, c->tcol, c->ct, c->mp, c->ef_f, c->Xt,
                            (__nv_bfloat16*)c->cosv, c->dcorr, c->metrics + 2, s);
-    if (!dw_sgd_full_enabled(sz, 0))   // else the dW + SGD kernel forms the radial dots from its accumulator
+    if (!dw_sgd_full_enabled(sz, 0) && !c->xws)   // else the dW + SGD kernel forms the radial dots itself
       n += launch_eform_dotw(sz, (const __nv_bfloat16*)c->cosv, c->ef_f, c->dcorr, c->st, c->mp, c->dotw, s);
     mark(c, 6, s);
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->cosv, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
@@ -706,6 +709,7 @@ void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
   } else if (c->use_tc && fused) {
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
               c->fused_gather ? 1 : 0};
+    if (c->eform_pair) { a.xws = c->xws; a.err = c->err_dev; }   // E-form pair path: radial dots in the dW kernel
     if (c->eform_pair)   // dW_hat = E'^T X~ (E-form): same contraction, other operands
       n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, s);
     else

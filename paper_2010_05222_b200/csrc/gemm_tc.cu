@@ -652,6 +652,8 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& sa, cudaStream_t s) {
   if (dw_sgd_full_enabled(sz, sa.gsc)) return launch_dw_sgd_full_tc(sz, G, Xb, st, sa, s);   // dwfull.cu
+  if (sa.xws && dw_sgd_pairx_enabled(sz, sa.gsc))                                              // dwxdot.cu
+    return launch_dw_sgd_pairx_tc(sz, G, Xb, st, sa, sa.xws, sa.err, s);
   if (dw_sgd_pair_enabled(sz)) return launch_dw_sgd_pair_tc(sz, G, Xb, st, sa, s);   // dwpair.cu (CTA pairs)
   CUtensorMap a = make_map(G, sz.k_pad, sz.M_pad, 64, 128);     // Gc class-major, K-major A (= Gc^T)
   CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);

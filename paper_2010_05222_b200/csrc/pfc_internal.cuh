@@ -226,6 +226,8 @@ int launch_dw_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* X
 struct SgdArgs {
   float* W; float* V; const int32_t* idx; const float* inv_norm; const float* dotw; const float* lr; float mu, lambda;
   int gsc;   // R25: G carries 1/||w|| (dW_hat tile is already scaled)
+  float* xws = nullptr;   // dwxdot.cu: the partner pairs' half-dots and flags (dw_sgd_pairx_ws_floats)
+  int* err = nullptr;
 };
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& a, cudaStream_t s);
@@ -238,6 +240,12 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
 bool dw_sgd_full_enabled(const Sizes& sz, int gsc);
 int launch_dw_sgd_full_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                           const SgdArgs& sa, cudaStream_t s);
+// dwxdot.cu — K11 + radial dot + K12 on CTA pairs, the dot's two column halves exchanged between partner pairs
+// (M >= 2048, d = 512, normalised W_s; PFC_DW_XDOT=0 disables): no radial-dot pass over E
+bool dw_sgd_pairx_enabled(const Sizes& sz, int gsc);
+int64_t dw_sgd_pairx_ws_floats(const Sizes& sz);
+int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
+                           const SgdArgs& sa, float* ws, int* err, cudaStream_t s);
 // dwx.cu — K9 + K11 + K12 fused for the train step (M <= 256, R25 scaling): dW + SGD update + dX_hat partials
 bool dwx_supported(const Sizes& sz);
 int64_t dwx_ws_floats(const Sizes& sz);

@@ -14,7 +14,10 @@ for r in rows[hi + 1:]:
 mult = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1e-3, 'us': 1, 'ms': 1e3}
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 for (i, name), m in data.items():
-    short = re.search(r'(k_[a-z0-9_]+(<[^>]*>)?)', name).group(1)
+    mt = re.search(r'pfc::.*?(k_[a-z0-9_]+(<[^>]*>)?)', name)
+    if not mt:            # torch's own kernels (the synthetic W fill before the timed steps)
+        continue
+    short = mt.group(1)
     a = agg[short]; a[0] += 1
     t = m['gpu__time_duration.sum']; a[1] += t[0] * mult[t[1]]
     for mm, idx in (('dram__bytes_read.sum', 2), ('dram__bytes_write.sum', 3)):
@@ -29,9 +32,10 @@ sec = {'k_tc_gemm<5>': 'dw_gemm_sgd', 'k_tc_gemm<6>': 'dw_gemm_sgd', 'k_tc_gemm<
        'k_logits_gather<1>': 'gather_logits', 'k_logits_gather<0>': 'gather_logits',
        'k_logits_pair<1>': 'logits_gemm', 'k_logits_pair<0>': 'logits_gemm', 'k_eform_dotw': 'eform_dotw',
        'k_logits_pair<1, 1>': 'logits_gemm', 'k_logits_pair<0, 1>': 'logits_gemm', 'k_logits_pair<1, 0>': 'logits_gemm',
-       'k_logits_pair<0, 0>': 'logits_gemm'}
+       'k_logits_pair<0, 0>': 'logits_gemm', 'k_dw_sgd_pairx<1>': 'dw_gemm_sgd', 'k_dw_sgd_pairx<0>': 'dw_gemm_sgd',
+       'k_dw_sgd_full<1>': 'dw_gemm_sgd', 'k_dw_sgd_full<0>': 'dw_gemm_sgd'}
 lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU): cold-cache, serialised launches",
-         "# k_logits_gather = K5+K6 (gather, norms, bf16, logits), k_dwx_t = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
+         "# k_logits_gather = K5+K6 (gather, norms, fp16 operand, logits), k_dwx_t = K9+K11+K12 (dW, momentum SGD, dX) at M <= 256;",
          "# k_tc_gemm<0> = logits (K6), <1> = dx split-K (K9), <5>/<6> = dW + fused momentum SGD (K11+K12) otherwise",
          "kernel, launches, avg_us, share_of_step, dram_read_MB_per_launch, dram_write_MB_per_launch"]
 traffic = {}
