@@ -16,8 +16,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 OUT_DIR = os.path.join(HERE, "_lib")
-OBJ_DIR = os.path.join(ROOT, "build", "obj")
-LIB = os.path.join(OUT_DIR, "libpfc.so")
+# PFC_BUILD_TAG=<tag>: a variant build (own objects, _lib/libpfc-<tag>.so); "checks" adds -DPFC_DEBUG_CHECKS (the
+# device-side bounds asserts of pfc_internal.cuh). Select it at run time with PFC_LIB.
+TAG = os.environ.get("PFC_BUILD_TAG", "")
+OBJ_DIR = os.path.join(ROOT, "build", "obj" + (f"-{TAG}" if TAG else ""))
+LIB = os.path.join(OUT_DIR, f"libpfc-{TAG}.so" if TAG else "libpfc.so")
+TAG_FLAGS = {"checks": ["-DPFC_DEBUG_CHECKS"]}.get(TAG, [])
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -35,7 +39,7 @@ def _compile(src, inc, verbose):
         return obj
     cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-c", src, "-o", obj,
            "-I", inc, "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr", "-Xptxas", "-v" if verbose else "-O3"]
-    cmd += os.environ.get("PFC_NVCC_EXTRA", "").split()   # variant builds (A/B timing); empty by default
+    cmd += TAG_FLAGS + os.environ.get("PFC_NVCC_EXTRA", "").split()   # variant builds (A/B timing); empty by default
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")

@@ -666,6 +666,7 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
                            (__nv_bfloat16*)c->cosv, c->dcorr, c->metrics + 2, s);
     mark(c, 6, s);
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 0};
+    a.rows = c->stage ? sz.k_pad : sz.C_local;
     EformArgs ef{c->ef_f, c->tcol, c->dcorr, c->xch, c->cnt, c->err_dev, c->mp.s};
     n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, c->split_ws, c->dXh, &ef, c->P(), s);
     c->launches += n;
@@ -689,6 +690,7 @@ void phase_d(pfc_ctx* c, const float* gmax, float* loss_out, bool fused, cudaStr
   mark(c, 6, s);
   if (fused && c->use_dwx) {
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay, 1};
+    a.rows = c->stage ? sz.k_pad : sz.C_local;
     n += launch_dwx_tc(sz, (const __nv_bfloat16*)c->G, c->Xb, c->st, a, c->split_ws, c->dXh, nullptr, c->P(), s);
   } else if (c->use_tc)
     n += launch_dx_tc(sz, (const __nv_bfloat16*)c->G, (const __nv_bfloat16*)c->Ws, c->st, c->dXh, c->split_ws,
@@ -710,6 +712,7 @@ void phase_e_dw(pfc_ctx* c, bool fused, cudaStream_t s) {
     SgdArgs a{c->Wk(), c->Vk(), c->idxk(), c->inv_norm, c->dotw, c->lr_dev, c->cfg.momentum, c->cfg.weight_decay,
               c->fused_gather ? 1 : 0};
     if (c->eform_pair) { a.xws = c->xws; a.err = c->err_dev; }   // E-form pair path: radial dots in the dW kernel
+    a.rows = c->stage ? sz.k_pad : sz.C_local;
     if (c->eform_pair)   // dW_hat = E'^T X~ (E-form): same contraction, other operands
       n += launch_dw_sgd_tc(sz, (const __nv_bfloat16*)c->cosv, c->Xt, c->st, a, s);
     else

@@ -180,6 +180,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           jr[r] = s_rowj[ew16 + 4 * b + r];
+          PFC_DCHECK(jr[r] < p.sgd.rows);
           if (jr[r] >= 0) {
             if (HINT) {
               wv[r] = ld_hint4(p.sgd.W + (int64_t)jr[r] * p.d + col, pol);

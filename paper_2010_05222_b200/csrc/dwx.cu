@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
 #pragma unroll
         for (int r = 0; r < 8; ++r) {
           jr[r] = s_rowj[ew * 16 + r0 + r];
+          PFC_DCHECK(jr[r] < p.sgd.rows);
           if (jr[r] >= 0) {
             if (HINT) {
               wv[r] = ld_hint4(p.sgd.W + (int64_t)jr[r] * p.d + col, pol);

@@ -41,6 +41,7 @@ struct XpParams {
   float* xdot;      // [n_units][128 * 2] this unit's half-dots, by CTA rank and row
   int* flag;        // [n_units][2] published (zeroed before the launch)
   int* err;
+  int ehint;
 };
 
 // staging index of float4 q (0..63) of row r (XOR swizzle inside each 32-float4 half)
@@ -91,13 +92,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
+      // PFC_DW_EHINT=1: E' loads with an L2 evict-last policy (read by the two partner pairs of a tile at the same
+      // time) — measured no better (c4rank 1.015 vs 1.008 ms), off by default
+      const uint64_t epol = policy_evict_last();
       for (int u = pair; u < n_units; u += npairs) {
         const int c0 = (u >> 1) * 256 + 128 * pr, d0 = (u & 1) * 256 + 128 * pr;
         for (int kb = 0; kb < n_kb; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * XP_HALF));
           uint8_t* sa = smem + stage * XP_STAGE;
-          tma_load_2d_pair(sa, &tmA, &full[stage], kb * XP_BK, c0);                       // E' rows: its classes
+          if (p.ehint) tma_load_2d_pair_hint(sa, &tmA, &full[stage], kb * XP_BK, c0, epol);  // E' rows: its classes
+          else tma_load_2d_pair(sa, &tmA, &full[stage], kb * XP_BK, c0);
           tma_load_2d_pair(sa + XP_HALF, &tmB, &full[stage], d0, kb * XP_BK);             // X~: its columns
           tma_load_2d_pair(sa + XP_HALF + XP_HALF / 2, &tmB, &full[stage], d0 + 64, kb * XP_BK);
           if (++stage == XP_STAGES) { stage = 0; phase ^= 1; }
@@ -218,6 +223,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       if (ew == 0 && lane == 0) {
         __threadfence();
         asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flag + (u * 2 + pr)), "r"(1) : "memory");
+        PFC_DCHECK((u ^ 1) < n_units);
         const int* f = p.flag + ((u ^ 1) * 2 + pr);
         int v = 0, spins = 0;
         do {
@@ -253,6 +259,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
           for (int r = 0; r < 4; ++r) {
             const int rr = ew * 16 + 4 * b + r;
             jr[slot][r] = s_rowj[rr];
+            PFC_DCHECK(jr[slot][r] < p.sgd.rows);
             if (jr[slot][r] >= 0) {
               wv[slot][r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[slot][r] * d + col);
               mv[slot][r] = HINT ? ld_hint4(p.sgd.V + (int64_t)jr[slot][r] * d + col, pol)
@@ -326,6 +333,8 @@ int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_b
   XpParams p{};
   p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa; p.err = err;
   p.xdot = ws;
+  static const int ehint = [] { const char* e = std::getenv("PFC_DW_EHINT"); return e ? std::atoi(e) : 0; }();
+  p.ehint = ehint;
   p.flag = reinterpret_cast<int*>(ws + units * 256);
   cudaMemsetAsync(p.flag, 0, (size_t)units * 2 * sizeof(int), s);
   // every pair of the grid is co-resident (one CTA per SM, units in lock-step): the partner waits cannot deadlock.

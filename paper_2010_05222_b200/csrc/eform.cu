@@ -32,6 +32,7 @@ __global__ void k_eform_prep(int M, int ldm, int d, const float* __restrict__ X3
   if (threadIdx.x == 0) {
     f[n] = fn;
     const int j = tcol[n];
+    PFC_DCHECK(n < ldm);
     if (j >= 0) {
       const float c_t = ct[n];
       const float g_t = gs * gt[n] * margin_dphi(mp, c_t);

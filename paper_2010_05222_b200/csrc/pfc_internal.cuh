@@ -12,6 +12,16 @@
 
 namespace pfc {
 
+// Device-side bounds checks of the row / slot indices the kernels address (compute-sanitizer is closed on the GPU
+// pool): compiled in with -DPFC_DEBUG_CHECKS (PFC_BUILD_TAG=checks python -m paper_2010_05222_b200.build builds
+// _lib/libpfc-checks.so; PFC_LIB selects it), where a violated check is a device assert (cudaErrorAssert, loud).
+#ifdef PFC_DEBUG_CHECKS
+#include <cassert>
+#define PFC_DCHECK(cond) assert(cond)
+#else
+#define PFC_DCHECK(cond) ((void)0)
+#endif
+
 // Sticky device error bits (reported as pfc_status by the next synchronising call).
 enum : int { ERR_DATA = 1, ERR_DEGENERATE = 2, ERR_NUMERIC = 4, ERR_INTERNAL = 8 };
 
@@ -228,6 +238,7 @@ struct SgdArgs {
   int gsc;   // R25: G carries 1/||w|| (dW_hat tile is already scaled)
   float* xws = nullptr;   // dwxdot.cu: the partner pairs' half-dots and flags (dw_sgd_pairx_ws_floats)
   int* err = nullptr;
+  int64_t rows = INT64_MAX;   // shard rows addressable through idx (PFC_DCHECK bounds)
 };
 int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                      const SgdArgs& a, cudaStream_t s);
@@ -266,6 +277,7 @@ __device__ __forceinline__ float* dx_dst(const Peers& P, float* local, int64_t i
   if (P.n == 0) return local + i;
   const int64_t row = i / d, col = i % d;
   const int q = (int)(row / B);
+  PFC_DCHECK(q < P.n && P.lay.xdx + ((int64_t)P.rank * B + (row % B) + 1) * d * 4 <= P.lay.bytes);
   return P.f32(q, P.lay.xdx) + ((int64_t)P.rank * B + (row % B)) * d + col;
 }
 // eform.cu — E-form preparation (f_n, X~, target entries of E) and the radial dots for the unfused-dX path

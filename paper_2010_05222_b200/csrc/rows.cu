@@ -524,6 +524,7 @@ __global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, co
 
 __global__ void k_push_dx(int64_t n, int d, int B, const float* __restrict__ dXh, Peers P) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  PFC_DCHECK(i >= n || (int)(i / d / B) < P.n);
   if (i < n) *dx_dst(P, nullptr, i, d, B) = dXh[i];
 }
 
@@ -718,6 +719,7 @@ __global__ void k_stage_rows(int64_t k_pad, int d, float* __restrict__ W, float*
   const int lane = threadIdx.x & 31;
   if (p >= st->k) return;
   const int64_t j = idx[p];
+  PFC_DCHECK(j >= 0 && p < k_pad);
   for (int c = lane * 4; c < d; c += 128) {
     if (TO_HOST) {
       *reinterpret_cast<float4*>(W + j * d + c) = *reinterpret_cast<const float4*>(Wst + p * d + c);
