@@ -7,13 +7,25 @@
 //   K4  compaction : idx_i = ascending ids of (positive or selected) via tile counts + scan + write (R4);
 //       tcol[n] = position of y_n in idx_i (binary search) or -1 when y_n is not in this shard.
 // Everything is device-resident (k_i is data-dependent); no host synchronisation.
+#include <cooperative_groups.h>
 #include <algorithm>
+#include <cstdlib>
 #include "pfc_internal.cuh"
 
 namespace pfc {
 namespace {
 
 constexpr int kThreads = 256;
+
+int num_sms_host() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
 
 __global__ void k_mark_positives(const int64_t* __restrict__ Y, int M, int64_t a, int64_t C_local,
                                  uint32_t* __restrict__ bits, SamplerState* st, int mode) {
@@ -331,11 +343,226 @@ __global__ void __launch_bounds__(kThreads) k_tile_write(int64_t C_local, const 
   }
 }
 
+// All of K2-K4 in ONE cooperative kernel (the default; PFC_SAMPLER_FUSED=0: the seven kernels above): the same
+// phases and arithmetic — so the same bit-exact selection — separated by grid-wide barriers instead of kernel
+// boundaries; the 40 MB key array stays L2-resident between the phases, and the launch gaps and tails of seven
+// kernels (plus three memsets) become six grid barriers. Each phase walks the classes (or 8192-class tiles) with a
+// grid stride; per-block selection from the histograms is computed redundantly by every block, as before.
+__global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __restrict__ Y, int M, int64_t a,
+                                                            int64_t C_local, uint64_t seed,
+                                                            const uint64_t* __restrict__ step_dev, int64_t budget,
+                                                            double rate, int mode, uint32_t* __restrict__ bits,
+                                                            uint32_t* __restrict__ keys, int* __restrict__ hist,
+                                                            int* __restrict__ tile_cnt, int ntiles, SamplerState* st,
+                                                            int32_t* __restrict__ idx, int* err) {
+  namespace cg = cooperative_groups;
+  cg::grid_group grid = cg::this_grid();
+  __shared__ int sh[2048];
+  __shared__ int wsum[kThreads / 32];
+  __shared__ int sdef, stie;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
+  const int64_t nwords = (C_local + 31) / 32;
+  // phase 0: zero the bitmap, the histograms and the state
+  for (int64_t i = gtid; i < nwords; i += gthreads) bits[i] = 0u;
+  for (int64_t i = gtid; i < 2048 + 2048 + 1024; i += gthreads) hist[i] = 0;
+  if (gtid < (int64_t)(sizeof(SamplerState) / sizeof(int))) reinterpret_cast<int*>(st)[gtid] = 0;
+  grid.sync();
+  // phase 1 (K2): positives
+  if (mode != PFC_SAMPLE_RANDOM)
+    for (int64_t n = gtid; n < M; n += gthreads) {
+      const int64_t y = Y[n] - a;
+      if (y >= 0 && y < C_local) {
+        const uint32_t mask = 1u << (y & 31);
+        const uint32_t old = atomicOr(&bits[y >> 5], mask);
+        if (!(old & mask)) atomicAdd(&st->npos, 1);
+      }
+    }
+  grid.sync();
+  // phase 2 (K3 pass 1): keys and the top-11-bit histogram of the non-positive classes
+  {
+    const uint32_t step = (uint32_t)*step_dev;
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    int64_t j = gtid;
+    for (; j + gthreads < C_local; j += 2 * gthreads) {
+      const uint32_t h0 = philox_class_key((uint64_t)(a + j), step, seed);
+      const uint32_t h1 = philox_class_key((uint64_t)(a + j + gthreads), step, seed);
+      keys[j] = h0;
+      keys[j + gthreads] = h1;
+      if (!is_pos(bits, j)) atomicAdd(&sh[h0 >> 21], 1);
+      if (!is_pos(bits, j + gthreads)) atomicAdd(&sh[h1 >> 21], 1);
+    }
+    if (j < C_local) {
+      const uint32_t h = philox_class_key((uint64_t)(a + j), step, seed);
+      keys[j] = h;
+      if (!is_pos(bits, j)) atomicAdd(&sh[h >> 21], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+      if (sh[i]) atomicAdd(&hist[i], sh[i]);
+  }
+  grid.sync();
+  // phase 3 (K3 pass 2): k_i, n_i; the first digit; histogram of the second inside its bucket
+  const int npos = st->npos;
+  const int kk = budget_k(npos, budget, C_local, rate, mode);
+  const int n_neg = kk - npos;
+  const bool none = n_neg == 0;
+  int b1 = 0, rem1 = 0;
+  if (!none) {
+    block_select(hist, 2048, n_neg, b1, rem1);
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t j0 = gtid * 4; j0 < C_local; j0 += gthreads * 4) {
+      const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
+      const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+      const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((hh[i] >> 21) == (uint32_t)b1 && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[(hh[i] >> 10) & 0x7FF], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x)
+      if (sh[i]) atomicAdd(&hist[2048 + i], sh[i]);
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    st->k = kk; st->n_neg = n_neg; st->none = none ? 1 : 0; st->prefix1 = (uint32_t)b1; st->rem1 = rem1;
+  }
+  grid.sync();
+  // phase 4 (K3 pass 3): the second digit; histogram of the last 10 bits
+  uint32_t pre = 0;
+  int rem2 = 0;
+  if (!none) {
+    int b2;
+    block_select(hist + 2048, 2048, rem1, b2, rem2);
+    pre = ((uint32_t)b1 << 11) | (uint32_t)b2;
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = 0;
+    __syncthreads();
+    for (int64_t j0 = gtid * 4; j0 < C_local; j0 += gthreads * 4) {
+      const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
+      const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+      const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if ((hh[i] >> 10) == pre && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[hh[i] & 0x3FF], 1);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < 1024; i += blockDim.x)
+      if (sh[i]) atomicAdd(&hist[4096 + i], sh[i]);
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->prefix2 = pre; st->rem2 = rem2; }
+  }
+  grid.sync();
+  // phase 5 (K4a): the threshold key T and t; definite / tied counts per 8192-class tile
+  uint32_t T = 0;
+  int tsel = 0;
+  if (!none) {
+    int b3;
+    block_select(hist + 4096, 1024, rem2, b3, tsel);
+    T = (pre << 10) | (uint32_t)b3;
+    if (blockIdx.x == 0 && threadIdx.x == 0) { st->T = T; st->t = tsel; }
+  }
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    uint32_t dm, tm;
+    flags32((int64_t)tile * kSelTile + 32 * threadIdx.x, C_local, bits, keys, none, T, dm, tm);
+    int ndef = __popc(dm), ntie = __popc(tm);
+    if (threadIdx.x == 0) { sdef = 0; stie = 0; }
+    __syncthreads();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      ndef += __shfl_xor_sync(0xffffffffu, ndef, o);
+      ntie += __shfl_xor_sync(0xffffffffu, ntie, o);
+    }
+    if ((threadIdx.x & 31) == 0) { atomicAdd(&sdef, ndef); atomicAdd(&stie, ntie); }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tile_cnt[tile] = sdef;
+      tile_cnt[ntiles + tile] = stie;
+    }
+    __syncthreads();
+  }
+  grid.sync();
+  // phase 6 (K4b): exclusive scans of the tile counts (block 0)
+  if (blockIdx.x == 0) {
+    int* def = tile_cnt;
+    int* tie = tile_cnt + ntiles;
+    int* tie_off = tile_cnt + 2 * ntiles;
+    int* sel_off = tile_cnt + 3 * ntiles;
+    const int lane = threadIdx.x & 31;
+    for (int pass = 0; pass < 2; ++pass) {
+      int carry = 0;
+      for (int base = 0; base < ntiles; base += kThreads) {
+        const int i = base + threadIdx.x;
+        int v = 0;
+        if (i < ntiles) v = pass == 0 ? tie[i] : def[i] + (none ? 0 : max(0, min(tsel - tie_off[i], tie[i])));
+        int tot;
+        const int ex = block_count_scan(v, wsum, tot);
+        if (i < ntiles) (pass == 0 ? tie_off : sel_off)[i] = carry + ex;
+        carry += tot;
+        __syncthreads();
+      }
+      if (pass == 1 && threadIdx.x == 0) {
+        st->total = carry;
+        if (carry != kk) atomicOr(err, ERR_INTERNAL);
+      }
+      (void)lane;
+      __syncthreads();
+    }
+  }
+  grid.sync();
+  // phase 7 (K4c): order-preserving write of the selected local ids
+  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const int64_t j0 = (int64_t)tile * kSelTile + 32 * threadIdx.x;
+    uint32_t dm, tm;
+    flags32(j0, C_local, bits, keys, none, T, dm, tm);
+    int ttot;
+    int trank = tile_cnt[2 * ntiles + tile] + block_count_scan(__popc(tm), wsum, ttot);
+    uint32_t sel = dm;
+    while (tm) {                                    // ties are taken smallest id first (R3): rank < t
+      const int i = __ffs(tm) - 1;
+      tm &= tm - 1;
+      if (trank < tsel) sel |= 1u << i;
+      ++trank;
+    }
+    int stot;
+    int pos = tile_cnt[3 * ntiles + tile] + block_count_scan(__popc(sel), wsum, stot);
+    while (sel) {
+      const int i = __ffs(sel) - 1;
+      sel &= sel - 1;
+      idx[pos++] = (int32_t)(j0 + i);
+    }
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint64_t* step, uint32_t* bits, uint32_t* keys,
                    int* hist, int* tile_cnt, SamplerState* st, int32_t* idx, int32_t* tcol, int* err,
                    cudaStream_t s) {
+  static const bool fused = [] { const char* e = std::getenv("PFC_SAMPLER_FUSED"); return !e || e[0] != '0'; }();
+  if (fused) {
+    static int per_sm = 0;
+    if (!per_sm) {
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_sampler_fused, kThreads, 0);
+      per_sm = std::max(1, std::min(per_sm, 4));
+    }
+    // all blocks co-resident (cooperative launch: a guarantee, or a loud launch failure)
+    const int grid = (int)std::max<int64_t>(1, std::min<int64_t>((sz.C_local + kThreads - 1) / kThreads,
+                                                                 (int64_t)per_sm * num_sms_host()));
+    cudaLaunchConfig_t lc{};
+    lc.gridDim = dim3(grid);
+    lc.blockDim = dim3(kThreads);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeCooperative;
+    at[0].val.cooperative = 1;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    cudaLaunchKernelEx(&lc, k_sampler_fused, Y, sz.M, sz.a, sz.C_local, seed, step, sz.budget, sz.rate,
+                       sz.sample_mode, bits, keys, hist, tile_cnt, sz.ntiles_sel, st, idx, err);
+    (void)tcol;
+    return 1;
+  }
   const int64_t nwords = (sz.C_local + 31) / 32;
   cudaMemsetAsync(bits, 0, nwords * sizeof(uint32_t), s);
   cudaMemsetAsync(hist, 0, (2048 + 2048 + 1024) * sizeof(int), s);
