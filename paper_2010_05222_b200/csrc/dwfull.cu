@@ -354,14 +354,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DF_THREADS, 1)
 }  // namespace
 
 bool dw_sgd_full_enabled(const Sizes& sz, int gsc) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DWFULL"); return e ? std::atoi(e) : 0; }();
+  const int forced = env_int("PFC_DWFULL", 0);
   return forced != 0 && gsc == 0 && sz.M > 256 && sz.d == 512 && sz.k_pad % 256 == 0;
 }
 
 int launch_dw_sgd_full_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                           const SgdArgs& sa, cudaStream_t s) {
   // W / V stores carry an L2 evict-first policy (PFC_DW_HINT=0 disables); their loads are L2 hits after the prefetch
-  static const bool hint = [] { const char* e = std::getenv("PFC_DW_HINT"); return !e || std::atoi(e) != 0; }();
+  const bool hint = env_int("PFC_DW_HINT", 1) != 0;
   auto kern = hint ? k_dw_sgd_full<true> : k_dw_sgd_full<false>;
   static bool attr = false;
   if (!attr) {

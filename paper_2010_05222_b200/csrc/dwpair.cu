@@ -293,7 +293,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DP_THREADS, 1)
 }  // namespace
 
 bool dw_sgd_pair_enabled(const Sizes& sz) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DW_PAIR"); return e ? std::atoi(e) : 1; }();
+  const int forced = env_int("PFC_DW_PAIR", 1);
   return forced != 0 && sz.M >= 2048 && sz.d % 256 == 0 && sz.k_pad % 256 == 0;   // M = 1024: DWF2 is as fast
 }
 
@@ -301,7 +301,7 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
                           const SgdArgs& sa, cudaStream_t s) {
   // W / V streamed with an L2 evict-first policy (the G tile shared by the pairs of both d-halves stays resident);
   // PFC_DW_HINT=0 disables
-  static const bool hint = [] { const char* e = std::getenv("PFC_DW_HINT"); return !e || std::atoi(e) != 0; }();
+  const bool hint = env_int("PFC_DW_HINT", 1) != 0;
   auto kern = hint ? k_dw_sgd_pair<true> : k_dw_sgd_pair<false>;
   static bool attr = false;
   if (!attr) {
@@ -313,7 +313,7 @@ int launch_dw_sgd_pair_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bf
   const CUtensorMap b = make_map(Xb, sz.M_pad, sz.d, 64, 64);        // X_hat: 64 batch rows x 64 columns
   TC_MAPS_OK();
   // tile-major order measured slower at the per-rank C4 shape (0.40 vs 0.346 ms): the interleaved order is the default
-  static const int order = [] { const char* e = std::getenv("PFC_DW_ORDER"); return e ? std::atoi(e) : 0; }();
+  const int order = env_int("PFC_DW_ORDER", 0);
   DpParams p{};
   p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa; p.tile_major = order;
   const int64_t units = (sz.k_pad / 256) * (sz.d / 256);

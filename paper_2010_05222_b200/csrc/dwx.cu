@@ -452,7 +452,7 @@ int dwx_gper(const Sizes& sz) { return std::max(1, num_sms() / (sz.d / 128)); }
 }  // namespace
 
 bool dwx_supported(const Sizes& sz) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DWX"); return e ? std::atoi(e) : 1; }();
+  const int forced = env_int("PFC_DWX", 1);
   return forced != 0 && sz.M <= 256 && sz.d % 128 == 0;
 }
 
@@ -462,7 +462,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
                   const SgdArgs& sa, float* ws, float* dXh, const EformArgs* ef, const Peers* P, cudaStream_t s) {
   // W / V streamed with an L2 evict-first policy so that the G' tile re-read for dX stays resident (-0.1 to -0.2 GB
   // of DRAM reads per step at C4); PFC_DWX_HINT=0 disables
-  static const bool hint = [] { const char* e = std::getenv("PFC_DWX_HINT"); return !e || std::atoi(e) != 0; }();
+  const bool hint = env_int("PFC_DWX_HINT", 1) != 0;
   auto kern = ef ? (hint ? k_dwx_t<true, true> : k_dwx_t<false, true>)
                  : (hint ? k_dwx_t<true, false> : k_dwx_t<false, false>);
   static bool attr = false;

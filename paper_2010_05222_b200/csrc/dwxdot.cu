@@ -310,7 +310,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
 }  // namespace
 
 bool dw_sgd_pairx_enabled(const Sizes& sz, int gsc) {
-  static const int forced = [] { const char* e = std::getenv("PFC_DW_XDOT"); return e ? std::atoi(e) : 1; }();
+  const int forced = env_int("PFC_DW_XDOT", 1);
   return forced != 0 && gsc == 0 && sz.M >= 2048 && sz.d == 512 && sz.k_pad % 256 == 0;
 }
 
@@ -318,7 +318,7 @@ int64_t dw_sgd_pairx_ws_floats(const Sizes& sz) { return (sz.k_pad / 256) * 2 * 
 
 int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Xb, const SamplerState* st,
                            const SgdArgs& sa, float* ws, int* err, cudaStream_t s) {
-  static const bool hint = [] { const char* e = std::getenv("PFC_DW_HINT"); return !e || std::atoi(e) != 0; }();
+  const bool hint = env_int("PFC_DW_HINT", 1) != 0;
   auto kern = hint ? k_dw_sgd_pairx<true> : k_dw_sgd_pairx<false>;
   static bool attr = false;
   if (!attr) {
@@ -333,7 +333,7 @@ int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_b
   XpParams p{};
   p.M = sz.M; p.d = sz.d; p.st = st; p.sgd = sa; p.err = err;
   p.xdot = ws;
-  static const int ehint = [] { const char* e = std::getenv("PFC_DW_EHINT"); return e ? std::atoi(e) : 0; }();
+  const int ehint = env_int("PFC_DW_EHINT", 0);
   p.ehint = ehint;
   p.flag = reinterpret_cast<int*>(ws + units * 256);
   cudaMemsetAsync(p.flag, 0, (size_t)units * 2 * sizeof(int), s);

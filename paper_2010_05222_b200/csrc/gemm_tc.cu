@@ -662,7 +662,7 @@ int launch_dw_sgd_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat1
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.k_pad = sz.k_pad; p.st = st; p.sgd = sa;
   // 256-class tiles pay off when the contraction is long (K = M >= 1024: operand-bandwidth bound); at small M
   // the update is HBM-bound and holding TMEM across the two halves only serialises it (PFC_DWF=1|2 overrides)
-  static const int forced = [] { const char* e = std::getenv("PFC_DWF"); return e ? std::atoi(e) : 0; }();
+  const int forced = env_int("PFC_DWF", 0);
   const int variant = forced ? forced : (sz.M >= 1024 ? 2 : 1);
   if (variant == 1) {
     const int64_t units = (sz.k_pad / 128) * (sz.d / 128);

@@ -290,7 +290,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
 }  // namespace
 
 bool logits_pair_enabled(const Sizes& sz) {
-  static const int forced = [] { const char* e = std::getenv("PFC_LOGITS_PAIR"); return e ? std::atoi(e) : 1; }();
+  const int forced = env_int("PFC_LOGITS_PAIR", 1);
   return forced != 0 && sz.M > 256 && sz.k_pad % 256 == 0;
 }
 
@@ -314,7 +314,7 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
   p.n_ltiles = sz.n_ltiles;
   const int mt = (int)((sz.M + 255) / 256);
   const int max_pairs = num_sms() / 2;
-  static const bool ares_on = [] { const char* e = std::getenv("PFC_LOGITS_ARES"); return !e || std::atoi(e) != 0; }();
+  const bool ares_on = env_int("PFC_LOGITS_ARES", 1) != 0;
   if (ares_on && sz.d <= 64 * L2R_KB && mt <= max_pairs) {
     const int64_t nt = sz.k_pad / 256;
     const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / mt, nt));

@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
 }  // namespace
 
 bool logits_gather_supported(const Sizes& sz) {
-  static const int forced = [] { const char* e = std::getenv("PFC_FUSED_GATHER"); return e ? std::atoi(e) : 1; }();
+  const int forced = env_int("PFC_FUSED_GATHER", 1);
   return forced != 0 && sz.M <= 256 && sz.d % LG_BK == 0 && sz.k_pad % 128 == 0;
 }
 

@@ -6,6 +6,7 @@
 #include <cuda_fp16.h>
 #include <nccl.h>
 #include <stdint.h>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/pfc.h"
@@ -21,6 +22,13 @@ namespace pfc {
 #else
 #define PFC_DCHECK(cond) ((void)0)
 #endif
+
+// Kernel-selection knobs (PFC_* environment variables, for A/B timing): read at every call, not cached, so that a
+// process (the test suite) can switch them between contexts.
+inline int env_int(const char* name, int def) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : def;
+}
 
 // Sticky device error bits (reported as pfc_status by the next synchronising call).
 enum : int { ERR_DATA = 1, ERR_DEGENERATE = 2, ERR_NUMERIC = 4, ERR_INTERNAL = 8 };

@@ -539,7 +539,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
 int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint64_t* step, uint32_t* bits, uint32_t* keys,
                    int* hist, int* tile_cnt, SamplerState* st, int32_t* idx, int32_t* tcol, int* err,
                    cudaStream_t s) {
-  static const bool fused = [] { const char* e = std::getenv("PFC_SAMPLER_FUSED"); return !e || e[0] != '0'; }();
+  const bool fused = env_int("PFC_SAMPLER_FUSED", 1) != 0;
   if (fused) {
     static int per_sm = 0;
     if (!per_sm) {

@@ -278,6 +278,19 @@ def test_pair_kernels_train_step(case, eform, monkeypatch):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
+@pytest.mark.parametrize("variant", ["PFC_DW_XDOT=0", "PFC_DWFULL=1", "PFC_SAMPLER_FUSED=0", "PFC_DW_ORDER=1"])
+def test_alternative_kernels_at_the_per_rank_shape(variant, monkeypatch):
+    """The non-default kernels kept for A/B timing stay correct at M = 2048, d = 512: the pair dW + SGD
+    kernel with the separate radial-dot pass, the all-column dW kernel, the seven-kernel sampler, the tile-major
+    unit order; two train steps against the oracle."""
+    k, v = variant.split("=")
+    monkeypatch.setenv(k, v)
+    case = (60000, 512, 2048, 0.05, "arcface", 0.5, "trained", 0.055)
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
+        assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
 @pytest.mark.parametrize("B,fused", [(96, True), (640, True), (96, False)], ids=["fused-M96", "pair-M640", "fb+step"])
 def test_host_resident_params_match_device(B, fused):
     """SURVEY.md §8(f) f4 (capacity mode): W and V in page-locked, device-mapped host memory run the same kernels
