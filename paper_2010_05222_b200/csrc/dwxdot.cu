@@ -15,7 +15,9 @@
 //   warp 1    TMEM allocation (cta_group::2); MMA issue (leader), commits multicast to both CTAs
 //   warps 2-9 epilogue (this CTA's 128 classes)
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "pfc_internal.cuh"
 #include "tc_common.cuh"
@@ -26,13 +28,29 @@ namespace {
 constexpr int XP_BK = 64;
 constexpr int XP_STAGES = 3;
 constexpr int XP_ACC = 2;
-constexpr int XP_EPI = 8;
+// epilogue warps: 8 (2 per TMEM lane quadrant, 16 rows each). Per-unit trace (PFC_DW_TRACE) at the per-rank C4 shape:
+// dot pass 3.8 us, partner wait 5.3 us, update 16.9 us per unit against ~12 us of MMAs. PFC_XP_EPI=16 at build time
+// (4 per quadrant, twice the loads in flight) measured slower: update 19.5 us, kernel 0.484 vs 0.41 ms.
+#ifndef PFC_XP_EPI
+#define PFC_XP_EPI 8
+#endif
+constexpr int XP_EPI = PFC_XP_EPI;
+constexpr int XP_RPW = 128 / XP_EPI;                  // rows per warp (16 or 8)
+constexpr int XP_NSET = XP_EPI / 4;                   // column sets per TMEM lane quadrant
+static_assert(XP_RPW == 8 || XP_RPW == 16, "epilogue layout");
+constexpr int XP_DB = XP_RPW == 16 ? 8 : 4;           // rows per batch of the dot pass (register budget)
 constexpr int XP_THREADS = 32 * (2 + XP_EPI);
 constexpr int XP_HALF = 128 * XP_BK * 2;              // 16 KB
 constexpr int XP_STAGE = 2 * XP_HALF;                 // A (128 classes x 64 batch) + B (64 batch x 128 columns)
 constexpr int XP_ST = 128 * 256 * 4;                  // fp32 staging of the 128 x 256 accumulator
 constexpr int XP_SMEM = XP_STAGES * XP_STAGE + XP_ST + 1024 + 256 + 3 * 128 * 4;
 static_assert(XP_SMEM <= 232448, "shared memory overflow");
+
+__device__ __forceinline__ uint64_t gtimer() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 struct XpParams {
   int M, d;
@@ -42,6 +60,8 @@ struct XpParams {
   int* flag;        // [n_units][2] published (zeroed before the launch)
   int* err;
   int ehint;
+  uint64_t* trace;   // PFC_DW_TRACE=1 (eager launches only): per CTA and unit, globaltimer at 6 epilogue points
+  int trace_units;
 };
 
 // staging index of float4 q (0..63) of row r (XOR swizzle inside each 32-float4 half)
@@ -168,17 +188,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         scalars(u + npairs);
         pf_j = nx_j;
       }
+      const int ui = (u - pair) / npairs;
+      uint64_t* tr = (p.trace && threadIdx.x == 64 && ui < p.trace_units) ? p.trace + ((int64_t)blockIdx.x * p.trace_units + ui) * 6 : nullptr;
+      if (tr) tr[0] = gtimer();
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
+      if (tr) tr[1] = gtimer();
       {   // the whole 128 x 256 accumulator -> staging (thread = row), TMEM released at once
         const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
 #pragma unroll 1
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < 16 / XP_NSET; ++c) {
           uint32_t v[16];
-          tmem_ld16(tacc + eset * 128 + c * 16, v);
+          tmem_ld16(tacc + eset * (256 / XP_NSET) + c * 16, v);
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            s_st[xidx(row_in, eset * 32 + c * 4 + q)] =
+            s_st[xidx(row_in, eset * (64 / XP_NSET) + c * 4 + q)] =
                 make_float4(__uint_as_float(v[4 * q]), __uint_as_float(v[4 * q + 1]), __uint_as_float(v[4 * q + 2]),
                             __uint_as_float(v[4 * q + 3]));
         }
@@ -191,15 +215,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       }
       if (++acc == XP_ACC) { acc = 0; acc_phase ^= 1; }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * XP_EPI) : "memory");   // staging and scalars complete
+      if (tr) tr[2] = gtimer();
       // this half's dots: warp per row, lanes along the 256 columns (W segments read coalesced; they stay in L2 for
       // the update below)
 #pragma unroll 1
-      for (int r8 = 0; r8 < 16; r8 += 8) {
-        float4 wa[8], wb[8];
-        int32_t j8[8];
+      for (int r8 = 0; r8 < XP_RPW; r8 += XP_DB) {
+        float4 wa[XP_DB], wb[XP_DB];
+        int32_t j8[XP_DB];
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          j8[r] = s_rowj[ew * 16 + r8 + r];
+        for (int r = 0; r < XP_DB; ++r) {
+          j8[r] = s_rowj[ew * XP_RPW + r8 + r];
           if (j8[r] >= 0) {
             const float* wp = p.sgd.W + (int64_t)j8[r] * d + dcol0 + lane * 4;
             wa[r] = *reinterpret_cast<const float4*>(wp);
@@ -209,8 +234,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
           }
         }
 #pragma unroll
-        for (int r = 0; r < 8; ++r) {
-          const int rr = ew * 16 + r8 + r;
+        for (int r = 0; r < XP_DB; ++r) {
+          const int rr = ew * XP_RPW + r8 + r;
           const float4 ga = s_st[xidx(rr, lane)], gb = s_st[xidx(rr, 32 + lane)];
           float v = wa[r].x * ga.x + wa[r].y * ga.y + wa[r].z * ga.z + wa[r].w * ga.w;
           v += wb[r].x * gb.x + wb[r].y * gb.y + wb[r].z * gb.z + wb[r].w * gb.w;
@@ -218,6 +243,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
           if (lane == 0) p.xdot[((int64_t)u * 2 + pr) * 128 + rr] = v;
         }
       }
+      if (tr) tr[3] = gtimer();
       // publish this CTA's half-dots, then take the partner CTA's (unit u ^ 1, same classes, same rank)
       asm volatile("bar.sync 3, %0;" ::"n"(32 * XP_EPI) : "memory");
       if (ew == 0 && lane == 0) {
@@ -238,6 +264,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         s_dot[row_in] = d0 + d1;
       }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * XP_EPI) : "memory");
+      if (tr) tr[4] = gtimer();
       if (pf_j >= 0) {   // the next unit's W / V row segments (256 columns) into L2
         const int ndc = ((u + npairs) & 1) * 256;
         const float* wp = p.sgd.W + (int64_t)pf_j * d + ndc;
@@ -257,7 +284,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         auto load = [&](int b, int slot) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const int rr = ew * 16 + 4 * b + r;
+            const int rr = ew * XP_RPW + 4 * b + r;
             jr[slot][r] = s_rowj[rr];
             PFC_DCHECK(jr[slot][r] < p.sgd.rows);
             if (jr[slot][r] >= 0) {
@@ -270,7 +297,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         auto upd = [&](int b, int slot) {
 #pragma unroll
           for (int r = 0; r < 4; ++r) {
-            const int rr = ew * 16 + 4 * b + r;
+            const int rr = ew * XP_RPW + 4 * b + r;
             if (jr[slot][r] >= 0) {
               const float inv = s_inv[rr];
               const float rad = s_dot[rr] * inv * inv;        // (w_hat . dW_hat) / ||w||
@@ -291,12 +318,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         load(0, 0);
         load(1, 1);
         upd(0, 0);
-        load(2, 0);
-        upd(1, 1);
-        load(3, 1);
-        upd(2, 0);
-        upd(3, 1);
+        if constexpr (XP_RPW == 16) {
+          load(2, 0);
+          upd(1, 1);
+          load(3, 1);
+          upd(2, 0);
+          upd(3, 1);
+        } else {
+          upd(1, 1);
+        }
       }
+      if (tr) tr[5] = gtimer();
     }
   }
   tc_fence_before();
@@ -350,7 +382,37 @@ int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_b
   at[0].val.cooperative = 1;
   lc.attrs = at;
   lc.numAttrs = 1;
+  // PFC_DW_TRACE=1: per-unit epilogue timestamps of one eager launch, written to $PFC_DW_TRACE_FILE (diagnostic)
+  static uint64_t* trace = nullptr;
+  const bool tracing = env_int("PFC_DW_TRACE", 0) != 0;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const int tunits = (int)((units + pairs - 1) / pairs);
+  if (tracing && cs == cudaStreamCaptureStatusNone) {
+    if (!trace) cudaMalloc(&trace, (size_t)2 * pairs * tunits * 6 * sizeof(uint64_t));
+    cudaMemsetAsync(trace, 0, (size_t)2 * pairs * tunits * 6 * sizeof(uint64_t), s);
+    p.trace = trace;
+    p.trace_units = tunits;
+  }
   cudaLaunchKernelEx(&lc, kern, a, b, p);
+  if (p.trace) {
+    std::vector<uint64_t> h((size_t)2 * pairs * tunits * 6);
+    cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const char* fn = std::getenv("PFC_DW_TRACE_FILE");
+    if (FILE* f = std::fopen(fn ? fn : "dw_trace.csv", "w")) {
+      std::fprintf(f, "cta,unit,wait_start,acc_full,staged,dot_done,xchg_done,update_done\n");
+      for (int c = 0; c < 2 * pairs; ++c)
+        for (int i = 0; i < tunits; ++i) {
+          const uint64_t* r = h.data() + ((size_t)c * tunits + i) * 6;
+          if (!r[0]) continue;
+          std::fprintf(f, "%d,%d,%llu,%llu,%llu,%llu,%llu,%llu\n", c, i, (unsigned long long)r[0],
+                       (unsigned long long)r[1], (unsigned long long)r[2], (unsigned long long)r[3],
+                       (unsigned long long)r[4], (unsigned long long)r[5]);
+        }
+      std::fclose(f);
+    }
+  }
   return 2;
 }
 
