@@ -59,7 +59,9 @@ struct XpParams {
   float* xdot;      // [n_units][128 * 2] this unit's half-dots, by CTA rank and row
   int* flag;        // [n_units][2] published (zeroed before the launch)
   int* err;
-  int ehint;
+  int ehint;   // E' loads: 0 default L2 policy, 1 evict-last, 2 evict-first
+  int pfnow;
+  int hoist;   // the update's first W / V loads issued before the partner wait   // prefetch this unit's W / V rows into L2 when its scalars are known (else the next unit's, a unit ahead)
   uint64_t* trace;   // PFC_DW_TRACE=1 (eager launches only): per CTA and unit, globaltimer at 6 epilogue points
   int trace_units;
 };
@@ -114,7 +116,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       uint32_t phase = 0;
       // PFC_DW_EHINT=1: E' loads with an L2 evict-last policy (read by the two partner pairs of a tile at the same
       // time) — measured no better (c4rank 1.015 vs 1.008 ms), off by default
-      const uint64_t epol = policy_evict_last();
+      const uint64_t epol = p.ehint == 2 ? policy_evict_first() : policy_evict_last();
       for (int u = pair; u < n_units; u += npairs) {
         const int c0 = (u >> 1) * 256 + 128 * pr, d0 = (u & 1) * 256 + 128 * pr;
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -185,8 +187,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       int32_t pf_j = -1;
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv;
+        if (p.pfnow && nx_j >= 0) {   // this unit's W / V row segments into L2 now (used ~10 us later)
+          const float* wp = p.sgd.W + (int64_t)nx_j * d + h * 256;
+          const float* vp = p.sgd.V + (int64_t)nx_j * d + h * 256;
+#pragma unroll
+          for (int l = 0; l < 8; ++l) {
+            if (p.pfnow == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          }
+        }
         scalars(u + npairs);
-        pf_j = nx_j;
+        pf_j = p.pfnow == 1 ? -1 : nx_j;
       }
       const int ui = (u - pair) / npairs;
       uint64_t* tr = (p.trace && threadIdx.x == 64 && ui < p.trace_units) ? p.trace + ((int64_t)blockIdx.x * p.trace_units + ui) * 6 : nullptr;
@@ -244,11 +255,57 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
         }
       }
       if (tr) tr[3] = gtimer();
-      // publish this CTA's half-dots, then take the partner CTA's (unit u ^ 1, same classes, same rank)
+      // publish this CTA's half-dots, then take the partner CTA's (unit u ^ 1, same classes, same rank); the first
+      // W / V loads of the update are issued before the wait (they need the rows, not the dot)
       asm volatile("bar.sync 3, %0;" ::"n"(32 * XP_EPI) : "memory");
       if (ew == 0 && lane == 0) {
         __threadfence();
         asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p.flag + (u * 2 + pr)), "r"(1) : "memory");
+      }
+      float4 wv[2][4], mv[2][4];
+      int32_t jr[2][4];
+      auto load = [&](int sh, int b, int slot) {
+        const int col = dcol0 + sh * 128 + lane * 4;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int rr = ew * XP_RPW + 4 * b + r;
+          jr[slot][r] = s_rowj[rr];
+          PFC_DCHECK(jr[slot][r] < p.sgd.rows);
+          if (jr[slot][r] >= 0) {
+            wv[slot][r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[slot][r] * d + col);
+            mv[slot][r] = HINT ? ld_hint4(p.sgd.V + (int64_t)jr[slot][r] * d + col, pol)
+                               : *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[slot][r] * d + col);
+          }
+        }
+      };
+      // momentum-SGD update of 4 rows over 128 columns (the staging holds dW_hat of this unit)
+      auto upd = [&](int sh, int b, int slot) {
+        const int col = dcol0 + sh * 128 + lane * 4;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int rr = ew * XP_RPW + 4 * b + r;
+          if (jr[slot][r] >= 0) {
+            const float inv = s_inv[rr];
+            const float rad = s_dot[rr] * inv * inv;        // (w_hat . dW_hat) / ||w||
+            const float4 g = s_st[xidx(rr, sh * 32 + lane)];
+            float4 w = wv[slot][r], m = mv[slot][r];
+            m.x = mu * m.x + (g.x - w.x * rad) * inv + lam * w.x;
+            m.y = mu * m.y + (g.y - w.y * rad) * inv + lam * w.y;
+            m.z = mu * m.z + (g.z - w.z * rad) * inv + lam * w.z;
+            m.w = mu * m.w + (g.w - w.w * rad) * inv + lam * w.w;
+            w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
+            float* wp = p.sgd.W + (int64_t)jr[slot][r] * d + col;
+            float* vp = p.sgd.V + (int64_t)jr[slot][r] * d + col;
+            if (HINT) { st_hint4(vp, m, pol); st_hint4(wp, w, pol); }
+            else { *reinterpret_cast<float4*>(vp) = m; *reinterpret_cast<float4*>(wp) = w; }
+          }
+        }
+      };
+      if (p.hoist) {
+        load(0, 0, 0);
+        load(0, 1, 1);
+      }
+      if (ew == 0 && lane == 0) {
         PFC_DCHECK((u ^ 1) < n_units);
         const int* f = p.flag + ((u ^ 1) * 2 + pr);
         int v = 0, spins = 0;
@@ -265,67 +322,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * XP_EPI) : "memory");
       if (tr) tr[4] = gtimer();
-      if (pf_j >= 0) {   // the next unit's W / V row segments (256 columns) into L2
+      if (pf_j >= 0) {   // the next unit's W (and, without PFC_DW_PFNOW, V) row segments (256 columns) into L2
         const int ndc = ((u + npairs) & 1) * 256;
         const float* wp = p.sgd.W + (int64_t)pf_j * d + ndc;
         const float* vp = p.sgd.V + (int64_t)pf_j * d + ndc;
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          if (!p.pfnow) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
         }
       }
-      // momentum-SGD update: per 128-column quarter, 4-row batches, the next batch's W / V loads in flight
-#pragma unroll 1
+      // the update, 4-row batches per 128-column quarter, the next batch's W / V loads in flight
+#pragma unroll
       for (int sh = 0; sh < 2; ++sh) {
-        const int col = dcol0 + sh * 128 + lane * 4;
-        float4 wv[2][4], mv[2][4];
-        int32_t jr[2][4];
-        auto load = [&](int b, int slot) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int rr = ew * XP_RPW + 4 * b + r;
-            jr[slot][r] = s_rowj[rr];
-            PFC_DCHECK(jr[slot][r] < p.sgd.rows);
-            if (jr[slot][r] >= 0) {
-              wv[slot][r] = *reinterpret_cast<const float4*>(p.sgd.W + (int64_t)jr[slot][r] * d + col);
-              mv[slot][r] = HINT ? ld_hint4(p.sgd.V + (int64_t)jr[slot][r] * d + col, pol)
-                                 : *reinterpret_cast<const float4*>(p.sgd.V + (int64_t)jr[slot][r] * d + col);
-            }
-          }
-        };
-        auto upd = [&](int b, int slot) {
-#pragma unroll
-          for (int r = 0; r < 4; ++r) {
-            const int rr = ew * XP_RPW + 4 * b + r;
-            if (jr[slot][r] >= 0) {
-              const float inv = s_inv[rr];
-              const float rad = s_dot[rr] * inv * inv;        // (w_hat . dW_hat) / ||w||
-              const float4 g = s_st[xidx(rr, sh * 32 + lane)];
-              float4 w = wv[slot][r], m = mv[slot][r];
-              m.x = mu * m.x + (g.x - w.x * rad) * inv + lam * w.x;
-              m.y = mu * m.y + (g.y - w.y * rad) * inv + lam * w.y;
-              m.z = mu * m.z + (g.z - w.z * rad) * inv + lam * w.z;
-              m.w = mu * m.w + (g.w - w.w * rad) * inv + lam * w.w;
-              w.x -= lr * m.x; w.y -= lr * m.y; w.z -= lr * m.z; w.w -= lr * m.w;
-              float* wp = p.sgd.W + (int64_t)jr[slot][r] * d + col;
-              float* vp = p.sgd.V + (int64_t)jr[slot][r] * d + col;
-              if (HINT) { st_hint4(vp, m, pol); st_hint4(wp, w, pol); }
-              else { *reinterpret_cast<float4*>(vp) = m; *reinterpret_cast<float4*>(wp) = w; }
-            }
-          }
-        };
-        load(0, 0);
-        load(1, 1);
-        upd(0, 0);
+        if (sh == 1 || !p.hoist) {
+          load(sh, 0, 0);
+          load(sh, 1, 1);
+        }
+        upd(sh, 0, 0);
         if constexpr (XP_RPW == 16) {
-          load(2, 0);
-          upd(1, 1);
-          load(3, 1);
-          upd(2, 0);
-          upd(3, 1);
+          load(sh, 2, 0);
+          upd(sh, 1, 1);
+          load(sh, 3, 1);
+          upd(sh, 2, 0);
+          upd(sh, 3, 1);
         } else {
-          upd(1, 1);
+          upd(sh, 1, 1);
         }
       }
       if (tr) tr[5] = gtimer();
@@ -367,6 +389,8 @@ int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_b
   p.xdot = ws;
   const int ehint = env_int("PFC_DW_EHINT", 0);
   p.ehint = ehint;
+  p.pfnow = env_int("PFC_DW_PFNOW", 1);
+  p.hoist = env_int("PFC_DW_HOIST", 1);
   p.flag = reinterpret_cast<int*>(ws + units * 256);
   cudaMemsetAsync(p.flag, 0, (size_t)units * 2 * sizeof(int), s);
   // every pair of the grid is co-resident (one CTA per SM, units in lock-step): the partner waits cannot deadlock.
