@@ -60,6 +60,7 @@ struct DwxParams {
   int* cnt;             // [nct] partials published per class tile (zeroed each step)
   int* err;
   float s;              // logit scale
+  int pfnow;            // prefetch the current tile's W / V rows at its start (as well as the next tile's)
 };
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
@@ -277,6 +278,15 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile fully consumed
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
+        if (p.pfnow && nx_j >= 0) {   // this tile's W / V row segments into L2 (PFC_DWX_PFNOW=1)
+          const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
+          const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          }
+        }
         nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
         if (i + 1 < ntl) {
           const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
@@ -478,6 +488,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   TC_MAPS_OK();
   DwxParams p{};
   p.M = sz.M; p.d = sz.d; p.nkb = (int)(sz.M_pad / 64); p.gper = dwx_gper(sz); p.st = st; p.sgd = sa; p.ws = ws;
+  p.pfnow = env_int("PFC_DWX_PFNOW", 0);
   if (ef) {
     p.f = ef->f; p.tcol = ef->tcol; p.dcorr = ef->dcorr; p.xch = ef->xch; p.cnt = ef->cnt; p.err = ef->err;
     p.s = ef->s;
