@@ -14,7 +14,7 @@ for r in rows[hi + 1:]:
 mult = {'byte': 1, 'Kbyte': 1e3, 'Mbyte': 1e6, 'Gbyte': 1e9, 'ns': 1e-3, 'us': 1, 'ms': 1e3}
 agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0])
 for (i, name), m in data.items():
-    mt = re.search(r'pfc::.*?(k_[a-z0-9_]+(<[^>]*>)?)', name)
+    mt = re.search(r'(?:pfc::|unnamed>::)(?:<unnamed>::)?(k_[a-z0-9_]+(<[^>]*>)?)', name)
     if not mt:            # torch's own kernels (the synthetic W fill before the timed steps)
         continue
     short = mt.group(1)
