@@ -16,9 +16,14 @@
  *   - Collective contract (world_size > 1): every rank calls the hot-path entry points in the same order
  *     with the same B (Alg.1 is a collective program).
  *   - Host-detectable errors are returned synchronously and leave the context unchanged. Errors found on
- *     the device (label outside [0, C), zero-norm row, non-finite loss) set a sticky device word that is
- *     reported by the next synchronising call (pfc_step, pfc_get_*, pfc_check) — or at once when the
- *     environment variable PFC_SYNC_CHECK=1 is set.
+ *     the device (label outside [0, C), zero-norm row, non-finite loss, an internal consistency check) set a
+ *     sticky device word. The last kernel of every step mirrors it into page-locked host memory, and every
+ *     hot-path entry point (pfc_forward_backward, pfc_train_step, pfc_step, the *_host and group variants)
+ *     checks that mirror first, without synchronising: an error of an earlier, completed step is returned by the
+ *     next call. Synchronising calls (pfc_check, pfc_get_*) report it at once; PFC_SYNC_CHECK=1 makes every
+ *     step synchronise and report its own error.
+ *   - NCCL: host waits poll ncclCommGetAsyncError; an asynchronous error or a collective exceeding
+ *     PFC_NCCL_TIMEOUT_S seconds (default 600) aborts the communicator and returns PFC_ERR_NCCL.
  *   - Not re-entrant: one host thread per context.
  */
 #ifndef PFC_H_
