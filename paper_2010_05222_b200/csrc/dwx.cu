@@ -17,7 +17,9 @@
 //             also stage the old w as the bf16 dX operand
 #include <cuda_bf16.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "pfc_internal.cuh"
 #include "tc_common.cuh"
@@ -61,7 +63,15 @@ struct DwxParams {
   int* err;
   float s;              // logit scale
   int pfnow;            // prefetch the current tile's W / V rows at its start (as well as the next tile's)
+  uint64_t* trace;      // PFC_DWX_TRACE=1 (eager launches): per-tile epilogue timestamps, [cta][tile][8]
+  int trace_tiles;
 };
+
+__device__ __forceinline__ uint64_t gtimer_dx() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -250,6 +260,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
         for (int q = 0; q < RPT; ++q) dst[t + q * 32 * DX_DOTW] = kc * B[q];
         if (DX_DOTW > 1) asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
         else __syncwarp();
+        if (t == 0 && p.trace && i < p.trace_tiles) p.trace[((int64_t)blockIdx.x * p.trace_tiles + i) * 8 + 7] = gtimer_dx();
         if (t == 0) {
           // release (cumulative over the barrier above): the partials are visible at gpu scope before the count
           // (the epilogues poll it with acquire loads)
@@ -276,6 +287,9 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
     const int col = n0 + lane * 4;           // row-update mapping: one 512-byte row segment per warp instruction
     for (int i = 0; i < ntl; ++i) {
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile fully consumed
+      uint64_t* tr = (p.trace && threadIdx.x == 64 && i < p.trace_tiles)
+                         ? p.trace + ((int64_t)blockIdx.x * p.trace_tiles + i) * 8 : nullptr;
+      if (tr) tr[0] = gtimer_dx();
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
         if (p.pfnow && nx_j >= 0) {   // this tile's W / V row segments into L2 (PFC_DWX_PFNOW=1)
@@ -296,6 +310,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
       mbar_wait(&d1_full[acc], aph);
       tc_fence_after();
+      if (tr) tr[1] = gtimer_dx();
       float rad16 = 0.f;   // E-form: lane l < 16 forms the radial dot of row ew * 16 + l
       float radp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
       if (EF) {
@@ -311,6 +326,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           if (v < n_dt) atomicOr(p.err, ERR_INTERNAL);   // never expected: bounded instead of a hang
         }
         __syncwarp();
+        if (tr) tr[2] = gtimer_dx();
         if (lane < 16) {   // loads only: summed after the staging
           const int row = ew * 16 + lane;
           rad16 = __ldcg(p.dcorr + ct * 128 + row);
@@ -337,9 +353,11 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       if (lane == 0) mbar_arrive(&d1_empty[acc]);
       if (++acc == 2) { acc = 0; aph ^= 1; }
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
+      if (tr) tr[3] = gtimer_dx();
       // (3) momentum-SGD row updates (rows L2-prefetched a tile ahead), 8 rows in flight per lane; the old w
       // also goes to the bf16 dX operand tile, once dX(t - 1) has read the previous one
       mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));
+      if (tr) tr[4] = gtimer_dx();
       if (EF) {   // into the per-row slot the update loop reads (a shuffle there serialises the row updates)
 #pragma unroll
         for (int q = 0; q < 8; ++q) rad16 += radp[q];
@@ -395,6 +413,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
             }
           }
         }
+        if (tr) tr[5 + r0 / 8] = gtimer_dx();
         if (r0 == 0 && eset == 0 && nx_j >= 0) {   // the next tile's W / V row segments into L2
           const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
           const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
@@ -495,6 +514,18 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     cudaMemsetAsync(ef->cnt, 0, (size_t)(sz.k_pad / 128) * sizeof(int), s);
   }
   const int grid = p.gper * (sz.d / 128);
+  static uint64_t* trace = nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const int ttiles = (int)((sz.k_pad / 128 + p.gper - 1) / p.gper);
+  if (env_int("PFC_DWX_TRACE", 0) && cs == cudaStreamCaptureStatusNone) {
+    static size_t cap = 0;
+    const size_t need = (size_t)grid * ttiles * 8 * sizeof(uint64_t);
+    if (need > cap) { if (trace) cudaFree(trace); cudaMalloc(&trace, need); cap = need; }
+    cudaMemsetAsync(trace, 0, need, s);
+    p.trace = trace;
+    p.trace_tiles = ttiles;
+  }
   if (ef) {
     // the E-form epilogue waits on radial-dot partials published by the other d-tile CTAs of its class tile: a
     // cooperative launch guarantees that the whole grid (<= one CTA per SM) is co-resident, or fails loudly
@@ -512,6 +543,24 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     cudaLaunchKernelEx(&lc, kern, tg, tx, p);
   } else {
     kern<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+  }
+  if (p.trace) {
+    std::vector<uint64_t> h((size_t)grid * ttiles * 8);
+    cudaMemcpyAsync(h.data(), trace, h.size() * sizeof(uint64_t), cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    const char* fn = std::getenv("PFC_DWX_TRACE_FILE");
+    if (FILE* f = std::fopen(fn ? fn : "dwx_trace.csv", "w")) {
+      std::fprintf(f, "cta,tile,start,d1_full,cnt_ok,staged,wb_empty,batch0,update_done,dot_published\n");
+      for (int c = 0; c < grid; ++c)
+        for (int i = 0; i < ttiles; ++i) {
+          const uint64_t* r = h.data() + ((size_t)c * ttiles + i) * 8;
+          if (!r[0]) continue;
+          std::fprintf(f, "%d,%d", c, i);
+          for (int q = 0; q < 8; ++q) std::fprintf(f, ",%llu", (unsigned long long)r[q]);
+          std::fprintf(f, "\n");
+        }
+      std::fclose(f);
+    }
   }
   const int64_t n = (int64_t)sz.M * sz.d;
   Peers q{};

@@ -59,6 +59,8 @@ struct LgParams {
   float2* partials;        // M x n_ltiles
   int n_ltiles;
   int write_ws;            // store bf16(w) into W_s (the separate dX GEMM needs it; the fused dW/dX kernel does not)
+  int g4;                  // PFC_LG_G4=1: the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity
+                           // holds, measured 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
 };
 
 __device__ __forceinline__ uint32_t pack_f16(float a, float b) {
@@ -75,7 +77,8 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // the softmax-gradient pass over the cosines disappears.
 template <bool EF>
 __global__ void __launch_bounds__(LG_THREADS, 1)
-    k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs, LgParams p) {
+    k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs,
+                    const __grid_constant__ CUtensorMap tmW, LgParams p) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* aux = smem + LG_STAGES * LG_STAGE;
@@ -97,7 +100,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < LG_STAGES; ++i) {
-      mbar_init(&full[i], 1 + 32 * LG_PROD);      // TMA expect_tx + one cp.async arrive per producer lane
+      mbar_init(&full[i], p.g4 ? 1 : 1 + 32 * LG_PROD);   // TMA expect_tx (+ one cp.async arrive per producer lane)
       mbar_init(&conv[i], LG_CONV);
       mbar_init(&empty[i], 2);                    // MMA commit + W_s store read back
     }
@@ -110,7 +113,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_smem();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmWs); }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmWs); if (p.g4) tma_prefetch(&tmW); }
   if (warp == LG_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
@@ -121,12 +124,45 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < LG_PROD) {
+  if (warp < LG_PROD && p.g4) {
+    // ---------------------------------------------------------------- producer (TMA gather4 variant)
+    // lane l gathers rows 4l .. 4l + 3 of the tile: two 32-column boxes (128 B per row, 128-byte swizzle) per K
+    // block, the two halves 16 KB apart; rows past k_i fetch row 0 (their converter threads write zeros)
+    if (warp == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = blockIdx.x; t < nt; t += gridDim.x) {
+        const int n0 = t * 128;
+        int r4[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int r = n0 + 4 * lane + i;
+          r4[i] = r < k ? p.idx[r] : 0;
+        }
+        for (int kb = 0; kb < n_kb; ++kb) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          uint8_t* sa = smem + stage * LG_STAGE;
+          uint8_t* sw = sa + LG_A_BYTES;
+          if (lane == 0) {
+            mbar_expect_tx(&full[stage], (uint32_t)(LG_A_BYTES + 128 * LG_BK * 4));
+            tma_load_2d(sa, &tmA, &full[stage], kb * LG_BK, 0);
+            tma_load_2d(sa + 128 * LG_BK * 2, &tmA, &full[stage], kb * LG_BK, 128);
+          }
+          __syncwarp();
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            tma_gather4(sw + h * 16384 + lane * 512, &tmW, &full[stage], kb * LG_BK + h * 32, r4[0], r4[1], r4[2], r4[3]);
+          if (++stage == LG_STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp < LG_PROD) {
     // ---------------------------------------------------------------- producers
     // W rows: 16-byte cp.async (LDGSTS); a warp instruction moves two rows x 256 B (coalesced); warp pw owns
     // rows 64 pw .. 64 pw + 63 of the tile, their ids held in registers for the whole tile; completion is
     // tracked by the stage mbarrier (cp.async.mbarrier.arrive.noinc). X_hat by TMA. (One 256-byte
-    // cp.async.bulk per row, and a single producer warp reading row ids from smem, were measured far slower.)
+    // cp.async.bulk per row, a single producer warp reading row ids from smem, and TMA tile::gather4 of 128-byte row
+    // boxes (PFC_LG_G4=1, the variant branch above) were measured slower.)
     int stage = 0;
     uint32_t phase = 0;
     const int half = lane >> 4, ch = lane & 15;
@@ -211,7 +247,10 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
           const float4* src = reinterpret_cast<const float4*>(sw + r * LG_PITCH);
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
-            const float4 v = src[q];
+            // gather4 layout: half q / 8 (16 KB apart), row r at 128 B, 16-byte chunk (q % 8) ^ (r % 8)
+            const float4 v = p.g4 ? *reinterpret_cast<const float4*>(sw + (q >> 3) * 16384 + r * 128 +
+                                                                   (((q & 7) ^ (r & 7)) << 4))
+                                  : src[q];
             ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
             amax = fmaxf(amax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
             pk[2 * q] = pack_f16(v.x, v.y);
@@ -431,15 +470,19 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   }
   const CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 X_hat (R27)
   const CUtensorMap ws = make_map(Ws, sz.k_pad, sz.d, 64, 128);
+  const int g4 = env_int("PFC_LG_G4", 0);
+  const CUtensorMap wm = g4 ? make_map_typed(W, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (uint64_t)sz.C_local, sz.d, 32, 1)
+                            : ws;
   TC_MAPS_OK();
   LgParams p{};
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.st = st; p.W = W; p.idx = idx; p.inv_norm = inv_norm; p.err = err;
   p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
   p.write_ws = write_ws ? 1 : 0;
+  p.g4 = g4;
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
-  if (eform) k_logits_gather<true><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
-  else k_logits_gather<false><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, p);
+  if (eform) k_logits_gather<true><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
+  else k_logits_gather<false><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
   return 1;
 }
 

@@ -9,6 +9,7 @@
 // Everything is device-resident (k_i is data-dependent); no host synchronisation.
 #include <cooperative_groups.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include "pfc_internal.cuh"
 
@@ -354,8 +355,19 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
                                                             double rate, int mode, uint32_t* __restrict__ bits,
                                                             uint32_t* __restrict__ keys, int* __restrict__ hist,
                                                             int* __restrict__ tile_cnt, int ntiles, SamplerState* st,
-                                                            int32_t* __restrict__ idx, int* err) {
+                                                            int32_t* __restrict__ idx, int* err,
+                                                            unsigned long long* trace) {
   namespace cg = cooperative_groups;
+  int tp = 0;
+  auto mark = [&]() {   // PFC_SAMPLER_TRACE=1: globaltimer at every phase boundary (block 0)
+    if (trace && blockIdx.x == 0 && threadIdx.x == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      trace[tp] = t;
+    }
+    ++tp;
+  };
+  mark();
   cg::grid_group grid = cg::this_grid();
   __shared__ int sh[2048];
   __shared__ int wsum[kThreads / 32];
@@ -368,6 +380,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
   for (int64_t i = gtid; i < 2048 + 2048 + 1024; i += gthreads) hist[i] = 0;
   if (gtid < (int64_t)(sizeof(SamplerState) / sizeof(int))) reinterpret_cast<int*>(st)[gtid] = 0;
   grid.sync();
+  mark();
   // phase 1 (K2): positives
   if (mode != PFC_SAMPLE_RANDOM)
     for (int64_t n = gtid; n < M; n += gthreads) {
@@ -379,6 +392,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
       }
     }
   grid.sync();
+  mark();
   // phase 2 (K3 pass 1): keys and the top-11-bit histogram of the non-positive classes
   {
     const uint32_t step = (uint32_t)*step_dev;
@@ -403,6 +417,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
       if (sh[i]) atomicAdd(&hist[i], sh[i]);
   }
   grid.sync();
+  mark();
   // phase 3 (K3 pass 2): k_i, n_i; the first digit; histogram of the second inside its bucket
   const int npos = st->npos;
   const int kk = budget_k(npos, budget, C_local, rate, mode);
@@ -413,13 +428,29 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     block_select(hist, 2048, n_neg, b1, rem1);
     for (int i = threadIdx.x; i < 2048; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    for (int64_t j0 = gtid * 4; j0 < C_local; j0 += gthreads * 4) {
-      const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
-      const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
-      const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+    // four coalesced 16-byte key loads in flight per thread (the L2-resident key array, padded to whole tiles)
+    const int64_t s4 = gthreads * 4;
+    for (int64_t base = gtid * 4; base < C_local; base += 4 * s4) {
+      uint4 h4[4];
+      uint32_t pw[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if ((hh[i] >> 21) == (uint32_t)b1 && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[(hh[i] >> 10) & 0x7FF], 1);
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j0 = base + u * s4;
+        if (j0 < C_local) {
+          h4[u] = *reinterpret_cast<const uint4*>(keys + j0);
+          pw[u] = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j0 = base + u * s4;
+        if (j0 >= C_local) break;
+        const uint32_t hh[4] = {h4[u].x, h4[u].y, h4[u].z, h4[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((hh[i] >> 21) == (uint32_t)b1 && !((pw[u] >> i) & 1u) && j0 + i < C_local)
+            atomicAdd(&sh[(hh[i] >> 10) & 0x7FF], 1);
+      }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 2048; i += blockDim.x)
@@ -429,6 +460,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     st->k = kk; st->n_neg = n_neg; st->none = none ? 1 : 0; st->prefix1 = (uint32_t)b1; st->rem1 = rem1;
   }
   grid.sync();
+  mark();
   // phase 4 (K3 pass 3): the second digit; histogram of the last 10 bits
   uint32_t pre = 0;
   int rem2 = 0;
@@ -438,13 +470,27 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     pre = ((uint32_t)b1 << 11) | (uint32_t)b2;
     for (int i = threadIdx.x; i < 1024; i += blockDim.x) sh[i] = 0;
     __syncthreads();
-    for (int64_t j0 = gtid * 4; j0 < C_local; j0 += gthreads * 4) {
-      const uint4 h4 = *reinterpret_cast<const uint4*>(keys + j0);
-      const uint32_t pw = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
-      const uint32_t hh[4] = {h4.x, h4.y, h4.z, h4.w};
+    const int64_t s4 = gthreads * 4;
+    for (int64_t base = gtid * 4; base < C_local; base += 4 * s4) {
+      uint4 h4[4];
+      uint32_t pw[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if ((hh[i] >> 10) == pre && !((pw >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[hh[i] & 0x3FF], 1);
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j0 = base + u * s4;
+        if (j0 < C_local) {
+          h4[u] = *reinterpret_cast<const uint4*>(keys + j0);
+          pw[u] = __ldg(&bits[j0 >> 5]) >> (j0 & 31);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int64_t j0 = base + u * s4;
+        if (j0 >= C_local) break;
+        const uint32_t hh[4] = {h4[u].x, h4[u].y, h4[u].z, h4[u].w};
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          if ((hh[i] >> 10) == pre && !((pw[u] >> i) & 1u) && j0 + i < C_local) atomicAdd(&sh[hh[i] & 0x3FF], 1);
+      }
     }
     __syncthreads();
     for (int i = threadIdx.x; i < 1024; i += blockDim.x)
@@ -452,6 +498,7 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     if (blockIdx.x == 0 && threadIdx.x == 0) { st->prefix2 = pre; st->rem2 = rem2; }
   }
   grid.sync();
+  mark();
   // phase 5 (K4a): the threshold key T and t; definite / tied counts per 8192-class tile
   uint32_t T = 0;
   int tsel = 0;
@@ -481,34 +528,38 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     __syncthreads();
   }
   grid.sync();
+  mark();
   // phase 6 (K4b): exclusive scans of the tile counts (block 0)
   if (blockIdx.x == 0) {
     int* def = tile_cnt;
     int* tie = tile_cnt + ntiles;
     int* tie_off = tile_cnt + 2 * ntiles;
     int* sel_off = tile_cnt + 3 * ntiles;
-    const int lane = threadIdx.x & 31;
+    // thread t scans the contiguous tiles [t cpt, (t + 1) cpt) serially around ONE block scan per pass
+    const int cpt = (ntiles + kThreads - 1) / kThreads;
+    const int i0 = min(ntiles, threadIdx.x * cpt), i1 = min(ntiles, i0 + cpt);
     for (int pass = 0; pass < 2; ++pass) {
-      int carry = 0;
-      for (int base = 0; base < ntiles; base += kThreads) {
-        const int i = base + threadIdx.x;
-        int v = 0;
-        if (i < ntiles) v = pass == 0 ? tie[i] : def[i] + (none ? 0 : max(0, min(tsel - tie_off[i], tie[i])));
-        int tot;
-        const int ex = block_count_scan(v, wsum, tot);
-        if (i < ntiles) (pass == 0 ? tie_off : sel_off)[i] = carry + ex;
-        carry += tot;
-        __syncthreads();
+      auto val = [&](int i) {
+        return pass == 0 ? tie[i] : def[i] + (none ? 0 : max(0, min(tsel - tie_off[i], tie[i])));
+      };
+      int local = 0;
+      for (int i = i0; i < i1; ++i) local += val(i);
+      int tot;
+      int run = block_count_scan(local, wsum, tot);
+      for (int i = i0; i < i1; ++i) {
+        const int v = val(i);
+        (pass == 0 ? tie_off : sel_off)[i] = run;
+        run += v;
       }
       if (pass == 1 && threadIdx.x == 0) {
-        st->total = carry;
-        if (carry != kk) atomicOr(err, ERR_INTERNAL);
+        st->total = tot;
+        if (tot != kk) atomicOr(err, ERR_INTERNAL);
       }
-      (void)lane;
       __syncthreads();
     }
   }
   grid.sync();
+  mark();
   // phase 7 (K4c): order-preserving write of the selected local ids
   for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const int64_t j0 = (int64_t)tile * kSelTile + 32 * threadIdx.x;
@@ -532,6 +583,8 @@ __global__ void __launch_bounds__(kThreads) k_sampler_fused(const int64_t* __res
     }
     __syncthreads();
   }
+  grid.sync();
+  mark();
 }
 
 }  // namespace
@@ -558,8 +611,22 @@ int launch_sampler(const Sizes& sz, const int64_t* Y, uint64_t seed, const uint6
     at[0].val.cooperative = 1;
     lc.attrs = at;
     lc.numAttrs = 1;
+    static unsigned long long* trace = nullptr;
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    const bool tracing = env_int("PFC_SAMPLER_TRACE", 0) != 0 && cs == cudaStreamCaptureStatusNone;
+    if (tracing && !trace) cudaMalloc(&trace, 64 * sizeof(unsigned long long));
     cudaLaunchKernelEx(&lc, k_sampler_fused, Y, sz.M, sz.a, sz.C_local, seed, step, sz.budget, sz.rate,
-                       sz.sample_mode, bits, keys, hist, tile_cnt, sz.ntiles_sel, st, idx, err);
+                       sz.sample_mode, bits, keys, hist, tile_cnt, sz.ntiles_sel, st, idx, err,
+                       tracing ? trace : (unsigned long long*)nullptr);
+    if (tracing) {
+      unsigned long long h[16] = {0};
+      cudaMemcpyAsync(h, trace, sizeof(h), cudaMemcpyDeviceToHost, s);
+      cudaStreamSynchronize(s);
+      std::fprintf(stderr, "sampler phases (us):");
+      for (int i = 1; i < 10 && h[i]; ++i) std::fprintf(stderr, " %.1f", (h[i] - h[i - 1]) / 1e3);
+      std::fprintf(stderr, "  grid=%d\n", grid);
+    }
     (void)tcol;
     return 1;
   }

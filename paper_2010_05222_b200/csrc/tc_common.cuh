@@ -46,6 +46,16 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
       "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1)
       : "memory");
 }
+// TMA row gather (sm_100a tile::gather4): rows r0..r3 of a 2D map (box {box_cols, 1}) at column c0, landing as four
+// consecutive box rows at dst (the map's swizzle applied by shared-memory address, as for a 4-row tile)
+__device__ __forceinline__ void tma_gather4(void* dst, const CUtensorMap* map, uint64_t* bar, int c0, int r0, int r1,
+                                            int r2, int r3) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, "
+      "%5, %6, %7}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+      : "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -240,9 +250,11 @@ EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// 2D bf16 tensor [rows][cols] (cols contiguous), box {box_cols, box_rows}, 128-byte swizzle. On failure the map
-// is zeroed and tmap_error() set: the caller must not launch with it (TC_MAPS_OK below).
-CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+// 2D tensor [rows][cols] (cols contiguous) of esize-byte elements, box {box_cols, box_rows}, 128-byte swizzle (or swz). On
+// failure the map is zeroed and tmap_error() set: the caller must not launch with it (TC_MAPS_OK below).
+CUtensorMap make_map_typed(const void* base, CUtensorMapDataType dt, uint32_t esize, uint64_t rows, uint64_t cols,
+                           uint32_t box_cols, uint32_t box_rows,
+                           CUtensorMapSwizzle swz = CU_TENSOR_MAP_SWIZZLE_128B) {
   CUtensorMap m;
   std::memset(&m, 0, sizeof(m));
   EncodeTiledFn fn = encode_fn();
@@ -251,17 +263,20 @@ CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t bo
     return m;
   }
   cuuint64_t dims[2] = {cols, rows};
-  cuuint64_t strides[1] = {cols * 2};
+  cuuint64_t strides[1] = {cols * esize};
   cuuint32_t box[2] = {box_cols, box_rows};
   cuuint32_t es[2] = {1, 1};
-  CUresult r = fn(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = fn(&m, dt, 2, const_cast<void*>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     tmap_error() = (int)r;
     std::memset(&m, 0, sizeof(m));
   }
   return m;
+}
+// the bf16 (16-bit) operand maps
+CUtensorMap make_map(const void* base, uint64_t rows, uint64_t cols, uint32_t box_cols, uint32_t box_rows) {
+  return make_map_typed(base, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, rows, cols, box_cols, box_rows);
 }
 // in a launcher, after its make_map calls: skip the launch when an encode failed
 #define TC_MAPS_OK() \

@@ -291,6 +291,17 @@ def test_alternative_kernels_at_the_per_rank_shape(variant, monkeypatch):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
+def test_tma_gather4_variant_of_the_fused_gather(monkeypatch):
+    """PFC_LG_G4=1: the fused gather + logits kernel (M <= 256) fetching the sampled W rows with TMA tile::gather4
+    instead of cp.async (measured slower) stays correct; two train steps against the oracle, with
+    k not a multiple of 128 (rows past k_i gather row 0 and are zeroed)."""
+    monkeypatch.setenv("PFC_LG_G4", "1")
+    case = (60001, 512, 256, 0.1, "arcface", 0.5, "trained", 0.055)
+    for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
+        check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
+        assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
+
+
 @pytest.mark.parametrize("B,fused", [(96, True), (640, True), (96, False)], ids=["fused-M96", "pair-M640", "fb+step"])
 def test_host_resident_params_match_device(B, fused):
     """SURVEY.md §8(f) f4 (capacity mode): W and V in page-locked, device-mapped host memory run the same kernels
