@@ -63,6 +63,8 @@ struct DwxParams {
   int* err;
   float s;              // logit scale
   int pfnow;            // prefetch the current tile's W / V rows at its start (as well as the next tile's)
+  int pf;               // PFC_DWX_PF: 1 (default) the next tile's W / V rows into L2 during this tile's update; 0 none;
+                        // 2 two tiles ahead; 3 the next tile's at this tile's start
   uint64_t* trace;      // PFC_DWX_TRACE=1 (eager launches): per-tile epilogue timestamps, [cta][tile][8]
   int trace_tiles;
 };
@@ -306,6 +308,15 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
           if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
         }
+        if (p.pf == 3 && nx_j >= 0) {   // the next tile's rows into L2 now, a whole tile ahead
+          const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
+          const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          }
+        }
       }
       // (2) D1 -> smem staging (XOR-swizzled float4 rows), TMEM released
       mbar_wait(&d1_full[acc], aph);
@@ -414,9 +425,14 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           }
         }
         if (tr) tr[5 + r0 / 8] = gtimer_dx();
-        if (r0 == 0 && eset == 0 && nx_j >= 0) {   // the next tile's W / V row segments into L2
-          const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
-          const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
+        int32_t pj = (p.pf == 1) ? nx_j : -1;
+        if (p.pf == 2 && r0 == 0 && eset == 0 && i + 2 < ntl) {   // two tiles ahead
+          const int prow = (g + (i + 2) * p.gper) * 128 + row_in;
+          if (prow < k) pj = p.sgd.idx[prow];
+        }
+        if (r0 == 0 && eset == 0 && pj >= 0) {   // the next tile's W / V row segments into L2
+          const float* wp = p.sgd.W + (int64_t)pj * p.d + n0;
+          const float* vp = p.sgd.V + (int64_t)pj * p.d + n0;
 #pragma unroll
           for (int l = 0; l < 4; ++l) {
             asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
@@ -508,6 +524,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   DwxParams p{};
   p.M = sz.M; p.d = sz.d; p.nkb = (int)(sz.M_pad / 64); p.gper = dwx_gper(sz); p.st = st; p.sgd = sa; p.ws = ws;
   p.pfnow = env_int("PFC_DWX_PFNOW", 0);
+  p.pf = env_int("PFC_DWX_PF", 1);
   if (ef) {
     p.f = ef->f; p.tcol = ef->tcol; p.dcorr = ef->dcorr; p.xch = ef->xch; p.cnt = ef->cnt; p.err = ef->err;
     p.s = ef->s;
