@@ -473,6 +473,433 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------------------------------------------------
+// k_dwx_ring (PFC_DWX_RING=1): the same per-tile work as k_dwx_t with the W / V row stream decoupled from the tile
+// pipeline. Two loader warps copy the 512-byte W and V segments of the tile's classes into a 64 KB shared ring
+// (16-byte cp.async, 8 classes per slot, up to 64 classes ahead, across tile boundaries), so the HBM reads stay in
+// flight while the epilogue waits for accumulators and radial dots. dW is computed transposed,
+//   D1^T[128 d-columns x 128 classes] = X~^T G'   (A = X~ chunk MN-major, B = G' chunk K-major),
+// so a TMEM lane is a d-column: each epilogue thread updates one column of 4 classes per slot straight from
+// tcgen05.ld (no fp32 staging tile) with 128-byte coalesced W / V stores per warp instruction.
+//   warp 0 TMA producer, warp 1 MMA issuer (as k_dwx_t), warps 2-9 epilogue, warps 10-11 ring loaders,
+//   warps 12-13 (E-form) radial-dot partials (as k_dwx_t)
+constexpr int RG_SLOTS = 8;
+constexpr int RG_SLOT = 8 * 1024;                   // 8 classes x (W 512 B + V 512 B)
+constexpr int RG_OFF_RING = OFF_WB + 2 * WB_HALF;
+constexpr int RG_OFF_AUX = RG_OFF_RING + RG_SLOTS * RG_SLOT;
+constexpr int RG_SMEM = RG_OFF_AUX + 256 + 3 * 128 * 4 + 1024;
+static_assert(RG_SMEM <= 232448, "shared memory overflow");
+constexpr int RG_LOAD_WARP0 = 2 + DX_EPI;
+constexpr int RG_DOT_WARP0 = RG_LOAD_WARP0 + 2;
+constexpr int RG_THREADS = 32 * RG_DOT_WARP0;
+constexpr int RG_THREADS_EF = RG_THREADS + 32 * DX_DOTW;
+
+__device__ __forceinline__ void st_hint1(float* a, float v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+
+template <bool HINT, bool EF>
+__global__ void __launch_bounds__(EF ? RG_THREADS_EF : RG_THREADS, 1)
+    k_dwx_ring(const __grid_constant__ CUtensorMap tmG, const __grid_constant__ CUtensorMap tmX, DwxParams p) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* sR = smem + OFF_R;
+  uint8_t* sG = smem + OFF_G;
+  uint8_t* sWb = smem + OFF_WB;
+  float* ring = reinterpret_cast<float*>(smem + RG_OFF_RING);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + RG_OFF_AUX);
+  uint64_t* g_full = bars;
+  uint64_t* g_empty = bars + 1;
+  uint64_t* x_full = bars + 2;        // [R_STAGES]
+  uint64_t* x_empty = bars + 4;       // [R_STAGES]
+  uint64_t* d1_full = bars + 6;       // [2]
+  uint64_t* d1_empty = bars + 8;      // [2]
+  uint64_t* wb_full = bars + 10;
+  uint64_t* wb_empty = bars + 11;
+  uint64_t* d2_full = bars + 12;
+  uint64_t* r_full = bars + 13;       // [RG_SLOTS]
+  uint64_t* r_empty = bars + 13 + RG_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 13 + 2 * RG_SLOTS);
+  int32_t* s_rowj = reinterpret_cast<int32_t*>(smem + RG_OFF_AUX + 256);
+  float* s_inv = reinterpret_cast<float*>(s_rowj + 128);
+  float* s_rad = s_inv + 128;
+  static_assert(R_STAGES == 2, "barrier layout");
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = p.st->k;
+  const int nct = (k + 127) / 128;
+  const int g = blockIdx.x % p.gper;
+  const int n0 = (blockIdx.x / p.gper) * 128;
+  const int ntl = g < nct ? (nct - g + p.gper - 1) / p.gper : 0;
+  const int nkb = p.nkb, nh = p.nkb / 2 > 0 ? p.nkb / 2 : 1;
+
+  if (threadIdx.x == 0) {
+    mbar_init(g_full, 1); mbar_init(g_empty, 1);
+    for (int i = 0; i < R_STAGES; ++i) { mbar_init(&x_full[i], 1); mbar_init(&x_empty[i], EF ? 1 + DX_DOTW : 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(&d1_full[i], 1); mbar_init(&d1_empty[i], DX_EPI); }
+    mbar_init(wb_full, DX_EPI);
+    mbar_init(wb_empty, 1);
+    mbar_init(d2_full, 1);
+    for (int i = 0; i < RG_SLOTS; ++i) { mbar_init(&r_full[i], 64); mbar_init(&r_empty[i], DX_EPI); }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    fence_proxy_async_smem();
+  }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmG); tma_prefetch(&tmX); }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(512));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;     // cols [0, 256): D1^T x 2; [256, 512): D2 halves
+
+  if (warp == 0) {
+    // ---------------------------------------------------------------- producer (as k_dwx_t)
+    if (lane == 0) {
+      int xs = 0;
+      uint32_t xph = 0;
+      auto load_gdx = [&](int i) {
+        mbar_wait(g_empty, (uint32_t)((i & 1) ^ 1));
+        mbar_expect_tx(g_full, (uint32_t)(nkb * G_CHUNK));
+        for (int kb = 0; kb < nkb; ++kb) tma_load_2d(sG + kb * G_CHUNK, &tmG, g_full, kb * 64, (g + i * p.gper) * 128);
+      };
+      for (int i = 0; i < ntl; ++i) {
+        const int ct = g + i * p.gper;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&x_empty[xs], xph ^ 1);
+          mbar_expect_tx(&x_full[xs], (uint32_t)R_STAGE);
+          uint8_t* st = sR + xs * R_STAGE;
+          tma_load_2d(st, &tmG, &x_full[xs], kb * 64, ct * 128);
+          tma_load_2d(st + G_CHUNK, &tmX, &x_full[xs], n0, kb * 64);
+          tma_load_2d(st + G_CHUNK + X_CHUNK / 2, &tmX, &x_full[xs], n0 + 64, kb * 64);
+          if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
+        }
+        if (i > 0) load_gdx(i - 1);
+      }
+      if (ntl > 0) load_gdx(ntl - 1);
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------------- MMA issuer
+    constexpr uint32_t IDESC_DWT = make_idesc(128, 128, true, false);   // A = X~ (MN-major), B = G' (K-major)
+    constexpr uint32_t IDESC_DX = make_idesc(128, 128, true, true);
+    int xs = 0, acc = 0;
+    uint32_t xph = 0, aph = 0;
+    auto dx = [&](int i) {
+      mbar_wait(wb_full, (uint32_t)(i & 1));
+      mbar_wait(g_full, (uint32_t)(i & 1));
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t ga = smem_u32(sG), wa = smem_u32(sWb);
+        for (int h = 0; h < nh; ++h)
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks)
+            tc_mma(tmem_base + 256 + h * 128, make_desc(ga + 2 * h * G_CHUNK + ks * 2048, G_CHUNK, 1024),
+                   make_desc(wa + ks * 2048, WB_HALF, 1024), IDESC_DX, (i > 0 || ks > 0) ? 1u : 0u);
+        tc_commit(g_empty);
+        tc_commit(wb_empty);
+      }
+      __syncwarp();
+    };
+    for (int i = 0; i < ntl; ++i) {
+      mbar_wait(&d1_empty[acc], aph ^ 1);
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        mbar_wait(&x_full[xs], xph);
+        tc_fence_after();
+        if (lane == 0) {
+          const uint32_t ga = smem_u32(sR + xs * R_STAGE), xa = ga + G_CHUNK;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            tc_mma(tmem_base + acc * 128, make_desc(xa + kk * 2048, X_CHUNK / 2, 1024), make_desc(ga + kk * 32, 16, 1024),
+                   IDESC_DWT, (kb > 0 || kk > 0) ? 1u : 0u);
+          tc_commit(&x_empty[xs]);
+        }
+        __syncwarp();
+        if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
+      }
+      if (lane == 0) tc_commit(&d1_full[acc]);
+      __syncwarp();
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+      if (i > 0) dx(i - 1);
+    }
+    if (ntl > 0) dx(ntl - 1);
+    if (lane == 0) {
+      if (ntl > 0) tc_commit(d2_full);
+      else mbar_arrive(d2_full);
+    }
+    __syncwarp();
+  } else if (warp >= RG_DOT_WARP0) {
+    // ---------------------------------------------------------------- E-form radial-dot partials (as k_dwx_t)
+    if (EF) {
+      constexpr int RPT = 128 / (32 * DX_DOTW);
+      const int t = threadIdx.x - 32 * RG_DOT_WARP0;
+      const int n_dt = p.d / 128, dt = blockIdx.x / p.gper;
+      const float kc = 0.69314718f / p.s;
+      int xs = 0;
+      uint32_t xph = 0;
+      for (int i = 0; i < ntl; ++i) {
+        const int ct = g + i * p.gper;
+        float B[RPT];
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) B[q] = 0.f;
+        for (int kb = 0; kb < nkb; ++kb) {
+          mbar_wait(&x_full[xs], xph);
+          if (kb % n_dt == dt) {
+            const uint8_t* ga = sR + xs * R_STAGE;
+            const float4* f4 = reinterpret_cast<const float4*>(p.f + kb * 64);
+#pragma unroll 2
+            for (int u = 0; u < 8; ++u) {
+              const float4 fa = __ldg(f4 + 2 * u), fb = __ldg(f4 + 2 * u + 1);
+              const float fv[8] = {fa.x, fa.y, fa.z, fa.w, fb.x, fb.y, fb.z, fb.w};
+#pragma unroll
+              for (int q = 0; q < RPT; ++q) {
+                const int row = t + q * 32 * DX_DOTW;
+                const uint4 qv = *reinterpret_cast<const uint4*>(ga + row * 128 + ((u ^ (row & 7)) << 4));
+                const uint32_t r[4] = {qv.x, qv.y, qv.z, qv.w};
+#pragma unroll
+                for (int e2 = 0; e2 < 4; ++e2) {
+                  const float el = fmaxf(__uint_as_float(r[e2] << 16), 1e-37f);
+                  const float eh = fmaxf(__uint_as_float(r[e2] & 0xFFFF0000u), 1e-37f);
+                  float ll, lh;
+                  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(ll) : "f"(el));
+                  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(lh) : "f"(eh));
+                  B[q] = fmaf(el * fv[2 * e2], ll, fmaf(eh * fv[2 * e2 + 1], lh, B[q]));
+                }
+              }
+            }
+          }
+          __syncwarp();
+          if ((t & 31) == 0) mbar_arrive(&x_empty[xs]);
+          if (++xs == R_STAGES) { xs = 0; xph ^= 1; }
+        }
+        float* dst = p.xch + ((int64_t)ct * n_dt + dt) * 128;
+#pragma unroll
+        for (int q = 0; q < RPT; ++q) dst[t + q * 32 * DX_DOTW] = kc * B[q];
+        if (DX_DOTW > 1) asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
+        else __syncwarp();
+        if (t == 0) asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(p.cnt + ct) : "memory");
+      }
+    }
+  } else if (warp >= RG_LOAD_WARP0) {
+    // ---------------------------------------------------------------- ring loaders (64 threads)
+    // thread t copies 16-byte chunk t of each class's 1 KB (W segment: t < 32, V segment: t >= 32), 8 classes per
+    // slot; the row ids come from idx (8 broadcast loads per slot); rows past k_i are not copied
+    const int t = threadIdx.x - 32 * RG_LOAD_WARP0;
+    (void)k;
+    const float* base = t < 32 ? p.sgd.W : p.sgd.V;
+    const int coff = 4 * (t & 31);
+    const uint32_t doff = (uint32_t)((t < 32 ? 0 : 512) + 16 * (t & 31));
+    const uint64_t pol = HINT ? policy_evict_first() : 0;
+    int rs = 0;
+    uint32_t rph = 0;
+    // the tile's 128 row ids in registers (lane l: classes l, l + 32, l + 64, l + 96), the next tile's loaded a
+    // tile ahead; each slot's 8 ids are shuffled out of them
+    auto ids = [&](int i, int32_t (&r)[4]) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int prow = (g + i * p.gper) * 128 + 32 * q + lane;
+        r[q] = (i < ntl && prow < k) ? __ldg(p.sgd.idx + prow) : -1;
+      }
+    };
+    int32_t cur[4], nxt[4];
+    ids(0, nxt);
+    for (int i = 0; i < ntl; ++i) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cur[q] = nxt[q];
+      ids(i + 1, nxt);
+      for (int grp = 0; grp < 16; ++grp) {
+        // slot grp holds classes 4 grp .. 4 grp + 3 (positions 0-3) and 64 + 4 grp .. (positions 4-7): each
+        // epilogue class set walks 64 contiguous TMEM columns
+        const int32_t lo = (grp >> 3) == 0 ? cur[0] : cur[1];
+        const int32_t hi = (grp >> 3) == 0 ? cur[2] : cur[3];
+        int32_t jj[8];
+#pragma unroll
+        for (int cl = 0; cl < 8; ++cl) jj[cl] = __shfl_sync(0xffffffffu, cl < 4 ? lo : hi, ((grp & 7) << 2) + (cl & 3));
+        mbar_wait(&r_empty[rs], rph ^ 1);
+        const uint32_t dst = smem_u32(ring) + rs * RG_SLOT + doff;
+#pragma unroll
+        for (int cl = 0; cl < 8; ++cl)
+          if (jj[cl] >= 0) {
+            const float* src = base + (int64_t)jj[cl] * p.d + n0 + coff;
+            if (HINT)
+              asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(dst + cl * 1024),
+                           "l"(src), "l"(pol)
+                           : "memory");
+            else
+              asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst + cl * 1024), "l"(src) : "memory");
+          }
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(&r_full[rs])) : "memory");
+        if (++rs == RG_SLOTS) { rs = 0; rph ^= 1; }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+  } else {
+    // ---------------------------------------------------------------- epilogue (thread = d-column of a quarter)
+    const int ew = warp - 2;
+    const int lg = warp & 3;
+    const int row_in = lg * 32 + lane;       // this thread's d-column in the tile (its TMEM lane); also a class row
+                                             // for the per-tile scalars
+    const int eset = ew >> 2;                // classes 4 eset .. 4 eset + 3 of every 8-class slot
+    const float lr = *p.sgd.lr;
+    const uint64_t pol = HINT ? policy_evict_first() : 0;
+    int32_t nx_j = -1;
+    float nx_inv = 0.f, nx_rad = 0.f;
+    if (eset == 0 && ntl > 0) {
+      const int prow = g * 128 + row_in;
+      if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
+    }
+    int acc = 0, rs = 0;
+    uint32_t aph = 0, rph = 0;
+    const int half = row_in >> 6, xi = row_in & 63;
+    for (int i = 0; i < ntl; ++i) {
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile's scalars consumed
+      uint64_t* tr = (p.trace && threadIdx.x == 64 && i < p.trace_tiles)
+                         ? p.trace + ((int64_t)blockIdx.x * p.trace_tiles + i) * 8 : nullptr;
+      if (tr) tr[0] = gtimer_dx();
+      if (eset == 0) {
+        s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
+        nx_j = -1; nx_inv = 0.f; nx_rad = 0.f;
+        if (i + 1 < ntl) {
+          const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
+          if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
+        }
+      }
+      float rad16 = 0.f;
+      float radp[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      if (EF) {   // radial dots of classes ew * 16 + l (l < 16): dcorr + the n_dt d-tile partials
+        const int ct = g + i * p.gper, n_dt = p.d / 128;
+        if (lane == 0) {
+          const int* c = p.cnt + ct;
+          int v, spins = 0;
+          do {
+            asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(c) : "memory");
+          } while (v < n_dt && ++spins < (1 << 26));
+          if (v < n_dt) atomicOr(p.err, ERR_INTERNAL);
+        }
+        __syncwarp();
+        if (lane < 16) {
+          const int row = ew * 16 + lane;
+          rad16 = __ldcg(p.dcorr + ct * 128 + row);
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < n_dt) radp[q] = __ldcg(p.xch + ((int64_t)ct * n_dt + q) * 128 + row);
+        }
+#pragma unroll
+        for (int q = 0; q < 8; ++q) rad16 += radp[q];
+      }
+      asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // s_rowj / s_inv / s_rad of this tile
+      if (EF) {
+        if (lane < 16) s_rad[ew * 16 + lane] = rad16;
+        asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");
+      }
+      if (tr) tr[1] = gtimer_dx();
+      mbar_wait(&d1_full[acc], aph);
+      tc_fence_after();
+      if (tr) tr[2] = gtimer_dx();
+      mbar_wait(wb_empty, (uint32_t)((i & 1) ^ 1));   // dX(t - 1) has read the previous bf16 w_old tile
+      if (tr) tr[3] = gtimer_dx();
+      const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 128 + 64 * eset;
+      uint64_t rwait = 0;
+#pragma unroll 1
+      for (int gh = 0; gh < 2; ++gh) {
+      uint32_t dv[32];   // dW^T of this thread's column for classes 64 eset + 32 gh + 0..31
+      tmem_ld32(tacc + 32 * gh, dv);
+#pragma unroll
+      for (int g8 = 0; g8 < 8; ++g8) {
+        const int grp = gh * 8 + g8;
+        const uint64_t tw0 = tr ? gtimer_dx() : 0;
+        mbar_wait(&r_full[rs], rph);
+        if (tr) rwait += gtimer_dx() - tw0;
+        float* sl = ring + rs * (RG_SLOT / 4);
+        // (a) column-wise update of this warp's 4 classes, written back into the slot in place
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int cl = 4 * eset + u, c = 64 * eset + 4 * grp + u;
+          const int32_t j = s_rowj[c];
+          const float wo = sl[cl * 256 + row_in];
+          const float mo = sl[cl * 256 + 128 + row_in];
+          const float ws = EF ? s_inv[c] : 1.f;
+          const __nv_bfloat16 wb = __float2bfloat16_rn(j >= 0 ? wo * ws : 0.f);
+          *reinterpret_cast<__nv_bfloat16*>(sWb + half * WB_HALF + c * 128 + ((((xi >> 3) ^ (c & 7)) << 4) | ((xi & 7) << 1))) = wb;
+          if (j >= 0) {
+            const float inv = s_inv[c];
+            const float rad = s_rad[c] * inv;
+            const float oi = p.sgd.gsc ? 1.f : inv;
+            const float m = p.sgd.mu * mo + (__uint_as_float(dv[4 * g8 + u]) - wo * rad) * oi + p.sgd.lambda * wo;
+            sl[cl * 256 + row_in] = wo - lr * m;
+            sl[cl * 256 + 128 + row_in] = m;
+          }
+        }
+        // (b) the 4 warps of this class set (one per column quarter) done: warp lg stores class 4 eset + lg's W and V
+        // segments row-wise (512-byte coalesced float4 stores)
+        asm volatile("bar.sync %0, 128;" ::"r"(6 + eset) : "memory");
+        {
+          const int cl = 4 * eset + lg, c = 64 * eset + 4 * grp + lg;
+          const int32_t j = s_rowj[c];
+          if (j >= 0) {
+            const float4 w4 = reinterpret_cast<const float4*>(sl + cl * 256)[lane];
+            const float4 m4 = reinterpret_cast<const float4*>(sl + cl * 256 + 128)[lane];
+            float* wp = p.sgd.W + (int64_t)j * p.d + n0 + 4 * lane;
+            float* vp = p.sgd.V + (int64_t)j * p.d + n0 + 4 * lane;
+            if (HINT) { st_hint4(vp, m4, pol); st_hint4(wp, w4, pol); }
+            else { *reinterpret_cast<float4*>(vp) = m4; *reinterpret_cast<float4*>(wp) = w4; }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&r_empty[rs]);
+        if (++rs == RG_SLOTS) { rs = 0; rph ^= 1; }
+        if (tr && grp == 7) tr[4] = gtimer_dx();
+        if (grp == 0 && eset == 0 && nx_j >= 0 && p.pf) {   // the next tile's rows into L2 (the ring reads them)
+          const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
+          const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
+#pragma unroll
+          for (int l = 0; l < 4; ++l) {
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          }
+        }
+      }
+      }
+      if (tr) { tr[5] = gtimer_dx(); tr[6] = tr[5] - rwait; }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&d1_empty[acc]);
+      if (++acc == 2) { acc = 0; aph ^= 1; }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(wb_full);
+    }
+    // dX_hat partial of this CTA -> split workspace (as k_dwx_t)
+    mbar_wait(d2_full, 0);
+    tc_fence_after();
+    if (eset < nh) {
+      const int row = eset * 128 + row_in;
+      float* dst = p.ws + ((int64_t)g * p.M + row) * p.d + n0;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(lg * 32) << 16) + 256 + eset * 128 + c * 32, v);
+        if (ntl == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j) v[j] = 0u;
+        }
+        if (row < p.M) {
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            reinterpret_cast<uint4*>(dst + c * 32)[q] = make_uint4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+        }
+      }
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base), "r"(512));
+  }
+}
+
 // dX_hat = sum of the split partials (fixed order); E-form: times f_n per batch row (dX_hat_n = f_n sum_j E'_nj w_hat_j)
 // P.n > 0 (fused reduce-scatter): each row goes straight into its owner's xdx slot `rank`
 __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
@@ -508,10 +935,19 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   // W / V streamed with an L2 evict-first policy so that the G' tile re-read for dX stays resident (-0.1 to -0.2 GB
   // of DRAM reads per step at C4); PFC_DWX_HINT=0 disables
   const bool hint = env_int("PFC_DWX_HINT", 1) != 0;
-  auto kern = ef ? (hint ? k_dwx_t<true, true> : k_dwx_t<false, true>)
-                 : (hint ? k_dwx_t<true, false> : k_dwx_t<false, false>);
+  const bool ringk = env_int("PFC_DWX_RING", 0) != 0;
+  auto kern = ringk ? (ef ? (hint ? k_dwx_ring<true, true> : k_dwx_ring<false, true>)
+                          : (hint ? k_dwx_ring<true, false> : k_dwx_ring<false, false>))
+                    : (ef ? (hint ? k_dwx_t<true, true> : k_dwx_t<false, true>)
+                          : (hint ? k_dwx_t<true, false> : k_dwx_t<false, false>));
+  const int nthreads = ringk ? (ef ? RG_THREADS_EF : RG_THREADS) : (ef ? DX_THREADS_EF : DX_THREADS);
+  const int smem_bytes = ringk ? RG_SMEM : DX_SMEM;
   static bool attr = false;
   if (!attr) {
+    cudaFuncSetAttribute(k_dwx_ring<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_SMEM);
+    cudaFuncSetAttribute(k_dwx_ring<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_SMEM);
+    cudaFuncSetAttribute(k_dwx_ring<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_SMEM);
+    cudaFuncSetAttribute(k_dwx_ring<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, RG_SMEM);
     cudaFuncSetAttribute(k_dwx_t<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
     cudaFuncSetAttribute(k_dwx_t<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
     cudaFuncSetAttribute(k_dwx_t<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, DX_SMEM);
@@ -549,8 +985,8 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     // (cudaErrorCooperativeLaunchTooLarge, reported by the step) instead of spinning on a CTA that never runs
     cudaLaunchConfig_t lc{};
     lc.gridDim = dim3(grid);
-    lc.blockDim = dim3(DX_THREADS_EF);
-    lc.dynamicSmemBytes = DX_SMEM;
+    lc.blockDim = dim3(nthreads);
+    lc.dynamicSmemBytes = smem_bytes;
     lc.stream = s;
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeCooperative;
@@ -559,7 +995,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
     lc.numAttrs = 1;
     cudaLaunchKernelEx(&lc, kern, tg, tx, p);
   } else {
-    kern<<<grid, DX_THREADS, DX_SMEM, s>>>(tg, tx, p);
+    kern<<<grid, nthreads, smem_bytes, s>>>(tg, tx, p);
   }
   if (p.trace) {
     std::vector<uint64_t> h((size_t)grid * ttiles * 8);

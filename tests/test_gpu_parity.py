@@ -291,11 +291,14 @@ def test_alternative_kernels_at_the_per_rank_shape(variant, monkeypatch):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
-def test_tma_gather4_variant_of_the_fused_gather(monkeypatch):
-    """PFC_LG_G4=1: the fused gather + logits kernel (M <= 256) fetching the sampled W rows with TMA tile::gather4
-    instead of cp.async (measured slower) stays correct; two train steps against the oracle, with
-    k not a multiple of 128 (rows past k_i gather row 0 and are zeroed)."""
-    monkeypatch.setenv("PFC_LG_G4", "1")
+@pytest.mark.parametrize("variant", ["PFC_LG_G4=1", "PFC_DWX_RING=1", "PFC_DWX_PF=0", "PFC_DWX_PF=3"])
+def test_alternative_kernels_at_m256(variant, monkeypatch):
+    """The non-default kernels of the M <= 256 path kept for A/B timing stay correct: the fused gather
+    fetching the W rows with TMA tile::gather4, the dW + SGD + dX kernel with the shared-memory W/V ring and the
+    transposed dW, the prefetch-timing variants; two train steps against the oracle, k not a multiple of 128 (rows
+    past k_i are gathered / loaded as padding and must not be updated)."""
+    k, v = variant.split("=")
+    monkeypatch.setenv(k, v)
     case = (60001, 512, 256, 0.1, "arcface", 0.5, "trained", 0.055)
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", fused=True):
         check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
