@@ -188,6 +188,16 @@ pfc_status pfc_forward_backward_host(pfc_ctx* ctx, const float* x_host, const in
 pfc_status pfc_train_step_host(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host, float* grad_x_host,
                                float* loss_host, float lr, void* stream);
 
+/* The two host-buffer entries WITHOUT the final synchronisation: the copies and the step are enqueued on
+ * `stream` and the call returns, so a training loop keeps the GPU fed (the next step is enqueued while this one
+ * runs). The host buffers must be page-locked (pinned); x_host / labels_host must stay unmodified and
+ * grad_x_host / loss_host are valid only after `stream` completes (cudaStreamSynchronize, or pfc_check).
+ * Device-detected errors of the step are reported by the next call, as for pfc_train_step. */
+pfc_status pfc_forward_backward_host_async(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host,
+                                           float* grad_x_host, float* loss_host, void* stream);
+pfc_status pfc_train_step_host_async(pfc_ctx* ctx, const float* x_host, const int64_t* labels_host,
+                                     float* grad_x_host, float* loss_host, float lr, void* stream);
+
 /* Lazy momentum-SGD update of the rows sampled by the last pfc_forward_backward (DESIGN.md
  * R15): g = (dw_hat - w_hat (w_hat . dw_hat)) / ||w||; v <- mu v + g + lambda w; w <- w - lr v.
  * Rows not sampled are untouched. Returns PFC_ERR_CONTRACT if no forward_backward preceded it or it was

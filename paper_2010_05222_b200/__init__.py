@@ -33,6 +33,7 @@ EXPORTS = ["pfc_get_unique_id", "pfc_init", "pfc_destroy", "pfc_last_error", "pf
            "pfc_get_sampled", "pfc_get_sampled_grad", "pfc_get_lse", "pfc_get_step", "pfc_set_step", "pfc_check",
            "pfc_launch_count", "pfc_path_flags", "pfc_get_state", "pfc_set_state", "pfc_version", "pfc_group_forward_backward", "pfc_sample_shard",
            "pfc_profile_enable", "pfc_profile_read", "pfc_profile_section", "pfc_train_step", "pfc_train_step_host",
+           "pfc_train_step_host_async", "pfc_forward_backward_host_async",
            "pfc_group_train_step", "pfc_get_metrics"]
 PROF_SECTIONS = 10
 
@@ -95,6 +96,8 @@ def load_library(path=LIB_PATH):
         "pfc_train_step": (st, [VP, VP, VP, VP, VP, F, VP]),
         "pfc_get_metrics": (st, [VP, P(F), P(F)]),
         "pfc_train_step_host": (st, [VP, VP, VP, VP, VP, F, VP]),
+        "pfc_train_step_host_async": (st, [VP, VP, VP, VP, VP, F, VP]),
+        "pfc_forward_backward_host_async": (st, [VP, VP, VP, VP, VP, VP]),
         "pfc_group_train_step": (st, [P(VP), ctypes.c_int32, P(VP), P(VP), P(VP), VP, F, VP]),
         "pfc_profile_enable": (st, [VP, ctypes.c_int32]),
         "pfc_profile_read": (st, [VP, P(ctypes.c_double), P(I64)]),
@@ -204,20 +207,21 @@ class PartialFC:
         self._check(self._lib.pfc_forward_backward(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss),
                                                    self._stream(stream)))
 
-    def forward_backward_host(self, x, labels, grad_x, loss=None, stream=None):
-        """Same with host (ideally pinned) CPU tensors; copies are inside the call; synchronises."""
-        self._check(self._lib.pfc_forward_backward_host(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss),
-                                                        self._stream(stream)))
+    def forward_backward_host(self, x, labels, grad_x, loss=None, stream=None, sync=True):
+        """Same with host (ideally pinned) CPU tensors; copies are inside the call; synchronises unless sync=False."""
+        fn = self._lib.pfc_forward_backward_host if sync else self._lib.pfc_forward_backward_host_async
+        self._check(fn(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), self._stream(stream)))
 
     def train_step(self, x, labels, grad_x, loss=None, lr=0.1, stream=None):
         """forward_backward + step(lr) fused (the SGD update runs in the dW contraction's epilogue)."""
         self._check(self._lib.pfc_train_step(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), float(lr),
                                              self._stream(stream)))
 
-    def train_step_host(self, x, labels, grad_x, loss=None, lr=0.1, stream=None):
-        """train_step with host (pinned) CPU tensors; copies inside the call; synchronises."""
-        self._check(self._lib.pfc_train_step_host(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), float(lr),
-                                                  self._stream(stream)))
+    def train_step_host(self, x, labels, grad_x, loss=None, lr=0.1, stream=None, sync=True):
+        """train_step with host (pinned) CPU tensors; copies inside the call; synchronises unless sync=False
+        (pfc_train_step_host_async: grad_x / loss valid once the stream completes)."""
+        fn = self._lib.pfc_train_step_host if sync else self._lib.pfc_train_step_host_async
+        self._check(fn(self._h, _ptr(x), _ptr(labels), _ptr(grad_x), _ptr(loss), float(lr), self._stream(stream)))
 
     def step(self, lr, stream=None):
         self._check(self._lib.pfc_step(self._h, float(lr), self._stream(stream)))

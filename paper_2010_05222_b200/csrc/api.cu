@@ -209,7 +209,7 @@ pfc_status wait_stream(pfc_ctx* c, cudaStream_t s) {
       c->comm = nullptr;
       return set_err(c, PFC_ERR_NCCL, m + " (communicator aborted)");
     }
-    std::this_thread::sleep_for(std::chrono::microseconds(50));
+    if (el > 2e-3) std::this_thread::sleep_for(std::chrono::microseconds(50));   // spin for the first 2 ms
   }
   ncclResult_t ar = ncclSuccess;
   ncclCommGetAsyncError(c->comm, &ar);
@@ -1015,7 +1015,7 @@ static pfc_status group_step(pfc_ctx** ctxs, int32_t n, const float* const* x, c
 }
 
 static pfc_status host_step(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
-                            float* loss_host, bool fused, float lr, void* stream) {
+                            float* loss_host, bool fused, float lr, void* stream, bool sync = true) {
   if (!c) return set_err(nullptr, PFC_ERR_CONTRACT, "ctx is NULL");
   if (!x_host || !labels_host || !grad_x_host) return set_err(c, PFC_ERR_CONTRACT, "NULL host buffer");
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -1026,7 +1026,21 @@ static pfc_status host_step(pfc_ctx* c, const float* x_host, const int64_t* labe
   if (r != PFC_OK) return r;
   CUDA_TRY(c, cudaMemcpyAsync(grad_x_host, c->gx_out, xb, cudaMemcpyDeviceToHost, s));
   if (loss_host) CUDA_TRY(c, cudaMemcpyAsync(loss_host, c->loss_dev, 4, cudaMemcpyDeviceToHost, s));
+  if (!sync) {
+    c->last_stream = s;
+    return PFC_OK;
+  }
   return wait_stream(c, s);
+}
+
+pfc_status pfc_forward_backward_host_async(pfc_ctx* c, const float* x_host, const int64_t* labels_host,
+                                           float* grad_x_host, float* loss_host, void* stream) {
+  return host_step(c, x_host, labels_host, grad_x_host, loss_host, false, 0.f, stream, false);
+}
+
+pfc_status pfc_train_step_host_async(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,
+                                     float* loss_host, float lr, void* stream) {
+  return host_step(c, x_host, labels_host, grad_x_host, loss_host, true, lr, stream, false);
 }
 
 pfc_status pfc_forward_backward_host(pfc_ctx* c, const float* x_host, const int64_t* labels_host, float* grad_x_host,

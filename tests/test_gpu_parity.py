@@ -573,6 +573,35 @@ def test_host_train_step_graph_matches_device(B):
     b.close()
 
 
+def test_host_async_entry_matches_sync_entry():
+    """pfc_train_step_host_async (no synchronisation between steps, the next step enqueued while this one runs):
+    three steps from distinct pinned input buffers, the results read after one final synchronisation, equal the
+    synchronous entry's step for step (grad_x of the last step, every loss, the parameters)."""
+    C, d, B = 30000, 256, 64
+    a = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
+    b = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=4)
+    xs = [torch.from_numpy(synth.make_features(7, i, 1, B, d)[0]).pin_memory() for i in range(3)]
+    ys = [torch.from_numpy(synth.make_labels(7, i, 1, B, C)[0]).pin_memory() for i in range(3)]
+    ga, gb = torch.empty(B, d).pin_memory(), torch.empty(B, d).pin_memory()
+    la = [torch.zeros(1).pin_memory() for _ in range(3)]
+    lb = torch.zeros(1).pin_memory()
+    s = torch.cuda.Stream()
+    for i in range(3):
+        a.train_step_host(xs[i], ys[i], ga, la[i], lr=0.05, stream=s, sync=False)
+    losses = []
+    for i in range(3):
+        b.train_step_host(xs[i], ys[i], gb, lb, lr=0.05, stream=s)
+        losses.append(lb.item())
+    s.synchronize()
+    assert [l.item() for l in la] == losses
+    assert torch.equal(ga, gb)
+    Wa, Va = a.params()
+    Wb, Vb = b.params()
+    assert torch.equal(Wa, Wb) and torch.equal(Va, Vb)
+    a.close()
+    b.close()
+
+
 def test_device_errors_are_reported():
     C, d, B = 1000, 128, 8
     layer = make_layer(C, d, B, 0.1, "arcface", 0.5, "fp32")
