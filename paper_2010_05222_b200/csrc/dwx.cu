@@ -28,6 +28,13 @@ namespace pfc {
 namespace {
 
 constexpr int DX_EPI = 8;
+#ifndef PFC_DWX_DIAG
+#define PFC_DWX_DIAG 0
+#endif
+// build-time diagnostics (PFC_BUILD_TAG=diag PFC_NVCC_EXTRA=-DPFC_DWX_DIAG=1): the per-tile epilogue trace
+// (PFC_DWX_TRACE) and the prefetch-timing variants (PFC_DWX_PF = 0 / 2 / 3) of k_dwx_t; compiled out by default,
+// where their checks cost the kernel 3-4% (measured)
+constexpr bool kDiag = PFC_DWX_DIAG != 0;
 #ifndef PFC_DX_DOTW
 #define PFC_DX_DOTW 2
 #endif
@@ -64,7 +71,7 @@ struct DwxParams {
   float s;              // logit scale
   int pfnow;            // prefetch the current tile's W / V rows at its start (as well as the next tile's)
   int pf;               // PFC_DWX_PF: 1 (default) the next tile's W / V rows into L2 during this tile's update; 0 none;
-                        // 2 two tiles ahead; 3 the next tile's at this tile's start
+                        // 2 two tiles ahead; 3 the next tile's at this tile's start (k_dwx_t: diagnostic builds)
   uint64_t* trace;      // PFC_DWX_TRACE=1 (eager launches): per-tile epilogue timestamps, [cta][tile][8]
   int trace_tiles;
 };
@@ -262,7 +269,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
         for (int q = 0; q < RPT; ++q) dst[t + q * 32 * DX_DOTW] = kc * B[q];
         if (DX_DOTW > 1) asm volatile("bar.sync 5, %0;" ::"n"(32 * DX_DOTW) : "memory");
         else __syncwarp();
-        if (t == 0 && p.trace && i < p.trace_tiles) p.trace[((int64_t)blockIdx.x * p.trace_tiles + i) * 8 + 7] = gtimer_dx();
+        if (kDiag && t == 0 && p.trace && i < p.trace_tiles) p.trace[((int64_t)blockIdx.x * p.trace_tiles + i) * 8 + 7] = gtimer_dx();
         if (t == 0) {
           // release (cumulative over the barrier above): the partials are visible at gpu scope before the count
           // (the epilogues poll it with acquire loads)
@@ -289,7 +296,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
     const int col = n0 + lane * 4;           // row-update mapping: one 512-byte row segment per warp instruction
     for (int i = 0; i < ntl; ++i) {
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile fully consumed
-      uint64_t* tr = (p.trace && threadIdx.x == 64 && i < p.trace_tiles)
+      uint64_t* tr = (kDiag && p.trace && threadIdx.x == 64 && i < p.trace_tiles)
                          ? p.trace + ((int64_t)blockIdx.x * p.trace_tiles + i) * 8 : nullptr;
       if (tr) tr[0] = gtimer_dx();
       if (eset == 0) {
@@ -308,7 +315,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           const int prow = (g + (i + 1) * p.gper) * 128 + row_in;
           if (prow < k) { nx_j = p.sgd.idx[prow]; nx_inv = p.sgd.inv_norm[prow]; nx_rad = EF ? 0.f : p.sgd.dotw[prow]; }
         }
-        if (p.pf == 3 && nx_j >= 0) {   // the next tile's rows into L2 now, a whole tile ahead
+        if (kDiag && p.pf == 3 && nx_j >= 0) {   // the next tile's rows into L2 now, a whole tile ahead
           const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
           const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
 #pragma unroll
@@ -425,8 +432,8 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
           }
         }
         if (tr) tr[5 + r0 / 8] = gtimer_dx();
-        int32_t pj = (p.pf == 1) ? nx_j : -1;
-        if (p.pf == 2 && r0 == 0 && eset == 0 && i + 2 < ntl) {   // two tiles ahead
+        int32_t pj = (!kDiag || p.pf == 1) ? nx_j : -1;
+        if (kDiag && p.pf == 2 && r0 == 0 && eset == 0 && i + 2 < ntl) {   // two tiles ahead
           const int prow = (g + (i + 2) * p.gper) * 128 + row_in;
           if (prow < k) pj = p.sgd.idx[prow];
         }
@@ -755,7 +762,7 @@ __global__ void __launch_bounds__(EF ? RG_THREADS_EF : RG_THREADS, 1)
     const int half = row_in >> 6, xi = row_in & 63;
     for (int i = 0; i < ntl; ++i) {
       asm volatile("bar.sync 3, %0;" ::"n"(32 * DX_EPI) : "memory");   // previous tile's scalars consumed
-      uint64_t* tr = (p.trace && threadIdx.x == 64 && i < p.trace_tiles)
+      uint64_t* tr = (kDiag && p.trace && threadIdx.x == 64 && i < p.trace_tiles)
                          ? p.trace + ((int64_t)blockIdx.x * p.trace_tiles + i) * 8 : nullptr;
       if (tr) tr[0] = gtimer_dx();
       if (eset == 0) {
@@ -971,7 +978,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   const int ttiles = (int)((sz.k_pad / 128 + p.gper - 1) / p.gper);
-  if (env_int("PFC_DWX_TRACE", 0) && cs == cudaStreamCaptureStatusNone) {
+  if (kDiag && env_int("PFC_DWX_TRACE", 0) && cs == cudaStreamCaptureStatusNone) {
     static size_t cap = 0;
     const size_t need = (size_t)grid * ttiles * 8 * sizeof(uint64_t);
     if (need > cap) { if (trace) cudaFree(trace); cudaMalloc(&trace, need); cap = need; }

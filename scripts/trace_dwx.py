@@ -1,4 +1,5 @@
-"""Summarise a k_dwx_t per-tile epilogue trace (PFC_DWX_TRACE=1, PFC_DWX_TRACE_FILE): median phase lengths (us)."""
+"""Summarise a k_dwx_t per-tile epilogue trace: median phase lengths (us). The trace needs the diagnostic build
+(PFC_BUILD_TAG=diag PFC_NVCC_EXTRA=-DPFC_DWX_DIAG=1) run with PFC_LIB=.../libpfc-diag.so PFC_DWX_TRACE=1 PFC_DWX_TRACE_FILE=..."""
 import csv
 import statistics as st
 import sys

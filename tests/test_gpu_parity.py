@@ -291,11 +291,11 @@ def test_alternative_kernels_at_the_per_rank_shape(variant, monkeypatch):
         assert maxrel(Wn, Wnr) <= 1e-6 + 0.1 * 2e-2 * np.max(np.abs(Vnr)) / np.max(np.abs(Wnr))
 
 
-@pytest.mark.parametrize("variant", ["PFC_LG_G4=1", "PFC_DWX_RING=1", "PFC_DWX_PF=0", "PFC_DWX_PF=3"])
+@pytest.mark.parametrize("variant", ["PFC_LG_G4=1", "PFC_DWX_RING=1"])
 def test_alternative_kernels_at_m256(variant, monkeypatch):
     """The non-default kernels of the M <= 256 path kept for A/B timing stay correct: the fused gather
     fetching the W rows with TMA tile::gather4, the dW + SGD + dX kernel with the shared-memory W/V ring and the
-    transposed dW, the prefetch-timing variants; two train steps against the oracle, k not a multiple of 128 (rows
+    transposed dW; two train steps against the oracle, k not a multiple of 128 (rows
     past k_i are gathered / loaded as padding and must not be updated)."""
     k, v = variant.split("=")
     monkeypatch.setenv(k, v)
