@@ -25,6 +25,12 @@
 namespace pfc {
 namespace {
 
+#ifndef PFC_DWX_DIAG
+#define PFC_DWX_DIAG 0
+#endif
+// build-time diagnostics (PFC_BUILD_TAG=diag PFC_NVCC_EXTRA=-DPFC_DWX_DIAG=1): the per-unit trace (PFC_DW_TRACE) and
+// the non-default prefetch / hoist / E-hint variants; compiled out by default (runtime checks in the epilogue cost)
+constexpr bool kXDiag = PFC_DWX_DIAG != 0;
 constexpr int XP_BK = 64;
 constexpr int XP_STAGES = 3;
 constexpr int XP_ACC = 2;
@@ -123,7 +129,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
           mbar_wait(&empty[stage], phase ^ 1);
           if (leader) mbar_expect_tx(&full[stage], (uint32_t)(4 * XP_HALF));
           uint8_t* sa = smem + stage * XP_STAGE;
-          if (p.ehint) tma_load_2d_pair_hint(sa, &tmA, &full[stage], kb * XP_BK, c0, epol);  // E' rows: its classes
+          if (kXDiag && p.ehint) tma_load_2d_pair_hint(sa, &tmA, &full[stage], kb * XP_BK, c0, epol);  // E' rows: its classes
           else tma_load_2d_pair(sa, &tmA, &full[stage], kb * XP_BK, c0);
           tma_load_2d_pair(sa + XP_HALF, &tmB, &full[stage], d0, kb * XP_BK);             // X~: its columns
           tma_load_2d_pair(sa + XP_HALF + XP_HALF / 2, &tmB, &full[stage], d0 + 64, kb * XP_BK);
@@ -187,20 +193,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
       int32_t pf_j = -1;
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv;
-        if (p.pfnow && nx_j >= 0) {   // this unit's W / V row segments into L2 now (used ~10 us later)
+        const int pfnow = kXDiag ? p.pfnow : 1;
+        if (pfnow && nx_j >= 0) {   // this unit's W / V row segments into L2 now (used ~10 us later)
           const float* wp = p.sgd.W + (int64_t)nx_j * d + h * 256;
           const float* vp = p.sgd.V + (int64_t)nx_j * d + h * 256;
 #pragma unroll
           for (int l = 0; l < 8; ++l) {
-            if (p.pfnow == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
+            if (pfnow == 1) asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
             asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
           }
         }
         scalars(u + npairs);
-        pf_j = p.pfnow == 1 ? -1 : nx_j;
+        pf_j = pfnow == 1 ? -1 : nx_j;
       }
       const int ui = (u - pair) / npairs;
-      uint64_t* tr = (p.trace && threadIdx.x == 64 && ui < p.trace_units) ? p.trace + ((int64_t)blockIdx.x * p.trace_units + ui) * 6 : nullptr;
+      uint64_t* tr = (kXDiag && p.trace && threadIdx.x == 64 && ui < p.trace_units) ? p.trace + ((int64_t)blockIdx.x * p.trace_units + ui) * 6 : nullptr;
       if (tr) tr[0] = gtimer();
       mbar_wait(&acc_full[acc], acc_phase);
       tc_fence_after();
@@ -301,7 +308,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
           }
         }
       };
-      if (p.hoist) {
+      const bool hoist = !kXDiag || p.hoist;
+      if (hoist) {
         load(0, 0, 0);
         load(0, 1, 1);
       }
@@ -329,13 +337,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(XP_THREADS, 1)
 #pragma unroll
         for (int l = 0; l < 8; ++l) {
           asm volatile("prefetch.global.L2 [%0];" ::"l"(wp + 32 * l));
-          if (!p.pfnow) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
+          if (kXDiag && !p.pfnow) asm volatile("prefetch.global.L2 [%0];" ::"l"(vp + 32 * l));
         }
       }
       // the update, 4-row batches per 128-column quarter, the next batch's W / V loads in flight
 #pragma unroll
       for (int sh = 0; sh < 2; ++sh) {
-        if (sh == 1 || !p.hoist) {
+        if (sh == 1 || !hoist) {
           load(sh, 0, 0);
           load(sh, 1, 1);
         }
@@ -408,7 +416,7 @@ int launch_dw_sgd_pairx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_b
   lc.numAttrs = 1;
   // PFC_DW_TRACE=1: per-unit epilogue timestamps of one eager launch, written to $PFC_DW_TRACE_FILE (diagnostic)
   static uint64_t* trace = nullptr;
-  const bool tracing = env_int("PFC_DW_TRACE", 0) != 0;
+  const bool tracing = kXDiag && env_int("PFC_DW_TRACE", 0) != 0;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   const int tunits = (int)((units + pairs - 1) / pairs);

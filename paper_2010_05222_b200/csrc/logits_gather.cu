@@ -59,8 +59,6 @@ struct LgParams {
   float2* partials;        // M x n_ltiles
   int n_ltiles;
   int write_ws;            // store bf16(w) into W_s (the separate dX GEMM needs it; the fused dW/dX kernel does not)
-  int g4;                  // PFC_LG_G4=1: the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity
-                           // holds, measured 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
 };
 
 __device__ __forceinline__ uint32_t pack_f16(float a, float b) {
@@ -75,7 +73,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // EF (E-form, DESIGN.md f1): store E = bf16(e^{s c}) (c the fp16-rounded cosine the partials use) instead of the
 // fp16 cosine: the fused dW/dX kernel then consumes E directly (G = (s/M) e^{-LSE_n} E off the target entries), so
 // the softmax-gradient pass over the cosines disappears.
-template <bool EF>
+template <bool EF, bool G4>
 __global__ void __launch_bounds__(LG_THREADS, 1)
     k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs,
                     const __grid_constant__ CUtensorMap tmW, LgParams p) {
@@ -100,7 +98,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < LG_STAGES; ++i) {
-      mbar_init(&full[i], p.g4 ? 1 : 1 + 32 * LG_PROD);   // TMA expect_tx (+ one cp.async arrive per producer lane)
+      mbar_init(&full[i], G4 ? 1 : 1 + 32 * LG_PROD);   // TMA expect_tx (+ one cp.async arrive per producer lane)
       mbar_init(&conv[i], LG_CONV);
       mbar_init(&empty[i], 2);                    // MMA commit + W_s store read back
     }
@@ -113,7 +111,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     fence_proxy_async_smem();
   }
-  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmWs); if (p.g4) tma_prefetch(&tmW); }
+  if (warp == 0 && lane == 0) { tma_prefetch(&tmA); tma_prefetch(&tmWs); if (G4) tma_prefetch(&tmW); }
   if (warp == LG_MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
                  "r"(512));
@@ -124,7 +122,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  if (warp < LG_PROD && p.g4) {
+  if (G4 && warp < LG_PROD) {
     // ---------------------------------------------------------------- producer (TMA gather4 variant)
     // lane l gathers rows 4l .. 4l + 3 of the tile: two 32-column boxes (128 B per row, 128-byte swizzle) per K
     // block, the two halves 16 KB apart; rows past k_i fetch row 0 (their converter threads write zeros)
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
 #pragma unroll
           for (int q = 0; q < 16; ++q) {
             // gather4 layout: half q / 8 (16 KB apart), row r at 128 B, 16-byte chunk (q % 8) ^ (r % 8)
-            const float4 v = p.g4 ? *reinterpret_cast<const float4*>(sw + (q >> 3) * 16384 + r * 128 +
+            const float4 v = G4 ? *reinterpret_cast<const float4*>(sw + (q >> 3) * 16384 + r * 128 +
                                                                    (((q & 7) ^ (r & 7)) << 4))
                                   : src[q];
             ss = fmaf(v.x, v.x, ss); ss = fmaf(v.y, v.y, ss); ss = fmaf(v.z, v.z, ss); ss = fmaf(v.w, v.w, ss);
@@ -464,8 +462,10 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
                             MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_logits_gather<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
-    cudaFuncSetAttribute(k_logits_gather<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    cudaFuncSetAttribute(k_logits_gather<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 X_hat (R27)
@@ -479,10 +479,12 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
   p.write_ws = write_ws ? 1 : 0;
-  p.g4 = g4;
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
-  if (eform) k_logits_gather<true><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
-  else k_logits_gather<false><<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
+  // G4 (PFC_LG_G4=1): the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity holds, measured
+  // 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
+  auto kern = eform ? (g4 ? k_logits_gather<true, true> : k_logits_gather<true, false>)
+                    : (g4 ? k_logits_gather<false, true> : k_logits_gather<false, false>);
+  kern<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
   return 1;
 }
 
