@@ -301,7 +301,7 @@ __global__ void __launch_bounds__(EF ? DX_THREADS_EF : DX_THREADS, 1)
       if (tr) tr[0] = gtimer_dx();
       if (eset == 0) {
         s_rowj[row_in] = nx_j; s_inv[row_in] = nx_inv; s_rad[row_in] = nx_rad;
-        if (p.pfnow && nx_j >= 0) {   // this tile's W / V row segments into L2 (PFC_DWX_PFNOW=1)
+        if (kDiag && p.pfnow && nx_j >= 0) {   // this tile's W / V row segments into L2 (PFC_DWX_PFNOW=1, diag)
           const float* wp = p.sgd.W + (int64_t)nx_j * p.d + n0;
           const float* vp = p.sgd.V + (int64_t)nx_j * p.d + n0;
 #pragma unroll

@@ -58,7 +58,6 @@ struct LgParams {
   __half* cosv;            // class-major [k_pad][ldm]
   float2* partials;        // M x n_ltiles
   int n_ltiles;
-  int write_ws;            // store bf16(w) into W_s (the separate dX GEMM needs it; the fused dW/dX kernel does not)
 };
 
 __device__ __forceinline__ uint32_t pack_f16(float a, float b) {
@@ -73,7 +72,7 @@ __device__ __forceinline__ uint32_t pack_bf16(float a, float b) {
 // EF (E-form, DESIGN.md f1): store E = bf16(e^{s c}) (c the fp16-rounded cosine the partials use) instead of the
 // fp16 cosine: the fused dW/dX kernel then consumes E directly (G = (s/M) e^{-LSE_n} E off the target entries), so
 // the softmax-gradient pass over the cosines disappears.
-template <bool EF, bool G4>
+template <bool EF, bool G4, bool WS>
 __global__ void __launch_bounds__(LG_THREADS, 1)
     k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs,
                     const __grid_constant__ CUtensorMap tmW, LgParams p) {
@@ -240,7 +239,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
         mbar_wait(&full[stage], phase);
         uint8_t* sw = smem + stage * LG_STAGE + LG_A_BYTES;
         uint32_t pk[32], pb[32];
-        const bool wb = p.write_ws;
+        constexpr bool wb = WS;
         if (valid) {
           const float4* src = reinterpret_cast<const float4*>(sw + r * LG_PITCH);
 #pragma unroll
@@ -299,7 +298,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
       for (int kb = 0; kb < n_kb; ++kb) {
         mbar_wait(&conv[stage], phase);
         if (lane == 0) {
-          if (p.write_ws) {
+          if (WS) {
             tma_store_2d(&tmWs, smem + stage * LG_STAGE + LG_A_BYTES + LG_WS_OFF, kb * LG_BK, t * 128);
             bulk_commit();
             bulk_wait_read0();                      // smem read back: the stage may be refilled
@@ -460,12 +459,15 @@ bool logits_gather_supported(const Sizes& sz) {
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __half* Xh,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
                             MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s) {
+  // WS: the bf16 W_s copy is stored (the separate dX GEMM needs it; the fused dW/dX kernel does not)
+  using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, LgParams);
+  static const KernT kerns[8] = {k_logits_gather<false, false, false>, k_logits_gather<false, false, true>,
+                                 k_logits_gather<false, true, false>,  k_logits_gather<false, true, true>,
+                                 k_logits_gather<true, false, false>,  k_logits_gather<true, false, true>,
+                                 k_logits_gather<true, true, false>,   k_logits_gather<true, true, true>};
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_logits_gather<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
-    cudaFuncSetAttribute(k_logits_gather<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
-    cudaFuncSetAttribute(k_logits_gather<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
-    cudaFuncSetAttribute(k_logits_gather<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
+    for (KernT k : kerns) cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, LG_SMEM);
     attr = true;
   }
   const CUtensorMap a = make_map(Xh, sz.M_pad, sz.d, 64, 128);   // fp16 X_hat (R27)
@@ -478,13 +480,10 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   p.M = sz.M; p.ldm = sz.M_pad; p.d = sz.d; p.st = st; p.W = W; p.idx = idx; p.inv_norm = inv_norm; p.err = err;
   p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
-  p.write_ws = write_ws ? 1 : 0;
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
   // G4 (PFC_LG_G4=1): the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity holds, measured
   // 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
-  auto kern = eform ? (g4 ? k_logits_gather<true, true> : k_logits_gather<true, false>)
-                    : (g4 ? k_logits_gather<false, true> : k_logits_gather<false, false>);
-  kern<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
+  kerns[(eform ? 4 : 0) + (g4 ? 2 : 0) + (write_ws ? 1 : 0)]<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
   return 1;
 }
 
