@@ -41,8 +41,10 @@ lines = [f"# ncu launch list summary of {src} (workload {workload}, {ngpu} GPU):
 traffic = {}
 for name, a in sorted(agg.items(), key=lambda kv: -kv[1][1]):
     lines.append(f"{name}, {a[0]}, {a[1]/a[0]:.1f}, {a[1]/tot:.3f}, {a[2]/a[0]/1e6:.1f}, {a[3]/a[0]/1e6:.1f}")
-    if name in sec:
-        traffic[sec[name]] = round((a[2] + a[3]) / a[0])
+    base = {'k_logits_gather': 'gather_logits', 'k_dwx_t': 'dwx_sgd', 'k_dwx_ring': 'dwx_sgd',
+            'k_logits_pair': 'logits_gemm', 'k_dw_sgd_pairx': 'dw_gemm_sgd'}.get(name.split('<')[0])
+    if name in sec or base:
+        traffic[sec.get(name, base)] = round((a[2] + a[3]) / a[0])
 open(out, 'w').write("\n".join(lines) + "\n")
 tp = 'profiles/ncu_traffic.json'
 try:
