@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
           if (rid[i] >= 0)
-            asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst0 + 2 * i * LG_PITCH),
+            asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst0 + 2 * i * LG_PITCH),
                          "l"(srcc + (int64_t)rid[i] * p.d)
                          : "memory");
         }
