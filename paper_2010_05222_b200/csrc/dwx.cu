@@ -911,6 +911,8 @@ __global__ void __launch_bounds__(EF ? RG_THREADS_EF : RG_THREADS, 1)
 // P.n > 0 (fused reduce-scatter): each row goes straight into its owner's xdx slot `rank`
 __global__ void k_ws_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
                             const float* __restrict__ f, float* __restrict__ out, Peers P, int B) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
@@ -1025,7 +1027,7 @@ int launch_dwx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* 
   const int64_t n = (int64_t)sz.M * sz.d;
   Peers q{};
   if (P) q = *P;
-  k_ws_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh, q,
+  launch_pdl(k_ws_reduce, dim3((unsigned)((n / 4 + 255) / 256)), dim3(256), 0, s, n, p.gper, n, sz.d, ws, ef ? ef->f : nullptr, dXh, q,
                                                               sz.B);
   return 2;
 }

@@ -21,6 +21,8 @@ __global__ void k_eform_prep(int M, int ldm, int d, const float* __restrict__ X3
                              const float* __restrict__ ct, MarginParams mp, float* __restrict__ f,
                              __nv_bfloat16* __restrict__ Xt, __nv_bfloat16* __restrict__ E, float* __restrict__ dcorr,
                              const float* __restrict__ mvalid) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int n = blockIdx.x;
   if (n >= M) return;
   const float gs = mp.s / *mvalid;   // the mean runs over the rows not ignored (finalize; = M without ignore_index)
@@ -97,7 +99,7 @@ int launch_eform_prep(const Sizes& sz, const float* X32, const float* lse, const
                       const float* ct, MarginParams mp, float* f, __nv_bfloat16* Xt, __nv_bfloat16* E, float* dcorr,
                       const float* mvalid, cudaStream_t s) {
   cudaMemsetAsync(dcorr, 0, (size_t)sz.k_pad * sizeof(float), s);
-  k_eform_prep<<<sz.M, 128, 0, s>>>(sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr, mvalid);
+  launch_pdl(k_eform_prep, dim3(sz.M), dim3(128), 0, s, sz.M, (int)sz.M_pad, sz.d, X32, lse, gt, tcol, ct, mp, f, Xt, E, dcorr, mvalid);
   return 1;
 }
 

@@ -150,6 +150,8 @@ struct Work {
 template <int KIND_>
 __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
     k_tc_gemm(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, TcParams p) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   constexpr int KIND = base_kind(KIND_);
   using C = Cfg<KIND_>;
   using S = Smem<KIND_>;
@@ -558,6 +560,8 @@ __global__ void __launch_bounds__(Smem<KIND_>::THREADS, 1)
 // P.n > 0 (fused reduce-scatter): each row goes straight into its owner's xdx slot `rank`
 __global__ void k_splitk_reduce(int64_t n, int nsplit, int64_t stride, int d, const float* __restrict__ ws,
                                 const float* __restrict__ rowscale, float* __restrict__ out, Peers P, int B) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   int64_t i = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (i >= n) return;
   float4 acc = *reinterpret_cast<const float4*>(ws + i);
@@ -579,7 +583,7 @@ void launch(const CUtensorMap& a, const CUtensorMap& b, const TcParams& p, int g
     cudaFuncSetAttribute(k_tc_gemm<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, Smem<KIND>::TOTAL);
     attr = true;
   }
-  k_tc_gemm<KIND><<<grid, Smem<KIND>::THREADS, Smem<KIND>::TOTAL, s>>>(a, b, p);
+  launch_pdl(k_tc_gemm<KIND>, dim3(grid), dim3(Smem<KIND>::THREADS), Smem<KIND>::TOTAL, s, a, b, p);
 }
 
 }  // namespace
@@ -644,7 +648,7 @@ int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* W
   const int64_t n = (int64_t)sz.M * sz.d;
   Peers q{};
   if (P) q = *P;
-  k_splitk_reduce<<<(unsigned)((n / 4 + 255) / 256), 256, 0, s>>>(n, nsplit, n, sz.d, split_ws, rowscale, dXh, q,
+  launch_pdl(k_splitk_reduce, dim3((unsigned)((n / 4 + 255) / 256)), dim3(256), 0, s, n, nsplit, n, sz.d, split_ws, rowscale, dXh, q,
                                                                   sz.B);
   return 2;
 }

@@ -57,6 +57,8 @@ struct L2Params {
 template <bool EF, bool ARES>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     k_logits_pair(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, L2Params p) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   constexpr int NST = ARES ? L2R_STAGES : L2_STAGES;               // ring stages
@@ -319,13 +321,13 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
     const int64_t nt = sz.k_pad / 256;
     const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / mt, nt));
     const int pairs = groups * mt;
-    if (eform) k_logits_pair<true, true><<<2 * pairs, L2_THREADS, L2R_SMEM, s>>>(a, b, p);
-    else k_logits_pair<false, true><<<2 * pairs, L2_THREADS, L2R_SMEM, s>>>(a, b, p);
+    if (eform) launch_pdl(k_logits_pair<true, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
+    else launch_pdl(k_logits_pair<false, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
   } else {
     const int64_t units = (int64_t)mt * (sz.k_pad / 256);
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, max_pairs));
-    if (eform) k_logits_pair<true, false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
-    else k_logits_pair<false, false><<<2 * pairs, L2_THREADS, L2_SMEM, s>>>(a, b, p);
+    if (eform) launch_pdl(k_logits_pair<true, false>, dim3(2 * pairs), dim3(L2_THREADS), L2_SMEM, s, a, b, p);
+    else launch_pdl(k_logits_pair<false, false>, dim3(2 * pairs), dim3(L2_THREADS), L2_SMEM, s, a, b, p);
   }
   return 1;
 }

@@ -76,6 +76,8 @@ template <bool EF, bool G4, bool WS>
 __global__ void __launch_bounds__(LG_THREADS, 1)
     k_logits_gather(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmWs,
                     const __grid_constant__ CUtensorMap tmW, LgParams p) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* aux = smem + LG_STAGES * LG_STAGE;
@@ -483,7 +485,7 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
   // G4 (PFC_LG_G4=1): the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity holds, measured
   // 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
-  kerns[(eform ? 4 : 0) + (g4 ? 2 : 0) + (write_ws ? 1 : 0)]<<<grid, LG_THREADS, LG_SMEM, s>>>(a, ws, wm, p);
+  launch_pdl(kerns[(eform ? 4 : 0) + (g4 ? 2 : 0) + (write_ws ? 1 : 0)], dim3(grid), dim3(LG_THREADS), LG_SMEM, s, a, ws, wm, p);
   return 1;
 }
 

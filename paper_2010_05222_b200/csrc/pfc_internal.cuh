@@ -8,6 +8,7 @@
 #include <stdint.h>
 #include <cstdlib>
 #include <string>
+#include <utility>
 
 #include "../../include/pfc.h"
 
@@ -28,6 +29,29 @@ namespace pfc {
 inline int env_int(const char* name, int def) {
   const char* e = std::getenv(name);
   return e && *e ? std::atoi(e) : def;
+}
+
+// Programmatic dependent launch (sm_90+): a kernel launched with launch_pdl may be scheduled while its stream
+// predecessor is still running; its first statement is pdl_wait(), which returns once the predecessor grid has
+// completed and its memory is visible (transitively every earlier kernel), and pdl_trigger() lets the kernel's own
+// dependents be scheduled as its CTAs retire. Both are no-ops for a normally launched kernel. PFC_PDL=0 launches
+// everything without the attribute.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t lc{};
+  lc.gridDim = grid;
+  lc.blockDim = block;
+  lc.dynamicSmemBytes = smem;
+  lc.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  lc.attrs = at;
+  lc.numAttrs = env_int("PFC_PDL", 1) != 0 ? 1 : 0;
+  return cudaLaunchKernelEx(&lc, kern, std::forward<Args>(args)...);
 }
 
 // Sticky device error bits (reported as pfc_status by the next synchronising call).

@@ -20,6 +20,8 @@ __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __
                               const int64_t* __restrict__ labels, float* __restrict__ xh_local,
                               float* __restrict__ xnorm, float* __restrict__ X32, int64_t* __restrict__ Y, int* err,
                               Peers P, int ignore) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= B) return;
   const float* xr = x + (int64_t)warp * d;
@@ -51,6 +53,8 @@ __global__ void k_normalize_x(int B, int d, int rank, int64_t C, const float* __
 // sit in [-1, 1], where fp16's 11-bit significand is 8x finer than bf16's)
 __global__ void k_x_to_bf16(int64_t n, const float* __restrict__ X32, __nv_bfloat16* __restrict__ Xb,
                             __half* __restrict__ Xh16) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) {
     const float v = X32[i];
@@ -64,6 +68,8 @@ template <bool BF16>
 __global__ void k_gather_w(int64_t k_pad, int d, const float* __restrict__ W, const int32_t* __restrict__ idx,
                            const SamplerState* st, void* __restrict__ Ws, __half* __restrict__ Ws16,
                            float* __restrict__ inv_norm, int* err) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= k_pad) return;
@@ -134,6 +140,8 @@ __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const flo
                              const int32_t* __restrict__ idx, const SamplerState* st,
                              const int* __restrict__ sel_off, int ntiles, int32_t* __restrict__ tcol,
                              float* __restrict__ ct) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= M) return;
   const int64_t j = Y[n] - a;
@@ -170,6 +178,8 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
                                                      const SamplerState* st, MarginParams mp,
                                                      float* __restrict__ rowmax, float* __restrict__ rowsum,
                                                      float* __restrict__ zt, Peers P) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   __shared__ float sm[8], ss[8];
   const int n = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -224,6 +234,8 @@ __global__ void __launch_bounds__(1024) k_prep_sum(int M, int64_t a, int64_t C_l
                                                    const float* __restrict__ zt, const int32_t* __restrict__ tcol,
                                                    const int64_t* __restrict__ Y, const float* __restrict__ ct,
                                                    float* __restrict__ red, Peers P) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   __shared__ float sh[32];
   float acc = 0.f;
   const int64_t ld = 3 * (int64_t)M + 1;
@@ -264,6 +276,8 @@ __global__ void __launch_bounds__(1024) k_finalize(int M, const float* __restric
                                                    float* __restrict__ lse, float* __restrict__ gt,
                                                    float* __restrict__ loss_out, float* __restrict__ metrics, int* err,
                                                    Peers P, const int64_t* __restrict__ Y, int ignore) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   __shared__ float sh[32];
   __shared__ int shn[32];
   float acc = 0.f;
@@ -505,6 +519,8 @@ __global__ void k_softmax_grad_targets(int M, int ldm, const void* __restrict__ 
 // reduction, Alg.1 L12-13).
 __global__ void k_xnorm_backward(int B, int d, const float* __restrict__ dxh, const float* __restrict__ xh,
                                  const float* __restrict__ xnorm, float* __restrict__ gx, Peers P) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   const int n = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (n >= B) return;
   const float* xr = xh + (int64_t)n * d;
@@ -595,28 +611,28 @@ SymLayout sym_layout(const Sizes& sz) {
 
 int launch_normalize_x(const Sizes& sz, const float* x, const int64_t* labels, float* xh_local, float* xnorm,
                        float* X32, int64_t* Y, int* err, const Peers* P, int ignore, cudaStream_t s) {
-  k_normalize_x<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, sz.rank, sz.C, x, labels, xh_local, xnorm, X32, Y,
+  launch_pdl(k_normalize_x, dim3((sz.B * 32 + 255) / 256), dim3(256), 0, s, sz.B, sz.d, sz.rank, sz.C, x, labels, xh_local, xnorm, X32, Y,
                                                         err, none_or(P), ignore);
   return 1;
 }
 
 int launch_x_to_bf16(const Sizes& sz, const float* X32, __nv_bfloat16* Xb, __half* Xh16, cudaStream_t s) {
   int64_t n = (int64_t)sz.M * sz.d;
-  k_x_to_bf16<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, X32, Xb, Xh16);
+  launch_pdl(k_x_to_bf16, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, s, n, X32, Xb, Xh16);
   return 1;
 }
 
 int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* idx, const SamplerState* st, void* Ws,
                     __half* Ws16, float* inv_norm, int* err, cudaStream_t s) {
   unsigned grid = (unsigned)((sz.k_pad * 32 + 255) / 256);
-  if (bf16) k_gather_w<true><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, Ws16, inv_norm, err);
-  else k_gather_w<false><<<grid, 256, 0, s>>>(sz.k_pad, sz.d, W, idx, st, Ws, nullptr, inv_norm, err);
+  if (bf16) launch_pdl(k_gather_w<true>, dim3(grid), dim3(256), 0, s, sz.k_pad, sz.d, W, idx, st, Ws, Ws16, inv_norm, err);
+  else launch_pdl(k_gather_w<false>, dim3(grid), dim3(256), 0, s, sz.k_pad, sz.d, W, idx, st, Ws, nullptr, inv_norm, err);
   return 1;
 }
 
 int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
                       const SamplerState* st, const int* tile_cnt, int32_t* tcol, float* ct, cudaStream_t s) {
-  k_target_cos<<<(sz.M * 32 + 255) / 256, 256, 0, s>>>(sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, idx, st,
+  launch_pdl(k_target_cos, dim3((sz.M * 32 + 255) / 256), dim3(256), 0, s, sz.M, sz.d, sz.a, sz.C_local, X32, W, Y, idx, st,
                                                        tile_cnt + 3 * sz.ntiles_sel, sz.ntiles_sel, tcol, ct);
   return 1;
 }
@@ -624,20 +640,20 @@ int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const i
 int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, const Peers* P,
                        cudaStream_t s) {
-  k_row_combine<<<sz.M, 256, 0, s>>>(sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
+  launch_pdl(k_row_combine, dim3(sz.M), dim3(256), 0, s, sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
                                      rowsum, zt, none_or(P));
   return 1;
 }
 
 int launch_prep_sum(const Sizes& sz, const float* rowmax, float* gmax, const float* rowsum, const float* zt,
                     const int32_t* tcol, const int64_t* Y, const float* ct, float* red, const Peers* P, cudaStream_t s) {
-  k_prep_sum<<<1, 1024, 0, s>>>(sz.M, sz.a, sz.C_local, rowmax, gmax, rowsum, zt, tcol, Y, ct, red, none_or(P));
+  launch_pdl(k_prep_sum, dim3(1), dim3(1024), 0, s, sz.M, sz.a, sz.C_local, rowmax, gmax, rowsum, zt, tcol, Y, ct, red, none_or(P));
   return 1;
 }
 
 int launch_finalize(const Sizes& sz, const float* gmax, const float* red, float* lse, float* gt, float* loss_out,
                     float* metrics, int* err, const Peers* P, const int64_t* Y, int ignore, cudaStream_t s) {
-  k_finalize<<<1, 1024, 0, s>>>(sz.M, gmax, red, lse, gt, loss_out, metrics, err, none_or(P), Y, ignore);
+  launch_pdl(k_finalize, dim3(1), dim3(1024), 0, s, sz.M, gmax, red, lse, gt, loss_out, metrics, err, none_or(P), Y, ignore);
   return 1;
 }
 
@@ -690,7 +706,7 @@ int launch_softmax_grad(const Sizes& sz, bool bf16, const void* cosv, const floa
 
 int launch_xnorm_backward(const Sizes& sz, const float* dxh, const float* xh_local, const float* xnorm, float* grad_x,
                           const Peers* P, cudaStream_t s) {
-  k_xnorm_backward<<<(sz.B * 32 + 255) / 256, 256, 0, s>>>(sz.B, sz.d, dxh, xh_local, xnorm, grad_x, none_or(P));
+  launch_pdl(k_xnorm_backward, dim3((sz.B * 32 + 255) / 256), dim3(256), 0, s, sz.B, sz.d, dxh, xh_local, xnorm, grad_x, none_or(P));
   return 1;
 }
 
@@ -736,10 +752,14 @@ __global__ void k_iota(int32_t* out, int64_t n, int32_t base) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) out[i] = base + (int32_t)i;
 }
-__global__ void k_set_f32(float* dst, float v) { *dst = v; }
+__global__ void k_set_f32(float* dst, float v) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  pdl_trigger(); *dst = v; }
 // end of a step: advance the device step counter and publish the sticky device error word to the host-mapped word
 // (plain store into page-locked memory; the host reads it at the next hot-path call without synchronising)
 __global__ void k_end_step(uint64_t* dst, uint64_t v, const int* err, volatile int* err_host) {
+  pdl_wait();      // programmatic dependent launch: the predecessor kernel has completed
+  // (no early trigger: the dependents launch as this grid completes)
   *dst += v;
   if (err_host) *err_host = *err;
 }
@@ -759,12 +779,12 @@ int launch_iota(int32_t* out, int64_t n, int32_t base) {
 }
 
 int launch_set_scalar(float* dst, float v, cudaStream_t s) {
-  k_set_f32<<<1, 1, 0, s>>>(dst, v);
+  launch_pdl(k_set_f32, dim3(1), dim3(1), 0, s, dst, v);
   return 1;
 }
 
 int launch_advance_step(uint64_t* step_dev, const int* err_dev, int* err_host_mapped, cudaStream_t s) {
-  k_end_step<<<1, 1, 0, s>>>(step_dev, 1, err_dev, err_host_mapped);
+  launch_pdl(k_end_step, dim3(1), dim3(1), 0, s, step_dev, 1, err_dev, err_host_mapped);
   return 1;
 }
 
