@@ -602,6 +602,34 @@ def test_host_async_entry_matches_sync_entry():
     b.close()
 
 
+@pytest.mark.parametrize("B", [64, 320], ids=["fused-M64", "pair-M320"])
+def test_programmatic_dependent_launch_is_bit_identical(B, monkeypatch):
+    """PFC_PDL=1 (the default: the step's non-cooperative kernels launched with programmatic stream serialisation,
+    each opening with griddepcontrol.wait) and PFC_PDL=0 (plain launches) give bit-identical steps, eager and
+    graph-replayed: the attribute may only move launches earlier, never let a kernel read unfinished data."""
+    C, d = 30000, 256
+    outs = []
+    for pdl in ("0", "1"):
+        monkeypatch.setenv("PFC_PDL", pdl)
+        layer = make_layer(C, d, B, 0.1, "arcface", 0.5, "bf16", seed=5)
+        s = torch.cuda.Stream()
+        res = []
+        with torch.cuda.stream(s):
+            for i in range(4):
+                x = torch.from_numpy(synth.make_features(8, i, 1, B, d)[0]).cuda()
+                y = torch.from_numpy(synth.make_labels(8, i, 1, B, C)[0]).cuda()
+                gx, loss = torch.empty_like(x), torch.zeros(1, device="cuda")
+                layer.train_step(x, y, gx, loss, lr=0.05, stream=s)
+                s.synchronize()
+                res.append((loss.item(), gx.cpu()))
+        W, V = layer.params()
+        outs.append((res, W.cpu(), V.cpu()))
+        layer.close()
+    for (l0, g0), (l1, g1) in zip(outs[0][0], outs[1][0]):
+        assert l0 == l1 and torch.equal(g0, g1)
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
+
+
 def test_device_errors_are_reported():
     C, d, B = 1000, 128, 8
     layer = make_layer(C, d, B, 0.1, "arcface", 0.5, "fp32")
