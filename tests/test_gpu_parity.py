@@ -401,18 +401,19 @@ def test_eform_scale_range(B, scale):
         check("bf16", L, Lr, gx, gxr, Vn=Vn, Vnr=Vnr)
 
 
-@pytest.mark.parametrize("cfg", ["c4", "c4rank", "c4rank-cosface-trained"])
+@pytest.mark.parametrize("cfg", ["c4", "c4-trained", "c4rank", "c4rank-cosface-trained"])
 def test_full_size_bench_workloads(cfg):
     """The bench's own workloads at full size, in the launch configuration bench.py times (bf16 fused train step):
     C4 on one GPU (10M classes, B = 256, k = 1M: fused gather + logits and dW + SGD + dX kernels, E-form) and the
     per-rank shape of the 8-GPU C4 job (1.25M classes, M = 2048: CTA-pair kernels, radial-dot pass). One step
     against the float64 oracle: sampled ids bit-exact, loss, grad_x, and the updated W / V of every sampled row."""
     case = {"c4": (10_000_000, 512, 256, 0.1, "arcface", 0.5, "init", 0.0),
+            "c4-trained": (10_000_000, 512, 256, 0.1, "arcface", 0.5, "trained", 0.055),
             "c4rank": (1_250_000, 512, 2048, 0.1, "arcface", 0.5, "init", 0.0),
             # the same kernels with the CosFace margin and trained-like features (target cosines near 1)
             "c4rank-cosface-trained": (1_250_000, 512, 2048, 0.1, "cosface", 0.35, "trained", 0.055)}[cfg]
     probe = make_layer(case[0], 512, case[2], 0.1, case[4], case[5], "bf16")
-    assert probe.path_flags() == (15 if cfg == "c4" else 9)
+    assert probe.path_flags() == (15 if cfg.startswith("c4-") or cfg == "c4" else 9)
     probe.close()
     torch.cuda.empty_cache()
     for (L, Lr, gx, gxr, _, _, Wn, Wnr, Vn, Vnr) in _run_single(case, "bf16", steps=1, fused=True):
