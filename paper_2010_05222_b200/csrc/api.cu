@@ -629,13 +629,14 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
     n += launch_gather_w(sz, bf, c->Wk(), c->idxk(), c->st, c->Ws, c->Ws16, c->inv_norm, c->err_dev, s);
   n += launch_target_cos(sz, c->X32, c->W, c->Y, c->idx, c->st, c->tile_cnt, c->tcol, c->ct, s);
   mark(c, 3, s);
+  int nparts = 0;   // per-row LSE partials the logits kernel leaves (0: one per 128-column tile)
   if (c->fused_gather)
     n += launch_logits_gather_tc(sz, c->Wk(), c->idxk(), c->Xh16, (__nv_bfloat16*)c->Ws, !(fused && c->use_dwx), c->inv_norm,
                                  c->tcol, c->st, c->mp, (__half*)c->cosv, c->partials, c->err_dev,
-                                 fused && c->eform, s);
+                                 fused && c->eform, &nparts, s);
   else if (c->use_tc && logits_pair_enabled(sz))
     n += launch_logits_pair_tc(sz, c->Xh16, c->Ws16, c->tcol, c->st, c->mp, (__half*)c->cosv,
-                               c->partials, fused && c->eform_pair, s);
+                               c->partials, fused && c->eform_pair, &nparts, s);
   else if (c->use_tc)
     n += launch_logits_tc(sz, c->Xh16, c->Ws16, c->tcol, c->ct, c->st, c->mp, (__half*)c->cosv,
                           c->partials, s);
@@ -643,7 +644,7 @@ void phase_b(pfc_ctx* c, bool fused, cudaStream_t s) {
     n += launch_logits_simt(sz, bf, bf ? (const void*)c->Xb : (const void*)c->X32, c->Ws, c->tcol, c->ct, c->st, c->mp,
                             c->cosv, c->partials, s);
   mark(c, 4, s);
-  n += launch_row_combine(sz, c->partials, c->Y, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, c->P(), s);
+  n += launch_row_combine(sz, c->partials, nparts, c->Y, c->ct, c->st, c->mp, c->rowmax, c->rowsum, c->zt, c->P(), s);
   c->launches += n;
 }
 

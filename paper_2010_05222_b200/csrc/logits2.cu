@@ -182,6 +182,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     const uint32_t acc_empty_leader = leader_addr(&acc_empty[0]);
     int acc = 0;
     uint32_t acc_phase = 0;
+    // ARES: this thread's row is fixed for the whole kernel, so the (max, sum) of its 128-column half of every class
+    // tile the pair takes are folded here, in the pair's fixed tile order, and one partial per (row, group, half)
+    // is stored at the end: 2 G partials per row instead of k / 128 scattered 8-byte stores (which cost a DRAM
+    // read-modify-write per store once the partials outgrow L2, 2.3 GB per launch at the 12.5M-class shard)
+    float racc_m = -INFINITY, racc_l = 0.f;
     for (int it = 0; it < n_iter; ++it) {
       int m0, n0;
       unit(it, m0, n0);
@@ -274,11 +279,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         float l = 0.f;
         if (m > -INFINITY)
           l = (mx > -INFINITY ? sum * ex2_ftz((mx - m) * sl) : 0.f) + (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
-        if (rv)
+        if (ARES) {
+          const float nm = fmaxf(racc_m, m);
+          if (nm > -INFINITY) {
+            racc_l = (racc_m > -INFINITY ? racc_l * ex2_ftz((racc_m - nm) * sl) : 0.f) +
+                     (m > -INFINITY ? l * ex2_ftz((m - nm) * sl) : 0.f);
+            racc_m = nm;
+          }
+        } else if (rv) {
           p.partials[(int64_t)row * p.n_ltiles + n0 / 128 + (eset >> 1)] =
               make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
+        }
       }
       if (++acc == L2_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+    if (ARES && !(eset & 1)) {   // slot 2 g + half of this row (every group has at least one class tile)
+      const int row = (pair % mt) * 256 + 128 * (int)rank + row_in;
+      if (row < p.M)
+        p.partials[(int64_t)row * p.n_ltiles + 2 * (pair / mt) + (eset >> 1)] =
+            make_float2(racc_m > -INFINITY ? racc_m * p.scale : -INFINITY, racc_l);
     }
   }
   tc_fence_before();
@@ -298,7 +317,7 @@ bool logits_pair_enabled(const Sizes& sz) {
 
 int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, const int32_t* tcol,
                           const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
-                          cudaStream_t s) {
+                          int* nparts, cudaStream_t s) {
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_logits_pair<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, L2_SMEM);
@@ -321,9 +340,11 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
     const int64_t nt = sz.k_pad / 256;
     const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / mt, nt));
     const int pairs = groups * mt;
+    *nparts = 2 * groups;   // per-row partials folded per group (ARES epilogue)
     if (eform) launch_pdl(k_logits_pair<true, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
     else launch_pdl(k_logits_pair<false, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
   } else {
+    *nparts = 0;            // one partial per 128-column tile
     const int64_t units = (int64_t)mt * (sz.k_pad / 256);
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, max_pairs));
     if (eform) launch_pdl(k_logits_pair<true, false>, dim3(2 * pairs), dim3(L2_THREADS), L2_SMEM, s, a, b, p);

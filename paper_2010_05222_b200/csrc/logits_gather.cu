@@ -321,6 +321,9 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
     const float sl = p.s_log2e;
     int acc = 0;
     uint32_t acc_phase = 0;
+    // the (max, sum) of this thread's rows over every class tile of this CTA, folded in the CTA's fixed tile order:
+    // one partial per (row, CTA) at the end instead of k / 128 (row_combine reads gridDim.x slots per row)
+    float racc_m[2] = {-INFINITY, -INFINITY}, racc_l[2] = {0.f, 0.f};
     for (int t = blockIdx.x; t < nt; t += gridDim.x) {
       const int n0 = t * 128;
       mbar_wait(&inv_full[acc], acc_phase);
@@ -437,11 +440,25 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
           if (m > -INFINITY)
             l = (pm[ms] > -INFINITY ? ps[ms] * ex2_ftz((pm[ms] - m) * sl) : 0.f) +
                 (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
-          if (row < p.M)
-            p.partials[(int64_t)row * p.n_ltiles + t] = make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
+          (void)row;
+          const float nm = fmaxf(racc_m[ms], m);
+          if (nm > -INFINITY) {
+            racc_l[ms] = (racc_m[ms] > -INFINITY ? racc_l[ms] * ex2_ftz((racc_m[ms] - nm) * sl) : 0.f) +
+                         (m > -INFINITY ? l * ex2_ftz((m - nm) * sl) : 0.f);
+            racc_m[ms] = nm;
+          }
         }
       }
       if (++acc == LG_ACC) { acc = 0; acc_phase ^= 1; }
+    }
+    if (eset == 0) {   // slot blockIdx.x of each row (written also when this CTA had no tile: -inf, 0)
+#pragma unroll
+      for (int ms = 0; ms < 2; ++ms) {
+        const int row = ms * 128 + row_in;
+        if (row < p.M)
+          p.partials[(int64_t)row * p.n_ltiles + blockIdx.x] =
+              make_float2(racc_m[ms] > -INFINITY ? racc_m[ms] * p.scale : -INFINITY, racc_l[ms]);
+      }
     }
   }
   __syncthreads();
@@ -460,7 +477,8 @@ bool logits_gather_supported(const Sizes& sz) {
 
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __half* Xh,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
-                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s) {
+                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, int* nparts,
+                            cudaStream_t s) {
   // WS: the bf16 W_s copy is stored (the separate dX GEMM needs it; the fused dW/dX kernel does not)
   using KernT = void (*)(const CUtensorMap, const CUtensorMap, const CUtensorMap, LgParams);
   static const KernT kerns[8] = {k_logits_gather<false, false, false>, k_logits_gather<false, false, true>,
@@ -483,6 +501,7 @@ int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx,
   p.tcol = tcol; p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
   const int grid = (int)std::min<int64_t>(sz.k_pad / 128, num_sms());
+  *nparts = grid;   // one folded LSE partial per (row, CTA)
   // G4 (PFC_LG_G4=1): the W rows by TMA tile::gather4 (128-byte swizzled 32-column boxes); parity holds, measured
   // 2x slower at C4 (1.07 vs 0.55 ms: ~19 cycles of TMA per 128-byte row)
   launch_pdl(kerns[(eform ? 4 : 0) + (g4 ? 2 : 0) + (write_ws ? 1 : 0)], dim3(grid), dim3(LG_THREADS), LG_SMEM, s, a, ws, wm, p);

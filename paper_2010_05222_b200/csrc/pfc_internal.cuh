@@ -192,7 +192,9 @@ int launch_gather_w(const Sizes& sz, bool bf16, const float* W, const int32_t* i
 int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const int64_t* Y, const int32_t* idx,
                       const SamplerState* st, const int* tile_cnt /* sampler K4 tile offsets */, int32_t* tcol,
                       float* ct, cudaStream_t s);
-int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
+// nparts > 0: the logits kernel folded its per-row partials into the first nparts slots of each row (else one
+// partial per 128-column tile up to k_i)
+int launch_row_combine(const Sizes& sz, const float2* partials, int nparts, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, const Peers* P,
                        cudaStream_t s);
 // fused (P): gmax is computed here from the peers' xmax slots (max in rank order) and written
@@ -251,12 +253,13 @@ int launch_logits_tc(const Sizes& sz, const __half* Xh, const __half* Ws16, cons
 bool logits_gather_supported(const Sizes& sz);
 int launch_logits_gather_tc(const Sizes& sz, const float* W, const int32_t* idx, const __half* Xh16,
                             __nv_bfloat16* Ws, bool write_ws, float* inv_norm, const int32_t* tcol, const SamplerState* st,
-                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, cudaStream_t s);
+                            MarginParams mp, __half* cosv, float2* partials, int* err, bool eform, int* nparts,
+                            cudaStream_t s);
 // logits2.cu — K6 on CTA pairs (tcgen05 cta_group::2, 256 x 256 tiles) for M > 256
 bool logits_pair_enabled(const Sizes& sz);
 int launch_logits_pair_tc(const Sizes& sz, const __half* Xh16, const __half* Ws16, const int32_t* tcol,
                           const SamplerState* st, MarginParams mp, __half* cosv, float2* partials, bool eform,
-                          cudaStream_t s);
+                          int* nparts, cudaStream_t s);
 // dX_hat = G W_s (split-K + fixed-order reduction); rowscale (E-form f_n, or NULL) multiplies each output row
 // P: the split-K reduction stores each owner's rows straight into its xdx slot (fused reduce-scatter)
 int launch_dx_tc(const Sizes& sz, const __nv_bfloat16* G, const __nv_bfloat16* Ws, const SamplerState* st,

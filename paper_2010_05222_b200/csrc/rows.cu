@@ -172,8 +172,8 @@ __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const flo
 
 // ---------------------------------------------------------------- K7: one 256-thread block per batch row
 // (the row's ~k/128 tile partials are spread over the block; two-level max then rescaled sum)
-__global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltile, int64_t a, int64_t C_local,
-                                                     const float2* __restrict__ partials,
+__global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltile, int nparts, int64_t a,
+                                                     int64_t C_local, const float2* __restrict__ partials,
                                                      const int64_t* __restrict__ Y, const float* __restrict__ ct,
                                                      const SamplerState* st, MarginParams mp,
                                                      float* __restrict__ rowmax, float* __restrict__ rowsum,
@@ -184,7 +184,8 @@ __global__ void __launch_bounds__(256) k_row_combine(int M, int ntiles, int ltil
   const int n = blockIdx.x;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const float2* pr = partials + (int64_t)n * ntiles;
-  const int nvalid = min(ntiles, (st->k + ltile - 1) / ltile);   // tiles past k_i are never written
+  // tiles past k_i are never written; nparts > 0: the logits kernel folded each row into its first nparts slots
+  const int nvalid = nparts > 0 ? min(ntiles, nparts) : min(ntiles, (st->k + ltile - 1) / ltile);
   // online (max, sum) per thread, four independent accumulators (loads in flight together)
   float mq[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY}, lq[4] = {0.f, 0.f, 0.f, 0.f};
   for (int t0 = threadIdx.x; t0 < nvalid; t0 += 4 * blockDim.x) {
@@ -637,10 +638,10 @@ int launch_target_cos(const Sizes& sz, const float* X32, const float* W, const i
   return 1;
 }
 
-int launch_row_combine(const Sizes& sz, const float2* partials, const int64_t* Y, const float* ct,
+int launch_row_combine(const Sizes& sz, const float2* partials, int nparts, const int64_t* Y, const float* ct,
                        const SamplerState* st, MarginParams mp, float* rowmax, float* rowsum, float* zt, const Peers* P,
                        cudaStream_t s) {
-  launch_pdl(k_row_combine, dim3(sz.M), dim3(256), 0, s, sz.M, sz.n_ltiles, sz.ltile, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
+  launch_pdl(k_row_combine, dim3(sz.M), dim3(256), 0, s, sz.M, sz.n_ltiles, sz.ltile, nparts, sz.a, sz.C_local, partials, Y, ct, st, mp, rowmax,
                                      rowsum, zt, none_or(P));
   return 1;
 }
