@@ -8,6 +8,7 @@
 //   K10 xnorm_backward   dx = (dx_hat - x_hat (x_hat . dx_hat)) / ||x||
 //   K12 sgd              lazy momentum SGD of the sampled rows
 #include <algorithm>
+#include <climits>
 #include "pfc_internal.cuh"
 
 namespace pfc {
@@ -149,22 +150,49 @@ __global__ void k_target_cos(int M, int d, int64_t a, int64_t C_local, const flo
     if (lane == 0) { ct[n] = 0.f; tcol[n] = -1; }
     return;
   }
-  if (lane == 0) {
-    // search only the positions of j's compaction tile: [sel_off[t], sel_off[t + 1]) (K4b exclusive scan)
-    const int t = (int)(j / kSelTile);
-    int lo = sel_off[t], hi = (t + 1 < ntiles ? sel_off[t + 1] : st->k) - 1, res = -1;
-    while (lo <= hi) {
-      const int mid = (lo + hi) >> 1;
-      const int v = idx[mid];
-      if (v == (int)j) { res = mid; break; }
-      if (v < (int)j) lo = mid + 1; else hi = mid - 1;
-    }
-    tcol[n] = res;
-  }
   const float* xr = X32 + (int64_t)n * d;
   const float* wr = W + j * d;
+  // the row's loads first (in flight during the search)
   float acc = 0.f, ss = 0.f;
-  for (int c = lane; c < d; c += 32) { const float w = wr[c]; acc += xr[c] * w; ss += w * w; }
+  if ((d & 127) == 0 && d <= 512) {
+    float4 xv[4], wv[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q * 128 < d) {
+        xv[q] = __ldg(reinterpret_cast<const float4*>(xr + q * 128 + lane * 4));
+        wv[q] = __ldg(reinterpret_cast<const float4*>(wr + q * 128 + lane * 4));
+      }
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q * 128 < d) {
+        acc += xv[q].x * wv[q].x + xv[q].y * wv[q].y + xv[q].z * wv[q].z + xv[q].w * wv[q].w;
+        ss += wv[q].x * wv[q].x + wv[q].y * wv[q].y + wv[q].z * wv[q].z + wv[q].w * wv[q].w;
+      }
+  } else {
+    for (int c = lane; c < d; c += 32) { const float w = wr[c]; acc += xr[c] * w; ss += w * w; }
+  }
+  // tcol: search only the positions of j's compaction tile, [sel_off[t], sel_off[t + 1]) (K4b exclusive scan),
+  // 32-ary with the warp (ascending ids: the lanes whose probe is <= j form a prefix)
+  {
+    const int t = (int)(j / kSelTile);
+    int lo = sel_off[t], hi = (t + 1 < ntiles ? sel_off[t + 1] : st->k) - 1, res = -1;
+    while (hi - lo + 1 > 32) {
+      const int step = (hi - lo + 1 + 31) / 32;
+      const int pos = lo + lane * step;
+      const int v = pos <= hi ? __ldg(idx + pos) : INT_MAX;
+      const unsigned le = __ballot_sync(0xffffffffu, v <= (int)j);
+      if (!le) { hi = lo - 1; break; }                 // j below the segment: not sampled
+      const int nlo = lo + (31 - __clz(le)) * step;
+      hi = min(hi, nlo + step - 1);
+      lo = nlo;
+    }
+    if (lo <= hi) {
+      const int pos = lo + lane;
+      const unsigned eq = __ballot_sync(0xffffffffu, pos <= hi && __ldg(idx + pos) == (int)j);
+      if (eq) res = lo + __ffs(eq) - 1;
+    }
+    if (lane == 0) tcol[n] = res;
+  }
   acc = warp_sum(acc);
   ss = warp_sum(ss);
   if (lane == 0) ct[n] = acc / fmaxf(sqrtf(ss), kNormEps);
