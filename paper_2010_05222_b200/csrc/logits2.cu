@@ -37,8 +37,11 @@ constexpr int L2_SMEM = L2_STAGES * L2_STAGE + 1024 + 256 + L2_PART;
 // keeps one 256-row M tile and walks class tiles), only the W_s tiles stream: half the operand traffic from L2
 constexpr int L2R_KB = 8;                               // d / 64 <= 8
 constexpr int L2R_A = L2R_KB * L2_HALF;                 // 128 KB
-constexpr int L2R_STAGES = 5;                           // B ring: 16 KB stages
-constexpr int L2R_SMEM = L2R_A + L2R_STAGES * L2_HALF + 1024 + 256 + L2_PART;
+#ifndef PFC_L2R_STAGES
+#define PFC_L2R_STAGES 6
+#endif
+constexpr int L2R_STAGES = PFC_L2R_STAGES;              // B ring: 16 KB stages (no s_part: ARES folds per thread)
+constexpr int L2R_SMEM = L2R_A + L2R_STAGES * L2_HALF + 1024 + 256;
 static_assert(L2_SMEM <= 232448 && L2R_SMEM <= 232448, "shared memory overflow");
 static_assert(L2_SMEM <= 232448, "shared memory overflow");
 struct L2Params {
@@ -186,7 +189,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
     // tile the pair takes are folded here, in the pair's fixed tile order, and one partial per (row, group, half)
     // is stored at the end: 2 G partials per row instead of k / 128 scattered 8-byte stores (which cost a DRAM
     // read-modify-write per store once the partials outgrow L2, 2.3 GB per launch at the 12.5M-class shard)
-    float racc_m = -INFINITY, racc_l = 0.f;
+    float racc_m = -INFINITY, racc_l = 0.f;   // ARES: this thread's 64-column set of every tile, folded
     for (int it = 0; it < n_iter; ++it) {
       int m0, n0;
       unit(it, m0, n0);
@@ -270,33 +273,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         if (leader) mbar_arrive(&acc_empty[acc]);
         else mbar_arrive_cluster(acc_empty_leader + acc * 8);
       }
+      if (ARES) {   // fold this thread's (max, sum) of its 64 columns; no exchange between the column sets
+        const float nm = fmaxf(racc_m, mx);
+        if (nm > -INFINITY) {
+          racc_l = (racc_m > -INFINITY ? racc_l * ex2_ftz((racc_m - nm) * sl) : 0.f) +
+                   (mx > -INFINITY ? sum * ex2_ftz((mx - nm) * sl) : 0.f);
+          racc_m = nm;
+        }
+      }
       float2* sp = s_part + acc * 256;
-      if (eset & 1) sp[(eset >> 1) * 128 + row_in] = make_float2(mx, sum);
-      asm volatile("bar.sync 4, %0;" ::"n"(32 * L2_EPI) : "memory");
-      if (!(eset & 1)) {
+      if (!ARES && (eset & 1)) sp[(eset >> 1) * 128 + row_in] = make_float2(mx, sum);
+      if (!ARES) asm volatile("bar.sync 4, %0;" ::"n"(32 * L2_EPI) : "memory");
+      if (!ARES && !(eset & 1)) {
         const float2 o = sp[(eset >> 1) * 128 + row_in];
         const float m = fmaxf(mx, o.x);
         float l = 0.f;
         if (m > -INFINITY)
           l = (mx > -INFINITY ? sum * ex2_ftz((mx - m) * sl) : 0.f) + (o.x > -INFINITY ? o.y * ex2_ftz((o.x - m) * sl) : 0.f);
-        if (ARES) {
-          const float nm = fmaxf(racc_m, m);
-          if (nm > -INFINITY) {
-            racc_l = (racc_m > -INFINITY ? racc_l * ex2_ftz((racc_m - nm) * sl) : 0.f) +
-                     (m > -INFINITY ? l * ex2_ftz((m - nm) * sl) : 0.f);
-            racc_m = nm;
-          }
-        } else if (rv) {
+        if (rv) {
           p.partials[(int64_t)row * p.n_ltiles + n0 / 128 + (eset >> 1)] =
               make_float2(m > -INFINITY ? m * p.scale : -INFINITY, l);
         }
       }
       if (++acc == L2_ACC) { acc = 0; acc_phase ^= 1; }
     }
-    if (ARES && !(eset & 1)) {   // slot 2 g + half of this row (every group has at least one class tile)
+    if (ARES) {   // slot 4 g + column set of this row (every group has at least one class tile)
       const int row = (pair % mt) * 256 + 128 * (int)rank + row_in;
       if (row < p.M)
-        p.partials[(int64_t)row * p.n_ltiles + 2 * (pair / mt) + (eset >> 1)] =
+        p.partials[(int64_t)row * p.n_ltiles + 4 * (pair / mt) + eset] =
             make_float2(racc_m > -INFINITY ? racc_m * p.scale : -INFINITY, racc_l);
     }
   }
@@ -336,11 +340,11 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
   const int mt = (int)((sz.M + 255) / 256);
   const int max_pairs = num_sms() / 2;
   const bool ares_on = env_int("PFC_LOGITS_ARES", 1) != 0;
-  if (ares_on && sz.d <= 64 * L2R_KB && mt <= max_pairs) {
-    const int64_t nt = sz.k_pad / 256;
-    const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / mt, nt));
+  const int64_t nt_all = sz.k_pad / 256;
+  const int groups = (int)std::max<int64_t>(1, std::min<int64_t>(max_pairs / std::max(1, mt), nt_all));
+  if (ares_on && sz.d <= 64 * L2R_KB && mt <= max_pairs && 4 * groups <= sz.n_ltiles) {
     const int pairs = groups * mt;
-    *nparts = 2 * groups;   // per-row partials folded per group (ARES epilogue)
+    *nparts = 4 * groups;   // per-row partials folded per group and 64-column set (ARES epilogue)
     if (eform) launch_pdl(k_logits_pair<true, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
     else launch_pdl(k_logits_pair<false, true>, dim3(2 * pairs), dim3(L2_THREADS), L2R_SMEM, s, a, b, p);
   } else {
