@@ -16,7 +16,9 @@
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "pfc_internal.cuh"
 #include "tc_common.cuh"
@@ -52,7 +54,17 @@ struct L2Params {
   __half* cosv;
   float2* partials;
   int n_ltiles;
+  unsigned long long* trace;   // diagnostic build (PFC_DWX_DIAG) with PFC_LP_TRACE=1: per CTA, summed wait times
 };
+#ifndef PFC_DWX_DIAG
+#define PFC_DWX_DIAG 0
+#endif
+constexpr bool kLpDiag = PFC_DWX_DIAG != 0;
+__device__ __forceinline__ unsigned long long lp_clock() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // EF (E-form train step, DESIGN.md f1): store E = bf16(e^{s c}) of the fp16-rounded cosine the partials use (0 at
 // the target and padding columns) instead of the cosine; the softmax-gradient pass then disappears (dX / dW
@@ -110,6 +122,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
   cluster_sync();            // barriers initialised and TMEM allocated in both CTAs before any remote traffic
   tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  const unsigned long long tk0 = (kLpDiag && p.trace) ? lp_clock() : 0ull;
 
   if (warp == 0) {
     // ---------------------------------------------------------------- producer (this CTA's halves)
@@ -152,11 +165,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
         tc_fence_after();
       }
       for (int it = 0; it < n_iter; ++it) {
+        const unsigned long long t0 = (kLpDiag && p.trace) ? lp_clock() : 0ull;
         mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+        if (kLpDiag && p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * 4 + 0, lp_clock() - t0);
         tc_fence_after();
         const uint32_t tacc = tmem_base + acc * 256;
         for (int kb = 0; kb < n_kb; ++kb) {
+          const unsigned long long t1 = (kLpDiag && p.trace) ? lp_clock() : 0ull;
           mbar_wait(&full[stage], phase);
+          if (kLpDiag && p.trace && lane == 0) atomicAdd(p.trace + blockIdx.x * 4 + 1, lp_clock() - t1);
           tc_fence_after();
           if (lane == 0) {
             const uint32_t sst = smem_u32(smem + RING0 + stage * STB);
@@ -196,7 +213,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
       const int row = m0 + 128 * (int)rank + row_in;
       const bool rv = row < p.M;
       const int tc = rv ? p.tcol[row] : -1;
+      const unsigned long long t2 = (kLpDiag && p.trace) ? lp_clock() : 0ull;
       mbar_wait(&acc_full[acc], acc_phase);
+      if (kLpDiag && p.trace && threadIdx.x == 64) atomicAdd(p.trace + blockIdx.x * 4 + 2, lp_clock() - t2);
       tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(lg * 32) << 16) + acc * 256;
       float mx = EF ? 0.f : -INFINITY, sum = 0.f;   // EF: unshifted sums (s + ln k < 80, api.cu)
@@ -304,6 +323,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(L2_THREADS, 1)
             make_float2(racc_m > -INFINITY ? racc_m * p.scale : -INFINITY, racc_l);
     }
   }
+  if (kLpDiag && p.trace && threadIdx.x == 64) p.trace[blockIdx.x * 4 + 3] = lp_clock() - tk0;
   tc_fence_before();
   cluster_sync();            // no CTA leaves while its pair may still read its shared memory or signal it
   if (warp == 1) {
@@ -337,6 +357,15 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
   p.M = sz.M; p.ldm = (int)sz.M_pad; p.d = sz.d; p.st = st; p.tcol = tcol;
   p.s_log2e = mp.s * 1.4426950408889634f; p.scale = mp.s; p.cosv = cosv; p.partials = partials;
   p.n_ltiles = sz.n_ltiles;
+  static unsigned long long* trace = nullptr;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const bool tracing = kLpDiag && env_int("PFC_LP_TRACE", 0) != 0 && cs == cudaStreamCaptureStatusNone;
+  if (tracing) {
+    if (!trace) cudaMalloc(&trace, 4 * 1024 * sizeof(unsigned long long));
+    cudaMemsetAsync(trace, 0, 4 * 1024 * sizeof(unsigned long long), s);
+    p.trace = trace;
+  }
   const int mt = (int)((sz.M + 255) / 256);
   const int max_pairs = num_sms() / 2;
   const bool ares_on = env_int("PFC_LOGITS_ARES", 1) != 0;
@@ -353,6 +382,21 @@ int launch_logits_pair_tc(const Sizes& sz, const __half* Xh, const __half* Ws, c
     const int pairs = (int)std::max<int64_t>(1, std::min<int64_t>(units, max_pairs));
     if (eform) launch_pdl(k_logits_pair<true, false>, dim3(2 * pairs), dim3(L2_THREADS), L2_SMEM, s, a, b, p);
     else launch_pdl(k_logits_pair<false, false>, dim3(2 * pairs), dim3(L2_THREADS), L2_SMEM, s, a, b, p);
+  }
+  if (tracing) {   // medians over the CTAs: MMA waits for a free accumulator / for W_s stages, epilogue waits, total
+    std::vector<unsigned long long> h(4 * 1024);
+    cudaMemcpyAsync(h.data(), trace, h.size() * 8, cudaMemcpyDeviceToHost, s);
+    cudaStreamSynchronize(s);
+    std::vector<double> v[4];
+    for (int b = 0; b < 1024; ++b)
+      if (h[b * 4 + 3])
+        for (int q = 0; q < 4; ++q)
+          if (q >= 2 || (b & 1) == 0) v[q].push_back(h[b * 4 + q] / 1e3);   // MMA waits: leader CTAs only
+    for (auto& x : v) std::sort(x.begin(), x.end());
+    if (!v[3].empty())
+      std::fprintf(stderr, "logits_pair (us, median over %zu CTAs, leader-only for the MMA waits): acc_empty %.1f  "
+                           "full %.1f  epilogue acc_full %.1f  total %.1f\n", v[3].size(), v[0][v[0].size() / 2],
+                   v[1][v[1].size() / 2], v[2][v[2].size() / 2], v[3][v[3].size() / 2]);
   }
   return 1;
 }
