@@ -369,6 +369,9 @@ def measure(cfgname, args, world, rank, local, dist, e2e=True, clocks=True):
         barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # each measured pass starts from an idle GPU (sustained load drives the B200 into its power
+        # cap within ~100 steps, which would otherwise carry over from the timed and per-kernel passes)
+        time.sleep(1.5)
         # the training-loop entry (pfc_train_step_host_async): every step's H2D copies, step and D2H copies of
         # grad_x and the loss enqueued on the stream, the host not waiting between steps
         e0.record(stream)
@@ -381,6 +384,7 @@ def measure(cfgname, args, world, rank, local, dist, e2e=True, clocks=True):
         # the synchronous entry (pfc_train_step_host: returns with grad_x and the loss in host memory)
         barrier()
         torch.cuda.synchronize()
+        time.sleep(1.5)
         e0.record(stream)
         for i in range(args.steps):
             layer.train_step_host(xh[i % NB], yh[i % NB], gh, lh, LR, stream)
