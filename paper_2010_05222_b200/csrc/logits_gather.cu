@@ -27,7 +27,11 @@ namespace {
 constexpr int LG_BK = 64;
 constexpr int LG_STAGES = 3;
 constexpr int LG_ACC = 2;
-constexpr int LG_PROD = 2;                              // producer warps (64 W rows each)
+#ifndef PFC_LG_PROD
+#define PFC_LG_PROD 2
+#endif
+constexpr int LG_PROD = PFC_LG_PROD;                    // producer warps (128 / LG_PROD W rows each; 4: no faster)
+constexpr int LG_PRW = 128 / LG_PROD;                   // rows per producer warp
 constexpr int LG_MMA_WARP = LG_PROD;
 constexpr int LG_CONV0 = LG_MMA_WARP + 1;
 constexpr int LG_CONV = 4;                              // converter warps: thread = class row of the tile
@@ -158,19 +162,19 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
   } else if (warp < LG_PROD) {
     // ---------------------------------------------------------------- producers
     // W rows: 16-byte cp.async (LDGSTS); a warp instruction moves two rows x 256 B (coalesced); warp pw owns
-    // rows 64 pw .. 64 pw + 63 of the tile, their ids held in registers for the whole tile; completion is
+    // rows LG_PRW pw .. LG_PRW (pw + 1) - 1 of the tile, their ids held in registers for the whole tile; completion is
     // tracked by the stage mbarrier (cp.async.mbarrier.arrive.noinc). X_hat by TMA. (One 256-byte
     // cp.async.bulk per row, a single producer warp reading row ids from smem, and TMA tile::gather4 of 128-byte row
     // boxes (PFC_LG_G4=1, the variant branch above) were measured slower.)
     int stage = 0;
     uint32_t phase = 0;
     const int half = lane >> 4, ch = lane & 15;
-    const int rbase = warp * 64 + half;
+    const int rbase = warp * LG_PRW + half;
     for (int t = blockIdx.x; t < nt; t += gridDim.x) {
       const int n0 = t * 128;
-      int rid[32];
+      int rid[LG_PRW / 2];
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
+      for (int i = 0; i < LG_PRW / 2; ++i) {
         const int r = n0 + rbase + 2 * i;
         rid[i] = r < k ? p.idx[r] : -1;
       }
@@ -186,7 +190,7 @@ __global__ void __launch_bounds__(LG_THREADS, 1)
         const uint32_t dst0 = smem_u32(sw) + rbase * LG_PITCH + ch * 16;
         const float* srcc = p.W + kb * LG_BK + ch * 4;
 #pragma unroll
-        for (int i = 0; i < 32; ++i) {
+        for (int i = 0; i < LG_PRW / 2; ++i) {
           if (rid[i] >= 0)
             asm volatile("cp.async.cg.shared.global.L2::256B [%0], [%1], 16;" ::"r"(dst0 + 2 * i * LG_PITCH),
                          "l"(srcc + (int64_t)rid[i] * p.d)
